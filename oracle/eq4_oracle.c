@@ -1,0 +1,426 @@
+/*
+ * eq4_oracle.c -- CPU ORACLE for the row-wise 4-bit clip-search + pack path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is a plain-C restatement of the
+ * reference package `embquant` (arXiv 1911.02079 artifact, pure Python/numpy)
+ * for the hot path named in BASELINE.json: ASYM, GREEDY and HIST-BRUTE
+ * clipping searches, the uniform codec and the packed 4-bit row layout.
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * `--impl reference` legs may load it -- as the checker or as the timed CPU
+ * baseline, never as the product path.  The product path is the CUDA
+ * library paper_1911_02079_b200/libeq4.so.
+ *
+ * Arithmetic contract (what makes this a bit-exact restatement):
+ *   - every floating-point operation is an IEEE-754 binary64 op in the same
+ *     order and association as the numpy expression it restates; the build
+ *     uses -ffp-contract=off so no mul+add is fused;
+ *   - np.sum over a contiguous float64 vector is numpy's pairwise sum
+ *     (numpy/_core/src/umath/loops_utils.h.src, PW_BLOCKSIZE=128, 8-way
+ *     unrolled leaves) added to the reduction identity 0.0;
+ *   - np.float16(x) / np.float32(x) are single round-to-nearest-even
+ *     conversions from binary64 (gcc _Float16 / (float) casts);
+ *   - x**3 on float64 arrays is libm pow(x, 3.0), as numpy's npy_pow.
+ * HIST-BRUTE's np.convolve goes through BLAS ddot in the reference, whose
+ * summation order is CPU-kernel specific; here each window norm is a plain
+ * ascending-j sum.  Its argmin agrees with the reference except at near-ties
+ * (see DESIGN.md "parity"); every other output of this file is bit-exact
+ * against the reference (pinned by tests/golden, generated from the
+ * reference itself by tests/golden/make_golden.py).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define EQO_OK 0
+#define EQO_EB 1        /* b < 1                          clipping.py:158-159, histclip.py:54-55 */
+#define EQO_ER 2        /* r not in (0, 1]                clipping.py:160-161 */
+#define EQO_EEMPTY 3    /* empty vector                   clipping.py:44-48, histclip.py:57-58 */
+#define EQO_ERANGE 4    /* ClipRange invalid (xmin>xmax)  table.py:70-74 */
+#define EQO_EFINITE 5   /* non-finite input               table.py:28-29 */
+#define EQO_ENBITS 6    /* nbits not in {4,8}             table.py:92-93 */
+#define EQO_EALLOC 7
+#define EQO_EMETHOD 8
+
+#define METHOD_ASYM 0
+#define METHOD_GREEDY 1
+#define METHOD_HIST_BRUTE 2
+
+#define DST_NBINS 16 /* histclip.py:31 */
+
+/* numpy pairwise summation (loops_utils.h.src @TYPE@_pairwise_sum). */
+static double np_pairwise_sum(const double *a, long n) {
+    if (n < 8) {
+        double res = 0.;
+        for (long i = 0; i < n; i++) res += a[i];
+        return res;
+    } else if (n <= 128) {
+        double r[8];
+        long i;
+        for (int j = 0; j < 8; j++) r[j] = a[j];
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; j++) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; i++) res += a[i];
+        return res;
+    } else {
+        long n2 = n / 2;
+        n2 -= n2 % 8;
+        return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
+    }
+}
+
+/* np.add.reduce of a 1-D float64 array: identity 0.0 plus the pairwise sum. */
+double eqo_np_sum(const double *a, long n) { return 0.0 + np_pairwise_sum(a, n); }
+
+/* np.clip(x, lo, hi) == minimum(maximum(x, lo), hi) for finite inputs. */
+static inline double np_clip(double x, double lo, double hi) {
+    double t = x > lo ? x : lo;
+    return t < hi ? t : hi;
+}
+
+/* table.py:81-103 quant_mse: float64 sum of squared reconstruction errors.
+ * scratch must hold d doubles. */
+int eqo_quant_mse(const float *xf, long d, double xmin, double xmax, int nbits,
+                  double *scratch, double *out) {
+    if (nbits != 4 && nbits != 8) return EQO_ENBITS;             /* table.py:92-93 */
+    if (!(isfinite(xmin) && isfinite(xmax))) return EQO_ERANGE;  /* table.py:71-72 */
+    if (xmin > xmax) return EQO_ERANGE;                          /* table.py:73-74 */
+    if (xmax == xmin) {                                          /* table.py:96-97 */
+        for (long i = 0; i < d; i++) {
+            double e = (double)xf[i] - xmin;
+            scratch[i] = e * e;
+        }
+        *out = eqo_np_sum(scratch, d);
+        return EQO_OK;
+    }
+    double qmax = (double)((1 << nbits) - 1);                    /* table.py:98 */
+    double scale = (xmax - xmin) / qmax;                         /* table.py:99 */
+    for (long i = 0; i < d; i++) {
+        double x = (double)xf[i];
+        double clamped = np_clip(x, xmin, xmax);                 /* table.py:100 */
+        double code = floor((clamped - xmin) / scale + 0.5);     /* table.py:101 */
+        code = np_clip(code, 0.0, qmax);
+        double recon = scale * code + xmin;                      /* table.py:102 */
+        double e = x - recon;                                    /* table.py:103 */
+        scratch[i] = e * e;
+    }
+    *out = eqo_np_sum(scratch, d);
+    return EQO_OK;
+}
+
+static int check_finite(const float *x, long d) {
+    for (long i = 0; i < d; i++)
+        if (!isfinite(x[i])) return EQO_EFINITE;
+    return EQO_OK;
+}
+
+static void row_minmax(const float *x, long d, double *lo, double *hi) {
+    float a = x[0], b = x[0];
+    for (long i = 1; i < d; i++) {
+        if (x[i] < a) a = x[i];
+        if (x[i] > b) b = x[i];
+    }
+    *lo = (double)a;
+    *hi = (double)b;
+}
+
+/* clipping.py:58-61 clip_range_asym. */
+int eqo_clip_range_asym(const float *x, long d, double *lo, double *hi) {
+    if (d <= 0) return EQO_EEMPTY;
+    row_minmax(x, d, lo, hi);
+    return EQO_OK;
+}
+
+/* clipping.py:142-193 clip_range_greedy (Alg. 1, pair recording).
+ * *iters receives the number of while-loop iterations (-1 for a constant
+ * row, where the reference returns before evaluating any loss), so the
+ * reference's WorkCounters.loss_evals == 1 + 2*iters (0 for constant rows).
+ * *best_i / *best_j receive the step counts of the returned pair:
+ * (x0 + i*step, x1 - j*step). */
+int eqo_clip_range_greedy(const float *x, long d, int nbits, int b, double r,
+                          double *lo, double *hi, int *iters, int *best_i, int *best_j,
+                          double *scratch) {
+    if (b < 1) return EQO_EB;                        /* clipping.py:158-159 */
+    if (!(0.0 < r && r <= 1.0)) return EQO_ER;       /* clipping.py:160-161 */
+    if (d <= 0) return EQO_EEMPTY;                   /* clipping.py:162 */
+    double x0, x1;
+    row_minmax(x, d, &x0, &x1);                      /* clipping.py:163 */
+    if (x0 == x1) {                                  /* clipping.py:164-165 */
+        *lo = x0; *hi = x1; *iters = -1; *best_i = 0; *best_j = 0;
+        return EQO_OK;
+    }
+    double stepsize = (x1 - x0) / (double)b;         /* clipping.py:172 */
+    double min_steps = (double)b * (1.0 - r) * stepsize; /* clipping.py:173 (left to right) */
+    double best_loss;
+    int rc = eqo_quant_mse(x, d, x0, x1, nbits, scratch, &best_loss); /* :174 */
+    if (rc) return rc;
+    double best_min = x0, best_max = x1;
+    long nl = 0, nr = 0;
+    int bi = 0, bj = 0, it = 0;
+    while ((x0 + (double)nl * stepsize) + min_steps < (x1 - (double)nr * stepsize)) { /* :180 */
+        double lmin = x0 + (double)(nl + 1) * stepsize, lmax = x1 - (double)nr * stepsize; /* :181 */
+        double rmin = x0 + (double)nl * stepsize, rmax = x1 - (double)(nr + 1) * stepsize; /* :182 */
+        double loss_l, loss_r;
+        rc = eqo_quant_mse(x, d, lmin, lmax, nbits, scratch, &loss_l);   /* :183 */
+        if (rc) return rc;
+        rc = eqo_quant_mse(x, d, rmin, rmax, nbits, scratch, &loss_r);   /* :184 */
+        if (rc) return rc;
+        if (loss_l < loss_r) {                                           /* :185 */
+            nl += 1;
+            if (loss_l < best_loss) {
+                best_loss = loss_l; best_min = lmin; best_max = lmax;
+                bi = (int)nl; bj = (int)nr;
+            }
+        } else {                                                         /* :189 */
+            nr += 1;
+            if (loss_r < best_loss) {
+                best_loss = loss_r; best_min = rmin; best_max = rmax;
+                bi = (int)nl; bj = (int)nr;
+            }
+        }
+        it++;
+    }
+    *lo = best_min; *hi = best_max; *iters = it; *best_i = bi; *best_j = bj;
+    return EQO_OK;
+}
+
+/* histclip.py:52-67 build_histogram. counts has b entries. */
+int eqo_build_histogram(const float *x, long d, int b, double *lo, double *hi, int64_t *counts) {
+    if (b < 1) return EQO_EB;
+    if (d <= 0) return EQO_EEMPTY;
+    row_minmax(x, d, lo, hi);
+    for (int i = 0; i < b; i++) counts[i] = 0;
+    if (*lo == *hi) {
+        counts[0] = d;
+        return EQO_OK;
+    }
+    double w = (*hi - *lo) / (double)b;
+    for (long i = 0; i < d; i++) {
+        double idx = floor(((double)x[i] - *lo) / w);
+        long k = (long)np_clip(idx, 0.0, (double)(b - 1));
+        counts[k] += 1;
+    }
+    return EQO_OK;
+}
+
+/* histclip.py:70-82 bin_l2_norm: density * (de**3 - db**3) / 3.0 */
+double eqo_bin_l2_norm(double db, double de, double density) {
+    return density * (pow(de, 3.0) - pow(db, 3.0)) / 3.0;
+}
+
+/* histclip.py:85-109 _offset_unit_norms for offsets k[0..n). */
+void eqo_offset_unit_norms(const double *k, long n, double bin_width, double dst_bin_width,
+                           double *out) {
+    double half = 0.5 * dst_bin_width;
+    for (long i = 0; i < n; i++) {
+        double begin = k[i] * bin_width;
+        double end = begin + bin_width;
+        double dob = np_clip(floor((begin + half) / dst_bin_width), 0.0, DST_NBINS - 1);
+        double doe = np_clip(floor((end + half) / dst_bin_width), 0.0, DST_NBINS - 1);
+        double begin_center = dob * dst_bin_width;
+        double end_center = doe * dst_bin_width;
+        double delta_begin = begin - begin_center;
+        double same = eqo_bin_l2_norm(delta_begin, end - begin_center, 1.0);
+        double split = eqo_bin_l2_norm(delta_begin, half, 1.0)
+                     + (doe - dob - 1.0) * eqo_bin_l2_norm(-half, half, 1.0)
+                     + eqo_bin_l2_norm(-half, end - end_center, 1.0);
+        out[i] = (dob == doe) ? same : split;
+    }
+}
+
+/* histclip.py:136-174 hist_brute_search.  scratch: >= 5*b doubles.
+ * Work counters follow histclip.py:148-150,162-164. */
+int eqo_hist_brute(const float *x, long d, int b, double *lo, double *hi, int *start, int *nsel,
+                   double *norm, long *cand_evals, long *bin_visits, double *scratch) {
+    if (b < 1) return EQO_EB;
+    if (d <= 0) return EQO_EEMPTY;
+    int64_t *counts = (int64_t *)malloc(sizeof(int64_t) * (size_t)b);
+    if (!counts) return EQO_EALLOC;
+    double hlo, hhi;
+    eqo_build_histogram(x, d, b, &hlo, &hhi, counts);
+    if (hlo == hhi) {                                         /* histclip.py:147-151 */
+        *cand_evals += 1;
+        *bin_visits += b;
+        *lo = hlo; *hi = hhi; *start = 0; *nsel = 1; *norm = 0.0;
+        free(counts);
+        return EQO_OK;
+    }
+    double w = (hhi - hlo) / (double)b;                       /* Histogram.bin_width */
+    double *density = scratch;                                /* b */
+    double *offsets = scratch + b;                            /* 2b-1 */
+    double *contrib = scratch + 3 * (long)b;                  /* 2b-1 */
+    for (int j = 0; j < b; j++) density[j] = (double)counts[j] / w;  /* :153 */
+    for (int i = 0; i < 2 * b - 1; i++) offsets[i] = (double)(i - (b - 1)); /* :154 */
+    double best_norm = INFINITY;
+    int best_start = 0, best_n = 1;
+    for (int n = 1; n <= b; n++) {                             /* :157 */
+        double dst_w = w * (double)n / (double)(DST_NBINS - 1);   /* :158 */
+        eqo_offset_unit_norms(offsets, 2 * b - 1, w, dst_w, contrib); /* :159 */
+        int ncand = b - n + 1;
+        *cand_evals += ncand;                                   /* :162-164 */
+        *bin_visits += (long)ncand * b;
+        /* :161 norms[s] = sum_j density[j] * contrib[j - s]; first argmin :165 */
+        double nmin = INFINITY;
+        int smin = 0;
+        for (int s = 0; s < ncand; s++) {
+            double acc = 0.0;
+            for (int j = 0; j < b; j++) acc += density[j] * contrib[(j - s) + (b - 1)];
+            if (acc < nmin) { nmin = acc; smin = s; }
+        }
+        if (nmin < best_norm) {                                 /* :166-168 */
+            best_norm = nmin; best_start = smin; best_n = n;
+        }
+    }
+    *lo = hlo + w * (double)best_start;                        /* :170 */
+    *hi = hlo + w * (double)(best_start + best_n);
+    *start = best_start; *nsel = best_n; *norm = best_norm;
+    free(counts);
+    if (!(isfinite(*lo) && isfinite(*hi)) || *lo > *hi) return EQO_ERANGE;
+    return EQO_OK;
+}
+
+/* uniform.py:60-80 quantize_uniform; aux 0 = fp32, 1 = fp16 (uniform.py:19-35).
+ * scale/bias are written as the stored aux value (little-endian bytes). */
+int eqo_quantize_uniform(const float *xf, long d, double xmin, double xmax, int nbits, int aux,
+                         uint8_t *codes, void *scale_out, void *bias_out) {
+    if (nbits != 4 && nbits != 8) return EQO_ENBITS;
+    double qmax = (double)((1 << nbits) - 1);
+    double scale_d, bias_d = xmin;
+    if (xmax == xmin) {                                          /* uniform.py:74-76 */
+        for (long i = 0; i < d; i++) codes[i] = 0;
+        scale_d = 0.0;
+    } else {
+        scale_d = (xmax - xmin) / qmax;                           /* uniform.py:77 */
+        for (long i = 0; i < d; i++) {
+            double c = np_clip((double)xf[i], xmin, xmax);        /* uniform.py:78 */
+            double code = np_clip(floor((c - xmin) / scale_d + 0.5), 0.0, qmax); /* :79 */
+            codes[i] = (uint8_t)code;
+        }
+    }
+    if (aux == 1) {                                               /* np.float16(x): one RNE rounding */
+        _Float16 s = (_Float16)scale_d, bb = (_Float16)bias_d;
+        memcpy(scale_out, &s, 2);
+        memcpy(bias_out, &bb, 2);
+    } else {                                                      /* np.float32(x) */
+        float s = (float)scale_d, bb = (float)bias_d;
+        memcpy(scale_out, &s, 4);
+        memcpy(bias_out, &bb, 4);
+    }
+    return EQO_OK;
+}
+
+/* packed.py:32-33 packed_row_stride */
+long eqo_packed_row_stride(long d, int aux) { return (d + 1) / 2 + 2 * (aux == 1 ? 2 : 4); }
+
+/* packed.py:68-83 pack_table4 for one row: nibbles (even j low), scale, bias. */
+static void pack_row(const uint8_t *codes, long d, int aux, const void *scale, const void *bias,
+                     uint8_t *out) {
+    long half = (d + 1) / 2;
+    for (long k = 0; k < half; k++) {
+        uint8_t lo4 = codes[2 * k];
+        uint8_t hi4 = (2 * k + 1 < d) ? codes[2 * k + 1] : 0;   /* packed.py:75-76 odd-d pad */
+        out[k] = (uint8_t)(lo4 | (hi4 << 4));                   /* packed.py:77 */
+    }
+    int ab = aux == 1 ? 2 : 4;
+    memcpy(out + half, scale, ab);                              /* packed.py:79-82 */
+    memcpy(out + half + ab, bias, ab);
+}
+
+int eqo_pack_table4(const uint8_t *codes, long rows, long d, int aux, const void *scales,
+                    const void *biases, uint8_t *out) {
+    long stride = eqo_packed_row_stride(d, aux);
+    int ab = aux == 1 ? 2 : 4;
+    for (long i = 0; i < rows; i++)
+        pack_row(codes + i * d, d, aux, (const uint8_t *)scales + i * ab,
+                 (const uint8_t *)biases + i * ab, out + i * stride);
+    return EQO_OK;
+}
+
+/* Table driver == pack_table4(quantize_table(EmbeddingTable(x), method, 4, aux, b, r)).
+ * methods.py:63-89 (per-row strategy loop) + uniform.py:142-167 + packed.py:68-83.
+ * Optional per-row outputs (NULL to skip):
+ *   lo/hi      f64 thresholds (ClipRange)
+ *   info0/info1  greedy: iterations / -; hist-brute: start_bin / nbins_selected
+ *   norm       hist-brute window norm
+ * Returns the first error code over rows (rows are independent). */
+int eqo_quantize_pack_table(const float *x, long rows, long d, long ld, int method, int b,
+                            double r, int aux, uint8_t *packed, double *lo_out, double *hi_out,
+                            int32_t *info0, int32_t *info1, double *norm_out, int nthreads) {
+    if (rows < 1 || d < 1) return EQO_EEMPTY;
+    if (method < 0 || method > 2) return EQO_EMETHOD;
+    if (method == METHOD_GREEDY) {
+        if (b < 1) return EQO_EB;
+        if (!(0.0 < r && r <= 1.0)) return EQO_ER;
+    }
+    if (method == METHOD_HIST_BRUTE && b < 1) return EQO_EB;
+    for (long i = 0; i < rows; i++)
+        if (check_finite(x + i * ld, d)) return EQO_EFINITE;      /* table.py:28-29 */
+    long stride = eqo_packed_row_stride(d, aux);
+    int err = 0;
+    long scratch_n = d > 5 * (long)b ? d : 5 * (long)b;
+    if (scratch_n < 16) scratch_n = 16;
+#ifdef _OPENMP
+    if (nthreads < 1) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+#endif
+    {
+        double *scratch = (double *)malloc(sizeof(double) * (size_t)scratch_n);
+        uint8_t *codes = (uint8_t *)malloc((size_t)d + 1);
+        if (!scratch || !codes) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            err = EQO_EALLOC;
+        } else {
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 64)
+#endif
+            for (long i = 0; i < rows; i++) {
+                const float *row = x + i * ld;
+                double lo = 0, hi = 0, nv = 0;
+                int a0 = 0, a1 = 0, rc = 0;
+                if (method == METHOD_ASYM) {
+                    rc = eqo_clip_range_asym(row, d, &lo, &hi);
+                } else if (method == METHOD_GREEDY) {
+                    int bi, bj;
+                    rc = eqo_clip_range_greedy(row, d, 4, b, r, &lo, &hi, &a0, &bi, &bj, scratch);
+                    a1 = bi;
+                } else {
+                    long ce = 0, bv = 0;
+                    rc = eqo_hist_brute(row, d, b, &lo, &hi, &a0, &a1, &nv, &ce, &bv, scratch);
+                }
+                if (!rc) {
+                    uint8_t sb[4], bb[4];
+                    rc = eqo_quantize_uniform(row, d, lo, hi, 4, aux, codes, sb, bb);
+                    if (!rc) pack_row(codes, d, aux, sb, bb, packed + i * stride);
+                }
+                if (rc) {
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+                    { if (!err) err = rc; }
+                }
+                if (lo_out) lo_out[i] = lo;
+                if (hi_out) hi_out[i] = hi;
+                if (info0) info0[i] = a0;
+                if (info1) info1[i] = a1;
+                if (norm_out) norm_out[i] = nv;
+            }
+        }
+        free(scratch);
+        free(codes);
+    }
+    return err;
+}
+
+int eqo_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

@@ -1,0 +1,221 @@
+"""Generate the golden fixtures from the REAL reference (run in the build container).
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [/root/reference/pkg/src]
+
+Imports the unmodified reference package ``embquant`` read-only and records
+its outputs for the hot path (ASYM / GREEDY / HIST-BRUTE clip ranges, the
+uniform codec, pack_table4 bytes, WorkCounters, quant_mse values) on seeded
+inputs.  The fixtures are committed; /root/reference does not exist on the GPU
+box, so tests there compare against these files and against the C oracle that
+these files pin.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF = sys.argv[1] if len(sys.argv) > 1 else "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+sys.dont_write_bytecode = True
+
+import embquant as eq  # noqa: E402
+from embquant.rng import derive_seed, uniform_open01  # noqa: E402
+from embquant.uniform import quantize_table_uniform  # noqa: E402
+
+sys.path.insert(0, os.path.join(HERE, "..", ".."))
+from oracle.rng import mixed_table  # noqa: E402  (plain numpy Generator recipe)
+
+
+def gaussian_rows(seed, rows, d, scale=1.0, loc=0.0):
+    return eq.sample_table(eq.RngSpec("gaussian", loc, scale, seed), rows, d).values.copy()
+
+
+def laplacian_rows(seed, rows, d, scale=1.0):
+    return eq.sample_table(eq.RngSpec("laplacian", 0.0, scale, seed), rows, d).values.copy()
+
+
+def ref_greedy(x, b, r, aux):
+    """pack_table4(quantize_table(t, 'greedy', 4, aux, b, r)) + per-row ranges/counters."""
+    t = eq.EmbeddingTable(x)
+    lo, hi, ev = [], [], []
+    for i in range(t.rows):
+        c = eq.WorkCounters()
+        cr = eq.clip_range_greedy(t.row(i), 4, b, r, counters=c)
+        lo.append(cr.xmin)
+        hi.append(cr.xmax)
+        ev.append(c.loss_evals)
+    q = eq.quantize_table(t, "greedy", 4, aux, b, r)
+    return eq.pack_table4(q).buffer.copy(), np.array(lo), np.array(hi), np.array(ev, np.int64)
+
+
+def ref_asym(x, aux):
+    t = eq.EmbeddingTable(x)
+    q = eq.quantize_table(t, "asym", 4, aux)
+    lo = np.array([eq.clip_range_asym(t.row(i)).xmin for i in range(t.rows)])
+    hi = np.array([eq.clip_range_asym(t.row(i)).xmax for i in range(t.rows)])
+    return eq.pack_table4(q).buffer.copy(), lo, hi
+
+
+def ref_hist(x, b, aux="fp16"):
+    t = eq.EmbeddingTable(x)
+    out = {k: [] for k in ("lo", "hi", "start", "n", "norm", "cand", "visits")}
+    for i in range(t.rows):
+        c = eq.WorkCounters()
+        w = eq.hist_brute_search(t.row(i), b, counters=c)
+        out["lo"].append(w.clip_range.xmin)
+        out["hi"].append(w.clip_range.xmax)
+        out["start"].append(w.start_bin)
+        out["n"].append(w.nbins_selected)
+        out["norm"].append(w.norm)
+        out["cand"].append(c.candidate_evals)
+        out["visits"].append(c.bin_visits)
+    ranges = [eq.ClipRange(a, b_) for a, b_ in zip(out["lo"], out["hi"])]
+    packed = eq.pack_table4(quantize_table_uniform(t, ranges, 4, aux, "hist-brute")).buffer.copy()
+    res = {k: np.array(v) for k, v in out.items()}
+    res["packed"] = packed
+    return res
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def make_config1():
+    t0 = time.time()
+    x = gaussian_rows(1911, 10000, 64)
+    out = {"table_sha256": np.array(sha(x)), "head": x[:16].copy()}
+    out["greedy_fp16_packed"], out["greedy_lo"], out["greedy_hi"], out["greedy_evals"] = \
+        ref_greedy(x, 200, 0.16, "fp16")
+    t = eq.EmbeddingTable(x)
+    ranges = [eq.ClipRange(a, b) for a, b in zip(out["greedy_lo"], out["greedy_hi"])]
+    out["greedy_fp32_packed"] = eq.pack_table4(quantize_table_uniform(t, ranges, 4, "fp32")).buffer
+    out["asym_fp16_packed"], _, _ = ref_asym(x, "fp16")
+    out["asym_fp32_packed"], _, _ = ref_asym(x, "fp32")
+    # laplacian port pin
+    lap = laplacian_rows(77, 64, 64)
+    out["laplacian_sha256"] = np.array(sha(lap))
+    np.savez_compressed(os.path.join(HERE, "config1.npz"), **out)
+    print(f"config1: {time.time() - t0:.1f}s")
+
+
+def edge_inputs():
+    """(name, x, b, r) greedy/asym edge cases; x is (rows, d) float32."""
+    cases = []
+    cases.append(("exact_grid", np.arange(16, dtype=np.float32)[None], 200, 0.16))
+    g = gaussian_rows(13, 1, 63)[0]
+    cases.append(("outlier", np.concatenate([g, np.float32([100.0])])[None], 200, 0.16))
+    cases.append(("constant", np.array([[4.0, 4.0], [2.5, 2.5]], np.float32), 200, 0.16))
+    cases.append(("constant_wide", np.full((2, 37), -1.25, np.float32), 200, 0.16))
+    for i, d in enumerate([1, 2, 3, 5, 7, 8, 9, 15, 16, 17, 31, 32, 33, 48, 63, 64, 65, 100, 127,
+                           128, 129, 200, 255, 256, 257, 300, 511, 512, 1000, 1024, 2048]):
+        rows = 6 if d <= 512 else 3
+        cases.append((f"gauss_d{d}", gaussian_rows(derive_seed(5, d), rows, d), 200, 0.16))
+    cases.append(("laplacian_d64", laplacian_rows(91, 64, 64), 200, 0.16))
+    cases.append(("offset_1000", (1000.0 + gaussian_rows(17, 16, 64) * 1e-3).astype(np.float32),
+                  200, 0.16))
+    cases.append(("tiny_1e-30", (gaussian_rows(18, 8, 32) * 1e-30).astype(np.float32), 200, 0.16))
+    cases.append(("subnormal", (gaussian_rows(19, 4, 16) * 1e-41).astype(np.float32), 200, 0.16))
+    cases.append(("huge_1e30", (gaussian_rows(20, 8, 32) * 1e30).astype(np.float32), 200, 0.16))
+    u = uniform_open01(21, 16 * 64).reshape(16, 64)
+    cases.append(("half_grid", (np.floor(u * 31) / 2).astype(np.float32), 200, 0.16))
+    cases.append(("few_values", (np.floor(u * 5) - 2).astype(np.float32), 200, 0.16))
+    gs = gaussian_rows(22, 8, 32)
+    cases.append(("symmetric", np.concatenate([gs, -gs], 1), 200, 0.16))
+    cases.append(("mixed_d128", mixed_table(384, 128, 1911), 200, 0.16))
+    cases.append(("mixed_d64", mixed_table(384, 64, 1912), 200, 0.16))
+    base = gaussian_rows(23, 12, 64)
+    odd = gaussian_rows(24, 6, 17)
+    for b, r in [(1, 0.16), (1, 1.0), (2, 1.0), (3, 0.9), (8, 0.5), (16, 0.16), (40, 0.16),
+                 (64, 0.16), (200, 0.01), (200, 0.5), (200, 1.0), (400, 0.16), (1000, 0.5)]:
+        cases.append((f"b{b}_r{r}", base, b, r))
+        cases.append((f"b{b}_r{r}_d17", odd, b, r))
+    return cases
+
+
+def make_edge():
+    t0 = time.time()
+    out = {}
+    meta = []
+    for k, (name, x, b, r) in enumerate(edge_inputs()):
+        x = np.ascontiguousarray(x, np.float32)
+        out[f"x_{k}"] = x
+        m = {"name": name, "b": b, "r": r, "greedy_error": None}
+        for aux in ("fp16", "fp32"):
+            try:
+                p, lo, hi, ev = ref_greedy(x, b, r, aux)
+                out[f"greedy_{aux}_{k}"] = p
+                out[f"greedy_lo_{k}"], out[f"greedy_hi_{k}"], out[f"greedy_evals_{k}"] = lo, hi, ev
+            except ValueError as e:
+                m["greedy_error"] = str(e)
+            p, lo, hi = ref_asym(x, aux)
+            out[f"asym_{aux}_{k}"] = p
+        meta.append(m)
+    out["meta"] = np.array(json.dumps(meta))
+    np.savez_compressed(os.path.join(HERE, "edge.npz"), **out)
+    print(f"edge: {len(meta)} cases {time.time() - t0:.1f}s")
+
+
+def make_hist():
+    t0 = time.time()
+    cases = []
+    for b in (8, 16, 40):
+        cases.append((f"gauss_b{b}", np.stack([gaussian_rows(s * 31 + 1, 1, 64)[0] for s in range(5)]), b))
+    cases.append(("lap_b16_d100", laplacian_rows(5, 6, 100), 16))
+    cases.append(("gauss_b64_d32", gaussian_rows(6, 6, 32), 64))
+    cases.append(("gauss_b200_d17", gaussian_rows(7, 4, 17), 200))
+    dense = uniform_open01(123, 4000).astype(np.float32)
+    cases.append(("outlier_prefix_b40", np.concatenate([dense, np.float32([25.0])])[None], 40))
+    cases.append(("constant_b16", np.full((1, 3), 4.0, np.float32), 16))
+    cases.append(("exact_grid_b16", np.arange(16, dtype=np.float32)[None], 16))
+    cases.append(("b1", gaussian_rows(8, 3, 64), 1))
+    cases.append(("config4_b200", gaussian_rows(2024, 256, 64), 200))
+    out = {}
+    meta = []
+    for k, (name, x, b) in enumerate(cases):
+        x = np.ascontiguousarray(x, np.float32)
+        out[f"x_{k}"] = x
+        res = ref_hist(x, b)
+        for key, v in res.items():
+            out[f"{key}_{k}"] = v
+        meta.append({"name": name, "b": b})
+    out["meta"] = np.array(json.dumps(meta))
+    np.savez_compressed(os.path.join(HERE, "hist.npz"), **out)
+    print(f"hist: {time.time() - t0:.1f}s")
+
+
+def make_mse():
+    """quant_mse values (table.py:81-103) for random rows/ranges: pins the f64 op order + np.sum."""
+    rng = np.random.default_rng(7)
+    xs, lo, hi, nb, val, dims = [], [], [], [], [], []
+    for i in range(1500):
+        d = int(rng.integers(1, 300)) if i % 5 else int(rng.choice([64, 128, 129, 256, 1000, 2048]))
+        x = (rng.standard_normal(d) * 10.0 ** rng.uniform(-3, 3)).astype(np.float32)
+        a, b = float(x.min()), float(x.max())
+        if i % 7 == 0:
+            l, h = a, a
+        else:
+            w = b - a
+            l = a + w * rng.uniform(0, 0.3)
+            h = b - w * rng.uniform(0, 0.3)
+            if l > h:
+                l, h = h, l
+        n = 8 if i % 11 == 0 else 4
+        xs.append(x); lo.append(l); hi.append(h); nb.append(n); dims.append(d)
+        val.append(eq.quant_mse(x, eq.ClipRange(l, h), n))
+    out = {"x": np.concatenate(xs), "dims": np.array(dims), "lo": np.array(lo), "hi": np.array(hi),
+           "nbits": np.array(nb), "value": np.array(val)}
+    np.savez_compressed(os.path.join(HERE, "quant_mse.npz"), **out)
+    print("quant_mse: done")
+
+
+if __name__ == "__main__":
+    which = sys.argv[2:] or ["mse", "edge", "hist", "config1"]
+    for w in which:
+        {"mse": make_mse, "edge": make_edge, "hist": make_hist, "config1": make_config1}[w]()
