@@ -1,0 +1,119 @@
+/*
+ * eq4.h -- C ABI of the B200-native row-wise 4-bit clip-search + pack library
+ * (libeq4.so, paper_1911_02079_b200/).  Plain pointers and sizes only.
+ *
+ * The reference (`embquant`, pure Python/numpy) has no FFI layer; its
+ * operator API for this path is the Python functions listed against each
+ * entry point below.  paper_1911_02079_b200/api.py binds this header with
+ * ctypes and re-exposes the reference's Python names; INTEGRATION.md shows
+ * the binding a maintainer would add to the reference itself.
+ *
+ * Conventions
+ *   - Device entry points (eq4_quantize_pack, eq4_pack, eq4_unpack,
+ *     eq4_quant_mse) take DEVICE pointers and a cudaStream_t passed as void*;
+ *     they are stream-ordered and never synchronize the host.
+ *   - Return 0 on success, an EQ4_E* code otherwise (argument errors are
+ *     detected synchronously, before any launch); eq4_last_error() returns a
+ *     thread-local message for the last failure on the calling thread.
+ *   - Data-dependent failures (non-finite input, a search producing
+ *     xmin > xmax) are reported through the optional device status word
+ *     `status` (EQ4_STATUS_* bits, OR-ed) and per-row info0 == -2.
+ *   - Row layout of `packed` is the reference's PackedTable4 layout
+ *     (packed.py:3-6,68-83): ceil(d/2) nibble bytes (element 2k in the low
+ *     nibble of byte k), then scale, then bias, little-endian, at the aux
+ *     width; row stride = eq4_packed_row_stride(d, aux).
+ */
+#ifndef EQ4_H
+#define EQ4_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EQ4_OK 0
+#define EQ4_EINVAL 1      /* bad argument                                  -> ValueError */
+#define EQ4_ECUDA 2       /* CUDA runtime failure                          -> RuntimeError */
+#define EQ4_EDATA 3       /* host path: non-finite input (table.py:28-29)  -> ValueError */
+#define EQ4_ERANGE 4      /* host path: xmin > xmax (table.py:73-74)       -> ValueError */
+#define EQ4_EUNSUPPORTED 5 /* valid for the reference, not on this path    -> ValueError */
+
+#define EQ4_METHOD_ASYM 0       /* clipping.py:58-61   clip_range_asym */
+#define EQ4_METHOD_GREEDY 1     /* clipping.py:142-193 clip_range_greedy */
+#define EQ4_METHOD_HIST_BRUTE 2 /* histclip.py:136-178 hist_brute_search */
+
+#define EQ4_AUX_FP32 0 /* uniform.py:19-35 aux_precision="fp32" */
+#define EQ4_AUX_FP16 1 /* aux_precision="fp16" */
+
+#define EQ4_STATUS_NONFINITE 1 /* a row holds NaN/Inf */
+#define EQ4_STATUS_RANGE 2     /* a GREEDY candidate had xmin > xmax (ClipRange ValueError) */
+
+/* Version string of the library build. */
+const char *eq4_version(void);
+
+/* Thread-local description of the last error returned on this thread. */
+const char *eq4_last_error(void);
+
+/* packed.py:32-33 packed_row_stride(dim, aux_precision). */
+int64_t eq4_packed_row_stride(int64_t dim, int aux);
+
+/*
+ * Fused clip-range search + quantize + pack of a whole table:
+ *   packed = pack_table4(quantize_table(table, method, 4, aux, b, r))
+ * replacing methods.py:63-89 quantize_table (per-row loop over
+ * methods.py:43-60 row_clip_range -> clipping.py / histclip.py strategies),
+ * uniform.py:142-167 quantize_table_uniform and packed.py:68-83 pack_table4.
+ *   x        [rows x ld] fp32, row-major, device; only the first `dim`
+ *            columns of each row are read
+ *   b, r     GREEDY bins / ratio (clipping.py:142-148); HIST-BRUTE bins
+ *   packed   [rows x eq4_packed_row_stride(dim, aux)] bytes, device
+ * Optional per-row device outputs (NULL to skip):
+ *   xmin, xmax  float64 ClipRange of the row (the reference's row_clip_range)
+ *   info0       GREEDY: while-loop iterations (loss_evals = 1 + 2*iters),
+ *               -1 constant row, -2 range error; HIST-BRUTE: start_bin
+ *   info1       GREEDY: (best_i << 16) | best_j; HIST-BRUTE: nbins_selected
+ *   norm        HIST-BRUTE window norm (HistWindow.norm); unused otherwise
+ *   status      device int32, EQ4_STATUS_* bits OR-ed in by the kernels
+ */
+int eq4_quantize_pack(const float *x, int64_t rows, int64_t dim, int64_t ld, int method, int b,
+                      double r, int aux, uint8_t *packed, double *xmin, double *xmax,
+                      int32_t *info0, int32_t *info1, double *norm, int32_t *status,
+                      void *stream);
+
+/*
+ * Same operation on HOST buffers (pinned or pageable), the call a
+ * reference-side binding makes: chunks of rows are staged through device
+ * memory with H2D copy / kernel / D2H copy overlapped on internal streams.
+ * Synchronous; data-dependent failures return EQ4_EDATA / EQ4_ERANGE with the
+ * first failing row in *bad_row and, for EQ4_ERANGE, the offending
+ * (xmin, xmax) pair in bad_lohi[0..1] (both optional).  xmin/xmax/info0/
+ * info1/norm are optional host arrays of length rows.  chunk_rows = 0 picks
+ * a default (~64 MiB of input per chunk).
+ */
+int eq4_quantize_pack_host(const float *x, int64_t rows, int64_t dim, int64_t ld, int method,
+                           int b, double r, int aux, uint8_t *packed, double *xmin, double *xmax,
+                           int32_t *info0, int32_t *info1, double *norm, int64_t chunk_rows,
+                           int64_t *bad_row, double *bad_lohi);
+
+/* packed.py:68-83 pack_table4 of an existing UniformQuantTable:
+ * codes [rows x dim] uint8 (values 0..15), scales/biases [rows] at the aux
+ * dtype (fp32 or fp16 bit patterns), all device. */
+int eq4_pack(const uint8_t *codes, int64_t rows, int64_t dim, int aux, const void *scales,
+             const void *biases, uint8_t *packed, void *stream);
+
+/* packed.py:86-99 _decode_rows inverse of eq4_pack: packed -> codes,
+ * scales, biases (aux-width bit patterns), all device. */
+int eq4_unpack(const uint8_t *packed, int64_t rows, int64_t dim, int aux, uint8_t *codes,
+               void *scales, void *biases, void *stream);
+
+/* table.py:81-103 quant_mse per row, bit-exact float64 (numpy pairwise sum):
+ * out[i] = quant_mse(x[i, :dim], ClipRange(xmin[i], xmax[i]), 4).  Device. */
+int eq4_quant_mse(const float *x, int64_t rows, int64_t dim, int64_t ld, const double *xmin,
+                  const double *xmax, double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EQ4_H */

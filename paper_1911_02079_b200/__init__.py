@@ -1,0 +1,36 @@
+"""B200-native row-wise 4-bit clip-search + pack (arXiv 1911.02079 hot path).
+
+Drop-in for the reference package's quantize entry points (``embquant``:
+methods.quantize_table / row_clip_range, clipping.clip_range_asym /
+clip_range_greedy, histclip.hist_brute_search, packed.pack_table4), computed
+by hand-written sm_100a kernels in libeq4.so (C ABI: include/eq4.h).
+"""
+
+from ._lib import EXPORTS, Eq4Error, LIB_PATH, load  # noqa: F401
+from .api import (  # noqa: F401
+    ALL_METHODS,
+    AUX_PRECISIONS,
+    CODEBOOK_METHODS,
+    GPU_METHODS,
+    UNIFORM_METHODS,
+    ClipRange,
+    EmbeddingTable,
+    HistWindow,
+    PackedTable4,
+    RowResults,
+    UniformQuantTable,
+    WorkCounters,
+    clip_range_asym,
+    clip_range_greedy,
+    clip_range_hist_brute,
+    hist_brute_search,
+    pack_table4,
+    packed_row_stride,
+    quant_mse,
+    quant_mse_rows,
+    quantize_pack_table4,
+    quantize_table,
+    row_clip_range,
+)
+
+__version__ = "0.1.0"

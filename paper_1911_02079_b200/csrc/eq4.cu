@@ -1,0 +1,1040 @@
+// eq4.cu -- B200 (sm_100a) kernels + C ABI for row-wise 4-bit clip-search + pack.
+//
+// Reference path (arXiv 1911.02079 artifact `embquant`):
+//   methods.py:63-89 quantize_table -> per row methods.py:43-60 row_clip_range
+//     -> clipping.py:58-61 clip_range_asym | clipping.py:142-193 clip_range_greedy
+//        | histclip.py:136-178 hist_brute_search (eq4_hist.cu)
+//   -> uniform.py:142-167 quantize_table_uniform -> packed.py:68-83 pack_table4
+// Here one launch does all of it for a whole table: rows are independent, so
+// each row is owned by a group of LPR lanes (E elements per lane, row held in
+// registers), the packed output of a tile of rows is staged in shared memory
+// and leaves as 16-byte stores.
+//
+// GREEDY fast path (the north-star kernel)
+// ----------------------------------------
+// The reference evaluates quant_mse (table.py:81-103) in float64 65-67 times
+// per row.  Every candidate it visits lies on the grid lo = x0 + i*step,
+// hi = x1 - j*step with step = (x1-x0)/b, so in the row coordinate
+//     Y = 15 * (x - x0) / step          (Y in [0, 15b])
+// candidate (i, j) has base B = 15 i, width W = b - i - j steps and
+// reconstruction points B + c*W, c = 0..15 (integers!).  Y is rounded once to
+// a float grid of quantum Q = 2^(ceil(log2 15b) - 24) (2^-12 for b=200) so that
+//     z = Y - B,   e = z - c*W
+// are EXACT fp32 operations; the per element-evaluation cost is 6 fp32
+// instructions (FADD, FFMA.SAT, FFMA.RM, FADD, FFMA, FFMA) against the 13
+// algorithmic FLOP of table.py:100-103.  The code c = floor(z/W + 1/2) clamped
+// to [0,15] comes from one saturating FFMA (s = sat((z/W + 1/2)/alpha)) and
+// one round-down FFMA (2^23 + floor(alpha*s)).
+// The approximate loss L~ differs from the reference's float64 value by at
+// most  tau*L + 2*delta*sqrt(d*L) + d*delta^2 + misround terms  (delta = Q/2;
+// fp32 summation), so every comparison whose two sides are
+// further apart than that band is decided exactly as the reference decides
+// it.  Comparisons inside the band (and every comparison of rows whose
+// candidate grid the reference rounds coarsely) are re-decided with the
+// bit-exact float64 restatement (eq4_device.cuh warp_np_loss), so the walk --
+// and therefore the thresholds, codes and bytes -- match the reference.
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/eq4.h"
+#include "eq4_device.cuh"
+
+namespace eq4 {
+
+constexpr int NTHREADS = 256;
+constexpr int NWARPS = NTHREADS / 32;
+constexpr int MAX_LEAVES = 64;          // numpy pairwise leaves for d <= 4096
+constexpr float ALPHA = 15.75f;         // saturation scale for the code FFMA
+constexpr float MAGIC = 8388608.f;      // 2^23
+enum { M_ASYM = 0, M_GREEDY = 1 };
+
+struct Params {
+  const float* x;
+  int64_t rows;
+  int64_t ld;
+  int d;
+  int b;
+  double r;
+  int aux;
+  int stride;   // packed row stride (bytes)
+  int half;     // ceil(d/2)
+  uint8_t* packed;
+  double* lo_out;
+  double* hi_out;
+  int32_t* info0;
+  int32_t* info1;
+  int32_t* status;
+  // GREEDY constants (host-computed)
+  int it_exact_from;  // loop iterations < this have a provably true condition
+  double qY, inv_qY;  // Y grid quantum and inverse
+  float delta;        // qY / 2
+  float tau2;         // relative band coefficient, both sides
+  float kmis;         // misround band per W^2, both sides
+};
+
+// Copy nbytes from shared src to global dst; src and dst agree modulo 16.
+__device__ __forceinline__ void copy_out(uint8_t* dst, const uint8_t* src, int nbytes) {
+  int head = (int)((16 - ((uintptr_t)dst & 15)) & 15);
+  if (head > nbytes) head = nbytes;
+  int nvec = (nbytes - head) >> 4;
+  int tail = head + (nvec << 4);
+  for (int i = threadIdx.x; i < head; i += NTHREADS) dst[i] = src[i];
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  for (int i = threadIdx.x; i < nvec; i += NTHREADS) d4[i] = s4[i];
+  for (int i = tail + threadIdx.x; i < nbytes; i += NTHREADS) dst[i] = src[i];
+}
+
+template <int LPR>
+__device__ __forceinline__ float group_min(float v) {
+#pragma unroll
+  for (int o = LPR / 2; o >= 1; o >>= 1) v = fminf(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+template <int LPR>
+__device__ __forceinline__ float group_max(float v) {
+#pragma unroll
+  for (int o = LPR / 2; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+template <int LPR>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int o = LPR / 2; o >= 1; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+template <int LPR>
+__device__ __forceinline__ bool group_any(bool v) {
+  unsigned bal = __ballot_sync(FULL, v);
+  if (LPR == 32) return bal != 0;
+  const int lane = threadIdx.x & 31;
+  unsigned gm = ((1u << LPR) - 1u) << (lane & ~(LPR - 1));
+  return (bal & gm) != 0;
+}
+
+// Sum a pair of per-lane partials over the LPR lanes of a group.  Every lane
+// of the group ends with bit-identical (SL, SR), so decisions stay uniform.
+template <int LPR>
+__device__ __forceinline__ void group_sum_pair(float aL, float aR, float& SL, float& SR) {
+  if (LPR == 1) {
+    SL = aL;
+    SR = aR;
+    return;
+  }
+  constexpr int HB = LPR / 2;
+  const bool upper = (threadIdx.x & HB) != 0;
+  float send = upper ? aL : aR;
+  float keep = upper ? aR : aL;
+  keep = __fadd_rn(keep, __shfl_xor_sync(FULL, send, HB));
+#pragma unroll
+  for (int o = HB / 2; o >= 1; o >>= 1) keep = __fadd_rn(keep, __shfl_xor_sync(FULL, keep, o));
+  float other = __shfl_xor_sync(FULL, keep, HB);
+  SL = upper ? other : keep;
+  SR = upper ? keep : other;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float sat_fma(float a, float b, float c) {
+  float r;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// shared row helpers (both methods)
+// ---------------------------------------------------------------------------
+
+// Number of valid slots of lane q (masked kernels: slot i holds element q + LPR*i).
+template <int LPR, int E, bool VEC>
+__device__ __forceinline__ int valid_slots(int q, int d) {
+  if (VEC) return E;
+  int n = (d - q + LPR - 1) / LPR;
+  return n < 0 ? 0 : (n > E ? E : n);
+}
+
+template <int LPR, int E, bool VEC>
+__device__ __forceinline__ void load_row(const Params& p, int64_t row, bool rvalid, int q, int nv,
+                                         float (&v)[E]) {
+  const float* xrow = p.x + (rvalid ? row : 0) * p.ld;
+  if (VEC) {
+    const float4* src = reinterpret_cast<const float4*>(xrow);
+#pragma unroll
+    for (int c = 0; c < E / 4; ++c) {
+      float4 t = rvalid ? __ldcs(src + q + LPR * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[4 * c] = t.x; v[4 * c + 1] = t.y; v[4 * c + 2] = t.z; v[4 * c + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = (rvalid && i < nv) ? __ldcs(xrow + q + LPR * i) : 0.f;
+  }
+}
+
+// Row min / max over the group + finiteness (table.py:28-29, clipping.py:58-61).
+template <int LPR, int E, bool VEC>
+__device__ __forceinline__ void row_minmax(const Params& p, const float (&v)[E], int nv, bool rvalid,
+                                           int q, float& mn, float& mx, bool& bad) {
+  mn = INFINITY;
+  mx = -INFINITY;
+  float sm = 0.f;
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    if (VEC || i < nv) {
+      mn = fminf(mn, v[i]);
+      mx = fmaxf(mx, v[i]);
+      sm = __fadd_rn(sm, v[i]);   // NaN/Inf propagate; overflow only gives a false alarm
+    }
+  }
+  mn = group_min<LPR>(mn);
+  mx = group_max<LPR>(mx);
+  sm = group_sum<LPR>(sm);
+  bad = false;
+  if (__any_sync(FULL, !isfinite(sm) && rvalid)) {
+    bool lb = false;
+#pragma unroll
+    for (int i = 0; i < E; ++i) lb |= (VEC || i < nv) && !isfinite(v[i]);
+    bad = group_any<LPR>(lb) && rvalid;
+    if (bad && q == 0 && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
+  }
+}
+
+// Codes (uniform.py:77-79) into the staged row + scale/bias (uniform.py:80,
+// packed.py:79-82).  VEC: nibbles straight into the packed row; masked: one
+// code byte per element into crow (packed by pack_tile).
+// Warp-collective: every lane of the warp must call it (rvalid gates stores).
+template <int LPR, int E, bool VEC>
+__device__ __forceinline__ void emit_row(const Params& p, const float (&v)[E], int nv, double lo,
+                                         double hi, bool range_ok, bool rvalid, int q, uint8_t* orow,
+                                         uint8_t* crow) {
+  const CodeParams cp = make_code_params(range_ok ? lo : 0.0, range_ok ? hi : 0.0);
+  unsigned long long need = 0ull;
+  if (VEC) {
+#pragma unroll
+    for (int c = 0; c < E / 4; ++c) {
+      bool n0, n1, n2, n3;
+      unsigned c0 = code_of(v[4 * c], cp, n0), c1 = code_of(v[4 * c + 1], cp, n1);
+      unsigned c2 = code_of(v[4 * c + 2], cp, n2), c3 = code_of(v[4 * c + 3], cp, n3);
+      need |= (unsigned long long)(n0 | (n1 << 1) | (n2 << 2) | (n3 << 3)) << (4 * c);
+      const int byte = 2 * (q + LPR * c);
+      if (rvalid) {
+        orow[byte] = (uint8_t)(c0 | (c1 << 4));
+        orow[byte + 1] = (uint8_t)(c2 | (c3 << 4));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      if (i < nv) {
+        bool ne;
+        const uint8_t c = (uint8_t)code_of(v[i], cp, ne);
+        if (rvalid) crow[q + LPR * i] = c;
+        need |= (unsigned long long)ne << i;
+      }
+    }
+  }
+  if (!rvalid) need = 0ull;
+  if (__any_sync(FULL, need != 0ull)) {   // rare: float64 codec for near-boundary elements
+    for (int i = 0; i < E; ++i) {
+      if (!((need >> i) & 1ull)) continue;
+      unsigned c = code_exact(v[i], cp);
+      if (VEC) {
+        const int byte = 2 * (q + LPR * (i >> 2)) + ((i & 3) >> 1);
+        const int sh = (i & 1) * 4;
+        orow[byte] = (uint8_t)((orow[byte] & ~(0xF << sh)) | (c << sh));
+      } else {
+        crow[q + LPR * i] = (uint8_t)c;
+      }
+    }
+  }
+  if (q == 0 && rvalid) {
+    uint8_t* a = orow + p.half;
+    const double sc = range_ok ? cp.scale : 0.0;
+    if (p.aux == EQ4_AUX_FP16) {
+      uint32_t s = aux_bits_f16(sc), bb = aux_bits_f16(lo);
+      a[0] = s & 0xff; a[1] = s >> 8; a[2] = bb & 0xff; a[3] = bb >> 8;
+    } else {
+      uint32_t s = aux_bits_f32(sc), bb = aux_bits_f32(lo);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { a[k] = (s >> (8 * k)) & 0xff; a[4 + k] = (bb >> (8 * k)) & 0xff; }
+    }
+  }
+}
+
+// Finish a tile: (masked) nibble packing from the code tile, then 16-byte
+// stores of the staged rows.
+template <int D, bool VEC>
+__device__ __forceinline__ void store_tile(const Params& p, const uint8_t* codes_s, uint8_t* out_tile,
+                                           int tile_rows, size_t gofs) {
+  if (!VEC) {
+    __syncthreads();
+    const int nb = tile_rows * p.half;
+    for (int t = threadIdx.x; t < nb; t += NTHREADS) {
+      int rr = t / p.half, m = t - rr * p.half;
+      unsigned c0 = codes_s[rr * D + 2 * m];
+      unsigned c1 = (2 * m + 1 < p.d) ? codes_s[rr * D + 2 * m + 1] : 0u;  // packed.py:75-76
+      out_tile[rr * p.stride + m] = (uint8_t)(c0 | (c1 << 4));
+    }
+  }
+  __syncthreads();
+  copy_out(p.packed + gofs, out_tile, tile_rows * p.stride);
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// ASYM: min/max -> codes -> pack (HBM-bound streaming kernel)
+// ---------------------------------------------------------------------------
+template <int LPR, int E, bool VEC>
+struct LayoutA {
+  static constexpr int RPB = NTHREADS / LPR;
+  static constexpr int D = LPR * E;
+  __host__ __device__ static size_t out_off() { return VEC ? 0 : (((size_t)RPB * D + 15) & ~(size_t)15); }
+  __host__ __device__ static size_t total(int stride) { return out_off() + (size_t)RPB * stride + 32; }
+};
+
+template <int LPR, int E, bool VEC>
+__global__ void __launch_bounds__(NTHREADS, E <= 16 ? 4 : (E == 32 ? 3 : 2))
+k_asym(const Params p) {
+  using L = LayoutA<LPR, E, VEC>;
+  constexpr int RPB = L::RPB;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const int g = tid / LPR, q = tid % LPR;
+  uint8_t* codes_s = smem;
+  uint8_t* out_base = smem + L::out_off();
+  const int nv = valid_slots<LPR, E, VEC>(q, p.d);
+  const int64_t ntiles = (p.rows + RPB - 1) / RPB;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * RPB, row = row0 + g;
+    const bool rvalid = row < p.rows;
+    const int tile_rows = (int)min((int64_t)RPB, p.rows - row0);
+    const size_t gofs = (size_t)row0 * p.stride;
+    uint8_t* out_tile = out_base + (((uintptr_t)p.packed + gofs) & 15);
+    float v[E];
+    load_row<LPR, E, VEC>(p, row, rvalid, q, nv, v);
+    float mn, mx;
+    bool bad;
+    row_minmax<LPR, E, VEC>(p, v, nv, rvalid, q, mn, mx, bad);
+    const double lo = (double)mn, hi = (double)mx;   // clipping.py:61
+    emit_row<LPR, E, VEC>(p, v, nv, lo, hi, !bad, rvalid, q, out_tile + g * p.stride,
+                          codes_s + g * L::D);
+    if (rvalid) {
+      if (q == 0) {
+        if (p.lo_out) { p.lo_out[row] = lo; p.hi_out[row] = hi; }
+        if (p.info0) p.info0[row] = 0;
+        if (p.info1) p.info1[row] = 0;
+      }
+    }
+    store_tile<L::D, VEC>(p, codes_s, out_tile, tile_rows, gofs);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GREEDY: clipping.py:142-193, fused with the codec and the packer
+// ---------------------------------------------------------------------------
+
+// Rarely-touched float64 state of one row's walk, kept in shared memory so the
+// hot loop holds only the row slice (Yh) and a few scalars in registers.
+struct RowShared {
+  double x0, x1, step, min_steps, kY2, best_ex, elo, ehi;
+};
+
+template <int LPR, int E, bool VEC>
+struct LayoutG {
+  static constexpr int RPB = NTHREADS / LPR;
+  static constexpr int D = LPR * E;
+  __host__ __device__ static size_t xs_bytes() { return (size_t)RPB * D * 4; }
+  __host__ __device__ static size_t ys_off() { return xs_bytes(); }
+  __host__ __device__ static size_t rs_off() { return 2 * xs_bytes(); }
+  __host__ __device__ static size_t leaf_off() { return rs_off() + (size_t)RPB * sizeof(RowShared); }
+  __host__ __device__ static size_t codes_off() { return leaf_off() + (size_t)NWARPS * MAX_LEAVES * 16; }
+  __host__ __device__ static size_t out_off() {
+    return (codes_off() + (VEC ? 0 : (size_t)RPB * D) + 15) & ~(size_t)15;
+  }
+  __host__ __device__ static size_t total(int stride) { return out_off() + (size_t)RPB * stride + 32; }
+};
+
+// One fast candidate: approximate loss (Y units) of base B, width W.
+template <int E, bool MASKED>
+__device__ __forceinline__ float eval_one(const float (&Yh)[E], int nv, float B, float nW, float kW,
+                                          float h) {
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    float z = __fadd_rn(Yh[i], -B);
+    float t = sat_fma(z, kW, h);
+    float m = __fmaf_rd(t, ALPHA, MAGIC);
+    float c = __fadd_rn(m, -MAGIC);
+    float e = __fmaf_rn(c, nW, z);
+    if (!MASKED || i < nv) s = __fmaf_rn(e, e, s);
+  }
+  return s;
+}
+
+// The two candidates of one iteration share W: L = (BL, W), R = (BL - 15, W).
+// 6 fp32 instructions per element and candidate.
+template <int E, bool MASKED>
+__device__ __forceinline__ void eval_pair(const float (&Yh)[E], int nv, float BL, float nW, float kW,
+                                          float h, float& aL, float& aR) {
+  float sL = 0.f, sR = 0.f;
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    float zL = __fadd_rn(Yh[i], -BL);
+    float zR = __fadd_rn(zL, 15.f);                       // exact
+    float tL = sat_fma(zL, kW, h);
+    float tR = sat_fma(zR, kW, h);
+    float mL = __fmaf_rd(tL, ALPHA, MAGIC);               // 2^23 + floor(alpha * t)
+    float mR = __fmaf_rd(tR, ALPHA, MAGIC);
+    float cL = __fadd_rn(mL, -MAGIC);
+    float cR = __fadd_rn(mR, -MAGIC);
+    float eL = __fmaf_rn(cL, nW, zL);                     // exact
+    float eR = __fmaf_rn(cR, nW, zR);
+    if (!MASKED || i < nv) {
+      sL = __fmaf_rn(eL, eL, sL);
+      sR = __fmaf_rn(eR, eR, sR);
+    }
+  }
+  aL = sL;
+  aR = sR;
+}
+
+// Exact (reference) decision of one loop iteration for one row.  Warp-
+// collective: every lane passes the owning group's (broadcast) state.
+struct ExactOut {
+  double vL, vR, vb;
+  int flags;  // 1 = range error, 2 = move left, 4 = candidate better than best
+};
+
+__device__ __forceinline__ ExactOut exact_decide(RowShared* R, double nl, double nr, int bi, int bj,
+                                                 bool bvalid, const float* xs, int d,
+                                                 double* leaf_sum, int* leaf_st, int* leaf_ln) {
+  ExactOut o;
+  const double x0 = R->x0, x1 = R->x1, st = R->step;
+  o.vL = o.vR = 0.0;
+  o.vb = R->best_ex;
+  o.flags = 0;
+  // clipping.py:181-184 candidates; ClipRange validation table.py:70-74 (L first)
+  double lmin = __dadd_rn(x0, __dmul_rn(nl + 1.0, st)), lmax = __dsub_rn(x1, __dmul_rn(nr, st));
+  double rmin = __dadd_rn(x0, __dmul_rn(nl, st)), rmax = __dsub_rn(x1, __dmul_rn(nr + 1.0, st));
+  const bool errL = !(lmin <= lmax);
+  const bool errR = !(rmin <= rmax);
+  if (!errL) o.vL = warp_np_loss(xs, d, lmin, lmax, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
+  if (errL || errR) {
+    if ((threadIdx.x & 31) == 0) {
+      R->elo = errL ? lmin : rmin;
+      R->ehi = errL ? lmax : rmax;
+    }
+    o.flags = 1;
+    return o;
+  }
+  o.vR = warp_np_loss(xs, d, rmin, rmax, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
+  const bool goL = o.vL < o.vR;                             // clipping.py:185
+  const double vc = goL ? o.vL : o.vR;
+  if (!bvalid) {
+    double blo = bi == 0 ? x0 : __dadd_rn(x0, __dmul_rn((double)bi, st));
+    double bhi = bj == 0 ? x1 : __dsub_rn(x1, __dmul_rn((double)bj, st));
+    o.vb = warp_np_loss(xs, d, blo, bhi, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
+  }
+  o.flags = (goL ? 2 : 0) | (vc < o.vb ? 4 : 0);            // clipping.py:187,191
+  return o;
+}
+
+enum : unsigned { F_ACTIVE = 1, F_EXACT_ONLY = 2, F_BEST_EX = 4, F_ERR = 8 };
+
+template <int LPR, int E, bool VEC>
+__global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Params p) {
+  using L = LayoutG<LPR, E, VEC>;
+  constexpr int RPB = L::RPB;
+  constexpr int D = L::D;
+  constexpr int RPW = 32 / LPR;
+  static_assert(LPR >= 1 && LPR <= 32 && (LPR & (LPR - 1)) == 0, "LPR");
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* xs = reinterpret_cast<float*>(smem);
+  float* ys = reinterpret_cast<float*>(smem + L::ys_off());
+  RowShared* rs = reinterpret_cast<RowShared*>(smem + L::rs_off());
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = tid / LPR, q = tid % LPR;
+  double* leaf_sum = reinterpret_cast<double*>(smem + L::leaf_off()) + warp * MAX_LEAVES * 2;
+  int* leaf_st = reinterpret_cast<int*>(leaf_sum + MAX_LEAVES);
+  int* leaf_ln = leaf_st + MAX_LEAVES;
+  uint8_t* codes_s = smem + L::codes_off();
+  uint8_t* out_base = smem + L::out_off();
+  const int d = p.d;
+  const int nv = valid_slots<LPR, E, VEC>(q, d);
+  const float hh = 0.5f / ALPHA;
+  const int64_t ntiles = (p.rows + RPB - 1) / RPB;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * RPB, row = row0 + g;
+    const bool rvalid = row < p.rows;
+    const int tile_rows = (int)min((int64_t)RPB, p.rows - row0);
+    const size_t gofs = (size_t)row0 * p.stride;
+    uint8_t* out_tile = out_base + (((uintptr_t)p.packed + gofs) & 15);
+    RowShared& R = rs[g];
+    float* xr = xs + g * D;
+    float* yr = ys + g * D;
+
+    float Yh[E];
+    float mn, mx;
+    bool bad;
+    {
+      float v[E];
+      load_row<LPR, E, VEC>(p, row, rvalid, q, nv, v);
+      if (VEC) {
+#pragma unroll
+        for (int c = 0; c < E / 4; ++c)
+          *reinterpret_cast<float4*>(xr + 4 * (q + LPR * c)) =
+              make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+          if (i < nv) xr[q + LPR * i] = v[i];
+      }
+      row_minmax<LPR, E, VEC>(p, v, nv, rvalid, q, mn, mx, bad);
+      const double x0 = (double)mn, x1 = (double)mx;
+      const double Dw = __dsub_rn(x1, x0);
+      const double step = __ddiv_rn(Dw, (double)p.b);                               // :172
+      const double kY = (x0 != x1) ? __ddiv_rn(15.0, step) : 0.0;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {      // Y on the exact fp32 grid of quantum qY
+        double Y = __dmul_rn(__dsub_rn((double)v[i], x0), kY);
+        Yh[i] = (float)(rint(Y * p.inv_qY) * p.qY);
+      }
+      // a copy in shared memory lets the rare exact path below clobber the
+      // registers: Yh is re-read after it instead of living across its calls
+      if (VEC) {
+#pragma unroll
+        for (int c = 0; c < E / 4; ++c)
+          *reinterpret_cast<float4*>(yr + 4 * (q + LPR * c)) =
+              make_float4(Yh[4 * c], Yh[4 * c + 1], Yh[4 * c + 2], Yh[4 * c + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) yr[q + LPR * i] = Yh[i];
+      }
+      if (q == 0) {
+        R.x0 = x0; R.x1 = x1; R.step = step;
+        R.min_steps = __dmul_rn(__dmul_rn((double)p.b, __dsub_rn(1.0, p.r)), step);  // :173
+        R.kY2 = kY * kY; R.best_ex = 0.0; R.elo = 0.0; R.ehi = 0.0;
+      }
+    }
+    __syncwarp();
+    unsigned flags = 0;
+    float tau2 = p.tau2;
+    if (rvalid && !bad && mn != mx) {                                                // :164-165
+      flags = F_ACTIVE;
+      const float M = fmaxf(fabsf(mn), fabsf(mx)), Dwf = mx - mn;
+      if (!(M <= 1e6f * Dwf)) flags |= F_EXACT_ONLY;   // reference grid rounds coarsely
+      tau2 += 6e-14f * (M / Dwf);
+    }
+    const float c1 = 4.2f * p.delta * sqrtf((float)d);
+    const float c0 = 2.1f * (float)d * p.delta * p.delta;
+    float Lbest;
+    {
+      const float Wf = (float)p.b;                                                   // :174
+      Lbest = group_sum<LPR>(eval_one<E, !VEC>(Yh, nv, 0.f, -Wf, rcp_approx(Wf * ALPHA), hh));
+    }
+    int nl = 0, nr = 0, bi = 0, bj = 0, iters = 0;
+    for (int it = 0;; ++it) {
+      if ((flags & F_ACTIVE) && (it >= p.it_exact_from || (flags & F_EXACT_ONLY))) {   // :180
+        const double lhs = __dadd_rn(__dadd_rn(R.x0, __dmul_rn((double)nl, R.step)), R.min_steps);
+        const double rhs = __dsub_rn(R.x1, __dmul_rn((double)nr, R.step));
+        if (!(lhs < rhs)) flags &= ~F_ACTIVE;
+      }
+      if (!__any_sync(FULL, flags & F_ACTIVE)) break;
+      const int W = p.b - it - 1;
+      float SL = 0.f, SR = 0.f;
+      bool need_ex = (flags & F_ACTIVE) != 0;
+      if (W >= 1) {
+        const float Wf = (float)W;
+        float aL, aR;
+        eval_pair<E, !VEC>(Yh, nv, (float)(15 * (nl + 1)), -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+        group_sum_pair<LPR>(aL, aR, SL, SR);
+        const float misW2 = p.kmis * Wf * Wf;
+        const bool goL = SL < SR;
+        const float cand = goL ? SL : SR;
+        const float mlr = fmaxf(SL, SR), mb = fmaxf(cand, Lbest);
+        const float cw = c0 + misW2;
+        const bool near_lr = fabsf(SL - SR) <= tau2 * mlr + c1 * sqrt_approx(mlr) + cw;
+        const bool near_b = fabsf(cand - Lbest) <= tau2 * mb + c1 * sqrt_approx(mb) + cw;
+        need_ex = (flags & F_ACTIVE) && ((flags & F_EXACT_ONLY) || near_lr || near_b);
+        if ((flags & F_ACTIVE) && !need_ex) {
+          if (goL) ++nl; else ++nr;
+          if (cand < Lbest) {
+            Lbest = cand; bi = nl; bj = nr;
+            flags &= ~F_BEST_EX;
+          }
+          ++iters;
+        }
+      }
+      unsigned bal = __ballot_sync(FULL, need_ex && q == 0);
+      if (bal) {
+      while (bal) {
+        const int leader = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const int lg = warp * RPW + leader / LPR;
+        const ExactOut o = exact_decide(
+            &rs[lg], (double)__shfl_sync(FULL, nl, leader), (double)__shfl_sync(FULL, nr, leader),
+            __shfl_sync(FULL, bi, leader), __shfl_sync(FULL, bj, leader),
+            (__shfl_sync(FULL, flags, leader) & F_BEST_EX) != 0, xs + lg * D, d, leaf_sum, leaf_st,
+            leaf_ln);
+        if (lg == g) {
+          if (o.flags & 1) {
+            flags = (flags & ~F_ACTIVE) | F_ERR;
+          } else {
+            const bool goL = (o.flags & 2) != 0;
+            const double vc = goL ? o.vL : o.vR;
+            if (goL) ++nl; else ++nr;
+            if (o.flags & 4) {
+              bi = nl; bj = nr;
+              if (q == 0) R.best_ex = vc;
+              Lbest = (W >= 1) ? (goL ? SL : SR) : (float)(vc * R.kY2);
+            } else if (q == 0) {
+              R.best_ex = o.vb;
+            }
+            flags |= F_BEST_EX;
+            ++iters;
+          }
+        }
+        __syncwarp();
+      }
+      if (VEC) {
+#pragma unroll
+        for (int c = 0; c < E / 4; ++c) {
+          const float4 t = *reinterpret_cast<const float4*>(yr + 4 * (q + LPR * c));
+          Yh[4 * c] = t.x; Yh[4 * c + 1] = t.y; Yh[4 * c + 2] = t.z; Yh[4 * c + 3] = t.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) Yh[i] = yr[q + LPR * i];
+      }
+      }
+    }
+
+    // ---- result, codes, pack ----
+    double lo, hi;
+    int info0 = -1, info1 = 0;
+    if (flags & F_ERR) {
+      lo = R.elo; hi = R.ehi; info0 = -2;
+      if (q == 0 && p.status) atomicOr(p.status, EQ4_STATUS_RANGE);
+    } else {
+      lo = bi == 0 ? R.x0 : __dadd_rn(R.x0, __dmul_rn((double)bi, R.step));
+      hi = bj == 0 ? R.x1 : __dsub_rn(R.x1, __dmul_rn((double)bj, R.step));
+      if (rvalid && !bad && mn != mx) { info0 = iters; info1 = (bi << 16) | bj; }
+    }
+    {
+      float v[E];
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[i] = (VEC || i < nv) ? xr[VEC ? 4 * (q + LPR * (i >> 2)) + (i & 3) : q + LPR * i] : 0.f;
+      emit_row<LPR, E, VEC>(p, v, nv, lo, hi, !bad && !(flags & F_ERR), rvalid, q,
+                            out_tile + g * p.stride, codes_s + g * D);
+    }
+    if (rvalid) {
+      if (q == 0) {
+        if (p.lo_out) { p.lo_out[row] = lo; p.hi_out[row] = hi; }
+        if (p.info0) p.info0[row] = info0;
+        if (p.info1) p.info1[row] = info1;
+      }
+    }
+    store_tile<D, VEC>(p, codes_s, out_tile, tile_rows, gofs);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pack / unpack / quant_mse utility kernels
+// ---------------------------------------------------------------------------
+__global__ void k_pack(const uint8_t* codes, int64_t rows, int d, int aux, const uint8_t* sc,
+                       const uint8_t* bi, uint8_t* out, int stride) {
+  const int half = (d + 1) / 2, ab = aux == EQ4_AUX_FP16 ? 2 : 4;
+  int64_t n = rows * stride;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = t / stride;
+    int k = (int)(t - r * stride);
+    uint8_t v;
+    if (k < half) {
+      unsigned c0 = codes[r * d + 2 * k] & 0xF;
+      unsigned c1 = (2 * k + 1 < d) ? (codes[r * d + 2 * k + 1] & 0xF) : 0u;
+      v = (uint8_t)(c0 | (c1 << 4));
+    } else if (k < half + ab) {
+      v = sc[r * ab + (k - half)];
+    } else {
+      v = bi[r * ab + (k - half - ab)];
+    }
+    out[t] = v;
+  }
+}
+
+__global__ void k_unpack(const uint8_t* packed, int64_t rows, int d, int aux, uint8_t* codes,
+                         uint8_t* sc, uint8_t* bi, int stride) {
+  const int half = (d + 1) / 2, ab = aux == EQ4_AUX_FP16 ? 2 : 4;
+  int64_t n = rows * stride;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = t / stride;
+    int k = (int)(t - r * stride);
+    uint8_t v = packed[t];
+    if (k < half) {
+      codes[r * d + 2 * k] = v & 0xF;
+      if (2 * k + 1 < d) codes[r * d + 2 * k + 1] = v >> 4;
+    } else if (k < half + ab) {
+      sc[r * ab + (k - half)] = v;
+    } else {
+      bi[r * ab + (k - half - ab)] = v;
+    }
+  }
+}
+
+// One warp per row: bit-exact quant_mse (table.py:81-103).
+__global__ void __launch_bounds__(NTHREADS) k_quant_mse(const float* x, int64_t rows, int d,
+                                                        int64_t ld, const double* lo,
+                                                        const double* hi, double* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* leaf_sum = reinterpret_cast<double*>(smem) + warp * MAX_LEAVES * 2;
+  int* leaf_st = reinterpret_cast<int*>(leaf_sum + MAX_LEAVES);
+  int* leaf_ln = leaf_st + MAX_LEAVES;
+  float* xs = reinterpret_cast<float*>(smem + (size_t)NWARPS * MAX_LEAVES * 16) + (size_t)warp * d;
+  for (int64_t row = blockIdx.x * (int64_t)NWARPS + warp; row < rows;
+       row += (int64_t)gridDim.x * NWARPS) {
+    for (int k = lane; k < d; k += 32) xs[k] = x[row * ld + k];
+    __syncwarp();
+    double v = warp_np_loss(xs, d, lo[row], hi[row], leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
+    if (lane == 0) out[row] = v;
+    __syncwarp();
+  }
+}
+
+}  // namespace eq4
+
+// ===========================================================================
+// Host side
+// ===========================================================================
+using namespace eq4;
+
+static thread_local std::string g_err;
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+static int cuda_fail(cudaError_t e, const char* where) {
+  return fail(EQ4_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+static int sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+template <typename Kern>
+static int launch_persistent(Kern kern, size_t smem, int64_t ntiles, const Params& p, cudaStream_t s,
+                             const char* name) {
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+  }
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NTHREADS, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+  if (occ < 1) occ = 1;
+  int64_t grid = std::min<int64_t>(ntiles, (int64_t)sm_count() * occ);
+  kern<<<(unsigned)grid, NTHREADS, smem, s>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, name);
+  return EQ4_OK;
+}
+
+template <int METHOD, int LPR, int E, bool VEC>
+static int launch_rq(const Params& p, cudaStream_t s) {
+  if (METHOD == M_ASYM) {
+    using L = LayoutA<LPR, E, VEC>;
+    return launch_persistent(k_asym<LPR, E, VEC>, L::total(p.stride), (p.rows + L::RPB - 1) / L::RPB,
+                             p, s, "k_asym");
+  } else {
+    using L = LayoutG<LPR, E, VEC>;
+    return launch_persistent(k_greedy<LPR, E, VEC>, L::total(p.stride),
+                             (p.rows + L::RPB - 1) / L::RPB, p, s, "k_greedy");
+  }
+}
+
+template <int METHOD>
+static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
+  const int d = p.d;
+  if (vec) {
+    switch (d) {
+      case 16: return METHOD == M_ASYM ? launch_rq<METHOD, 2, 8, true>(p, s)
+                                       : launch_rq<METHOD, 1, 16, true>(p, s);
+      case 32: return launch_rq<METHOD, 2, 16, true>(p, s);
+      case 64: return launch_rq<METHOD, 4, 16, true>(p, s);
+      case 128: return launch_rq<METHOD, 8, 16, true>(p, s);
+      case 256: return launch_rq<METHOD, 16, 16, true>(p, s);
+      case 512: return launch_rq<METHOD, 32, 16, true>(p, s);
+      case 1024: return launch_rq<METHOD, 32, 32, true>(p, s);
+      case 2048: return launch_rq<METHOD, 32, 64, true>(p, s);
+      default: break;
+    }
+  }
+  if (d <= 8) return launch_rq<METHOD, 1, 8, false>(p, s);
+  if (d <= 16) return launch_rq<METHOD, 1, 16, false>(p, s);
+  if (d <= 32) return launch_rq<METHOD, 2, 16, false>(p, s);
+  if (d <= 64) return launch_rq<METHOD, 4, 16, false>(p, s);
+  if (d <= 128) return launch_rq<METHOD, 8, 16, false>(p, s);
+  if (d <= 256) return launch_rq<METHOD, 16, 16, false>(p, s);
+  if (d <= 512) return launch_rq<METHOD, 32, 16, false>(p, s);
+  if (d <= 1024) return launch_rq<METHOD, 32, 32, false>(p, s);
+  if (d <= 2048) return launch_rq<METHOD, 32, 64, false>(p, s);
+  return fail(EQ4_EUNSUPPORTED, "dim > 2048 is not supported by the B200 path");
+}
+
+// GREEDY error-band constants: per side, the fp32
+// loss carries <= (E - 1 + log2 LPR + 2) u relative summation error; both
+// sides -> x2; 5% margin.
+static float tau2_for(int d) {
+  int lpr, e;
+  if (d <= 16) { lpr = 1; e = 16; }
+  else if (d <= 512) { lpr = 1; while (lpr * 16 < d) lpr *= 2; e = 16; }
+  else if (d <= 1024) { lpr = 32; e = 32; }
+  else { lpr = 32; e = 64; }
+  int lg = 0;
+  while ((1 << lg) < lpr) lg++;
+  return (float)(2.0 * 1.05 * (e - 1 + lg + 2) * 5.9604645e-8);
+}
+
+extern "C" {
+
+const char* eq4_version(void) { return "eq4 0.1.0 (sm_100a)"; }
+
+const char* eq4_last_error(void) { return g_err.c_str(); }
+
+int64_t eq4_packed_row_stride(int64_t dim, int aux) {
+  return (dim + 1) / 2 + 2 * (aux == EQ4_AUX_FP16 ? 2 : 4);
+}
+
+int eq4_quantize_pack(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, int b,
+                      double r, int aux, uint8_t* packed, double* xmin, double* xmax,
+                      int32_t* info0, int32_t* info1, double* norm, int32_t* status,
+                      void* stream) {
+  if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "table must be at least 1x1");
+  if (ld < dim) return fail(EQ4_EINVAL, "ld must be >= dim");
+  if (!x || !packed) return fail(EQ4_EINVAL, "null buffer");
+  if (aux != EQ4_AUX_FP16 && aux != EQ4_AUX_FP32) return fail(EQ4_EINVAL, "aux must be fp32 or fp16");
+  if ((xmin == nullptr) != (xmax == nullptr)) return fail(EQ4_EINVAL, "xmin/xmax must be given together");
+  if (method == EQ4_METHOD_GREEDY || method == EQ4_METHOD_HIST_BRUTE) {
+    if (b < 1) return fail(EQ4_EINVAL, "b must be >= " "1, got " + std::to_string(b));
+  }
+  if (method == EQ4_METHOD_GREEDY && !(0.0 < r && r <= 1.0))
+    return fail(EQ4_EINVAL, "r must be in (0, 1], got " + std::to_string(r));
+  cudaStream_t s = (cudaStream_t)stream;
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.x = x; p.rows = rows; p.ld = ld; p.d = (int)dim; p.b = b; p.r = r; p.aux = aux;
+  p.stride = (int)eq4_packed_row_stride(dim, aux);
+  p.half = (int)((dim + 1) / 2);
+  p.packed = packed; p.lo_out = xmin; p.hi_out = xmax; p.info0 = info0; p.info1 = info1;
+  p.status = status;
+  const bool vec = (dim % 4 == 0) && (ld % 4 == 0) && (((uintptr_t)x & 15) == 0);
+  if (method == EQ4_METHOD_ASYM) return dispatch_rq<M_ASYM>(p, vec, s);
+  if (method == EQ4_METHOD_GREEDY) {
+    if (b > 65535) return fail(EQ4_EUNSUPPORTED, "b > 65535 is not supported by the B200 path");
+    // loop iterations it with it <= b - b(1-r) - 3 have a condition that holds
+    // by a margin of >= 2 steps, far above float64 rounding of the row
+    // (rows where rounding could matter run exact_only).
+    double B1 = (double)b * (1.0 - r);
+    double T = (double)b - B1;
+    p.it_exact_from = std::max(0, (int)std::floor(T) - 3);
+    int ey = 0;
+    while (std::ldexp(1.0, ey) <= 15.0 * b) ey++;
+    p.qY = std::ldexp(1.0, ey - 24);
+    p.inv_qY = 1.0 / p.qY;
+    p.delta = (float)(p.qY * 0.5);
+    p.tau2 = tau2_for((int)dim);
+    // misround: the code argument alpha*s carries |error| <= eta = 4u*alpha
+    // (approximate reciprocal 2u, product/add roundings), so a code can differ
+    // from the reference's only for elements within eta of a rounding
+    // boundary, each adding <= 2*eta*W^2 to the loss; allow 2 per side, both
+    // sides.
+    p.kmis = (float)(2.0 * 2.0 * 2.0 * 4.0 * 5.9604645e-8 * 15.75);
+    return dispatch_rq<M_GREEDY>(p, vec, s);
+  }
+  if (method == EQ4_METHOD_HIST_BRUTE)
+    return fail(EQ4_EUNSUPPORTED, "hist-brute not built yet");
+  return fail(EQ4_EINVAL, "unknown method " + std::to_string(method));
+}
+
+int eq4_pack(const uint8_t* codes, int64_t rows, int64_t dim, int aux, const void* scales,
+             const void* biases, uint8_t* packed, void* stream) {
+  if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "bad shape");
+  int stride = (int)eq4_packed_row_stride(dim, aux);
+  int64_t n = rows * stride;
+  int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
+  k_pack<<<grid, 256, 0, (cudaStream_t)stream>>>(codes, rows, (int)dim, aux,
+                                                 (const uint8_t*)scales, (const uint8_t*)biases,
+                                                 packed, stride);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? EQ4_OK : cuda_fail(e, "k_pack");
+}
+
+int eq4_unpack(const uint8_t* packed, int64_t rows, int64_t dim, int aux, uint8_t* codes,
+               void* scales, void* biases, void* stream) {
+  if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "bad shape");
+  int stride = (int)eq4_packed_row_stride(dim, aux);
+  int64_t n = rows * stride;
+  int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
+  k_unpack<<<grid, 256, 0, (cudaStream_t)stream>>>(packed, rows, (int)dim, aux, codes,
+                                                   (uint8_t*)scales, (uint8_t*)biases, stride);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? EQ4_OK : cuda_fail(e, "k_unpack");
+}
+
+int eq4_quant_mse(const float* x, int64_t rows, int64_t dim, int64_t ld, const double* xmin,
+                  const double* xmax, double* out, void* stream) {
+  if (rows < 1 || dim < 1 || ld < dim) return fail(EQ4_EINVAL, "bad shape");
+  if (dim > 4096) return fail(EQ4_EUNSUPPORTED, "quant_mse: dim > 4096");
+  size_t smem = (size_t)NWARPS * MAX_LEAVES * 16 + (size_t)NWARPS * dim * 4;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_quant_mse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+  }
+  int64_t grid = std::min<int64_t>((rows + NWARPS - 1) / NWARPS, (int64_t)sm_count() * 8);
+  k_quant_mse<<<(unsigned)grid, NTHREADS, smem, (cudaStream_t)stream>>>(x, rows, (int)dim, ld, xmin,
+                                                                     xmax, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? EQ4_OK : cuda_fail(e, "k_quant_mse");
+}
+
+// Host-buffer entry point: chunks of rows are staged through device memory on
+// two streams so that the H2D copy of chunk i+1, the kernel of chunk i and
+// the D2H copy of chunk i-1 overlap (copy engines run beside the SMs).
+int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld, int method,
+                           int b, double r, int aux, uint8_t* packed, double* xmin, double* xmax,
+                           int32_t* info0, int32_t* info1, double* norm, int64_t chunk_rows,
+                           int64_t* bad_row, double* bad_lohi) {
+  if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "table must be at least 1x1");
+  if (ld < dim) return fail(EQ4_EINVAL, "ld must be >= dim");
+  if (!x || !packed) return fail(EQ4_EINVAL, "null buffer");
+  const int64_t stride = eq4_packed_row_stride(dim, aux);
+  int64_t chunk = chunk_rows > 0 ? chunk_rows : std::max<int64_t>(1024, (64ll << 20) / (dim * 4));
+  chunk = std::min(chunk, rows);
+  const int64_t nchunks = (rows + chunk - 1) / chunk;
+  const int NS = 2;
+  cudaStream_t st[NS];
+  for (int i = 0; i < NS; i++) cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking);
+  struct Buf { float* x; uint8_t* out; double* lo; double* hi; int32_t* i0; int32_t* i1; int32_t* status; };
+  Buf bf[NS];
+  memset(bf, 0, sizeof(bf));
+  int32_t* hstatus = nullptr;
+  int rc = EQ4_OK;
+  cudaError_t e = cudaMallocHost(&hstatus, sizeof(int32_t) * nchunks);
+  if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocHost");
+  const bool want_lohi = xmin != nullptr;
+  for (int i = 0; i < NS && rc == EQ4_OK; i++) {
+    e = cudaMallocAsync(&bf[i].x, chunk * dim * 4, st[i]);
+    if (e == cudaSuccess) e = cudaMallocAsync(&bf[i].out, chunk * stride, st[i]);
+    if (e == cudaSuccess) e = cudaMallocAsync(&bf[i].i0, chunk * 4, st[i]);
+    if (e == cudaSuccess) e = cudaMallocAsync(&bf[i].status, 4, st[i]);
+    if (e == cudaSuccess && info1) e = cudaMallocAsync(&bf[i].i1, chunk * 4, st[i]);
+    if (e == cudaSuccess && want_lohi) e = cudaMallocAsync(&bf[i].lo, chunk * 8, st[i]);
+    if (e == cudaSuccess && want_lohi) e = cudaMallocAsync(&bf[i].hi, chunk * 8, st[i]);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocAsync");
+  }
+  for (int64_t c = 0; c < nchunks && rc == EQ4_OK; c++) {
+    const int si = (int)(c % NS);
+    cudaStream_t s = st[si];
+    Buf& B = bf[si];
+    const int64_t r0 = c * chunk, nr = std::min(chunk, rows - r0);
+    e = cudaMemcpy2DAsync(B.x, dim * 4, x + r0 * ld, ld * 4, dim * 4, nr, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(B.status, 0, 4, s);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
+    rc = eq4_quantize_pack(B.x, nr, dim, dim, method, b, r, aux, B.out, B.lo, B.hi, B.i0, B.i1,
+                           nullptr, B.status, s);
+    if (rc) break;
+    e = cudaMemcpyAsync(packed + r0 * stride, B.out, nr * stride, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && info0) e = cudaMemcpyAsync(info0 + r0, B.i0, nr * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && info1) e = cudaMemcpyAsync(info1 + r0, B.i1, nr * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && want_lohi) e = cudaMemcpyAsync(xmin + r0, B.lo, nr * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && want_lohi) e = cudaMemcpyAsync(xmax + r0, B.hi, nr * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hstatus + c, B.status, 4, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "D2H"); break; }
+  }
+  for (int i = 0; i < NS; i++) {
+    e = cudaStreamSynchronize(st[i]);
+    if (e != cudaSuccess && rc == EQ4_OK) rc = cuda_fail(e, "stream sync");
+  }
+  // data-dependent failures: report the first failing row, like the reference's row loop
+  if (rc == EQ4_OK) {
+    for (int64_t c = 0; c < nchunks && rc == EQ4_OK; c++) {
+      if (!hstatus[c]) continue;
+      const int64_t r0 = c * chunk, nr = std::min(chunk, rows - r0);
+      int64_t first_nf = -1, first_rg = -1;
+      if (hstatus[c] & EQ4_STATUS_NONFINITE)
+        for (int64_t i = 0; i < nr && first_nf < 0; i++)
+          for (int64_t k = 0; k < dim; k++)
+            if (!std::isfinite(x[(r0 + i) * ld + k])) { first_nf = i; break; }
+      double elo = 0, ehi = 0;
+      if (hstatus[c] & EQ4_STATUS_RANGE) {
+        // re-run this chunk with per-row outputs to locate the row
+        Buf& B = bf[0];
+        double *dlo = nullptr, *dhi = nullptr;
+        cudaMallocAsync(&dlo, nr * 8, st[0]);
+        cudaMallocAsync(&dhi, nr * 8, st[0]);
+        cudaMemcpy2DAsync(B.x, dim * 4, x + r0 * ld, ld * 4, dim * 4, nr, cudaMemcpyHostToDevice, st[0]);
+        rc = eq4_quantize_pack(B.x, nr, dim, dim, method, b, r, aux, B.out, dlo, dhi, B.i0, nullptr,
+                               nullptr, nullptr, st[0]);
+        int32_t* hi0 = (int32_t*)malloc(nr * 4);
+        cudaMemcpyAsync(hi0, B.i0, nr * 4, cudaMemcpyDeviceToHost, st[0]);
+        cudaStreamSynchronize(st[0]);
+        for (int64_t i = 0; i < nr; i++)
+          if (hi0[i] == -2) { first_rg = i; break; }
+        if (first_rg >= 0) {
+          cudaMemcpy(&elo, dlo + first_rg, 8, cudaMemcpyDeviceToHost);
+          cudaMemcpy(&ehi, dhi + first_rg, 8, cudaMemcpyDeviceToHost);
+        }
+        free(hi0);
+        cudaFreeAsync(dlo, st[0]);
+        cudaFreeAsync(dhi, st[0]);
+      }
+      int64_t first = -1;
+      int code = EQ4_OK;
+      if (first_nf >= 0) { first = first_nf; code = EQ4_EDATA; }
+      if (first_rg >= 0 && (first < 0 || first_rg < first)) { first = first_rg; code = EQ4_ERANGE; }
+      if (code == EQ4_EDATA) {
+        rc = fail(EQ4_EDATA, "table contains non-finite values (NaN/Inf)");
+      } else if (code == EQ4_ERANGE) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "xmin %.17g exceeds xmax %.17g", elo, ehi);
+        rc = fail(EQ4_ERANGE, buf);
+        if (bad_lohi) { bad_lohi[0] = elo; bad_lohi[1] = ehi; }
+      }
+      if (bad_row && first >= 0) *bad_row = r0 + first;
+    }
+  }
+  for (int i = 0; i < NS; i++) {
+    cudaFreeAsync(bf[i].x, st[i]); cudaFreeAsync(bf[i].out, st[i]); cudaFreeAsync(bf[i].i0, st[i]);
+    cudaFreeAsync(bf[i].status, st[i]);
+    if (bf[i].i1) cudaFreeAsync(bf[i].i1, st[i]);
+    if (bf[i].lo) { cudaFreeAsync(bf[i].lo, st[i]); cudaFreeAsync(bf[i].hi, st[i]); }
+    cudaStreamSynchronize(st[i]);
+    cudaStreamDestroy(st[i]);
+  }
+  if (hstatus) cudaFreeHost(hstatus);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,208 @@
+// eq4_device.cuh -- device-side building blocks for the row-wise 4-bit
+// clip-search + pack kernels (sm_100a).
+//
+// Two arithmetic tiers live here:
+//  * "np_*" helpers restate the reference's float64 numpy expressions op by
+//    op with explicitly rounded intrinsics (__dadd_rn/__dmul_rn/__ddiv_rn are
+//    never contracted into FMAs), so their results are bit-identical to the
+//    reference: quant_mse (table.py:81-103), quantize_uniform
+//    (uniform.py:60-80) and numpy's pairwise np.sum order.
+//  * the search kernels evaluate the same objective approximately in fp32
+//    (see eq4.cu, "GREEDY fast path") and only fall back to the np_* tier when
+//    two competing values lie inside a proven error band.
+#pragma once
+#include <cuda_fp16.h>
+#include <cstdint>
+
+namespace eq4 {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// Exact (numpy float64) tier
+// ---------------------------------------------------------------------------
+
+// np.clip(x, lo, hi) == minimum(maximum(x, lo), hi) for finite operands.
+__device__ __forceinline__ double np_clip(double x, double lo, double hi) {
+  double t = x > lo ? x : lo;
+  return t < hi ? t : hi;
+}
+
+// uniform.py:78-79 / table.py:100-101: one code, float64, half-up rounding.
+__device__ __forceinline__ double np_code(double x, double lo, double hi, double scale) {
+  double c = np_clip(x, lo, hi);
+  double q = __ddiv_rn(__dsub_rn(c, lo), scale);
+  return np_clip(floor(__dadd_rn(q, 0.5)), 0.0, 15.0);
+}
+
+// table.py:96-103: squared reconstruction error of one element.
+// scale must be (hi - lo) / 15 (float64) unless hi == lo.
+__device__ __forceinline__ double np_err2(double x, double lo, double hi, double scale) {
+  if (hi == lo) {
+    double e = __dsub_rn(x, lo);
+    return __dmul_rn(e, e);
+  }
+  double code = np_code(x, lo, hi, scale);
+  double recon = __dadd_rn(__dmul_rn(scale, code), lo);
+  double e = __dsub_rn(x, recon);
+  return __dmul_rn(e, e);
+}
+
+// numpy pairwise-sum leaves: np.add.reduce splits n > 128 into
+// n2 = n/2 - (n/2 % 8) and n - n2 recursively; leaves have <= 128 elements.
+// Enumerate the leaves of [0, n) in order.  Returns the leaf count.
+__device__ __forceinline__ int np_leaves(int n, int* starts, int* lens, int max_leaves) {
+  int st_a[32], st_n[32];
+  int sp = 0, cnt = 0;
+  st_a[sp] = 0; st_n[sp] = n; sp++;
+  while (sp > 0) {
+    sp--;
+    int a = st_a[sp], m = st_n[sp];
+    if (m <= 128) {
+      if (cnt < max_leaves) { starts[cnt] = a; lens[cnt] = m; }
+      cnt++;
+    } else {
+      int n2 = m / 2;
+      n2 -= n2 % 8;
+      st_a[sp] = a + n2; st_n[sp] = m - n2; sp++;   // right pushed first
+      st_a[sp] = a; st_n[sp] = n2; sp++;            // left popped first
+    }
+  }
+  return cnt;
+}
+
+// Combine leaf sums in the recursion's association order.
+__device__ __noinline__ double np_combine(int n, const double* leaf_sum, int* li) {
+  if (n <= 128) return leaf_sum[(*li)++];
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  double left = np_combine(n2, leaf_sum, li);
+  double right = np_combine(n - n2, leaf_sum, li);
+  return __dadd_rn(left, right);
+}
+
+// Warp-cooperative, bit-exact quant_mse (table.py:81-103) of one row whose
+// fp32 values sit in shared memory `xs[0..d)`.  All 32 lanes must call it
+// with identical arguments; every lane returns the same value.
+// scratch: per-warp shared buffer of >= 3*max_leaves doubles/ints.
+__device__ __noinline__ double warp_np_loss(const float* xs, int d, double lo, double hi,
+                                            double* leaf_sum, int* leaf_start, int* leaf_len,
+                                            int max_leaves) {
+  const int lane = threadIdx.x & 31;
+  double scale = (hi == lo) ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+  if (d < 8) {  // numpy: res = 0.; res += a[i] sequentially
+    double res = 0.0;
+    if (lane == 0)
+      for (int i = 0; i < d; i++) res = __dadd_rn(res, np_err2((double)xs[i], lo, hi, scale));
+    res = __shfl_sync(FULL, res, 0);
+    return __dadd_rn(0.0, res);
+  }
+  int nl = np_leaves(d, leaf_start, leaf_len, max_leaves);
+  __syncwarp();
+  const int g = lane >> 3, m = lane & 7;
+  for (int base = 0; base < nl; base += 4) {
+    int li = base + g;
+    bool ok = li < nl;
+    int a = ok ? leaf_start[li] : 0;
+    int len = ok ? leaf_len[li] : 8;
+    int nfull = len - (len % 8);
+    // chain m: r[m] = a[m] + a[m+8] + ... (sequential), loops_utils.h.src
+    double r = ok ? np_err2((double)xs[a + m], lo, hi, scale) : 0.0;
+    for (int i = 8 + m; i < nfull; i += 8)
+      r = __dadd_rn(r, np_err2((double)xs[a + i], lo, hi, scale));
+    // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)); a+b == b+a bitwise
+    r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 4));
+    if (ok && m == 0) {
+      for (int i = nfull; i < len; i++) r = __dadd_rn(r, np_err2((double)xs[a + i], lo, hi, scale));
+      leaf_sum[li] = r;
+    }
+  }
+  __syncwarp();
+  double total = 0.0;
+  if (lane == 0) {
+    int li = 0;
+    total = np_combine(d, leaf_sum, &li);
+  }
+  total = __shfl_sync(FULL, total, 0);
+  return __dadd_rn(0.0, total);
+}
+
+// ---------------------------------------------------------------------------
+// Codes for the final quantize pass (uniform.py:77-79), fast path + exact fix-up
+// ---------------------------------------------------------------------------
+
+struct CodeParams {
+  double lo, hi, scale;   // float64 range and (hi - lo) / 15
+  float lo_rd, hi_ru;     // largest float <= lo, smallest float >= hi
+  float lo_hi, lo_lo;     // lo split as float hi + float lo
+  float inv;              // ~15 / (hi - lo)
+  bool degenerate;        // hi == lo  -> all codes 0 (uniform.py:74-76)
+  bool slow;              // range too extreme for the fp32 estimate
+};
+
+__device__ __forceinline__ CodeParams make_code_params(double lo, double hi) {
+  CodeParams p;
+  p.lo = lo;
+  p.hi = hi;
+  p.degenerate = (hi == lo);
+  p.scale = p.degenerate ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+  p.lo_rd = __double2float_rd(lo);
+  p.hi_ru = __double2float_ru(hi);
+  p.lo_hi = __double2float_rn(lo);
+  p.lo_lo = __double2float_rn(__dsub_rn(lo, (double)p.lo_hi));
+  double w = __dsub_rn(hi, lo);
+  p.inv = p.degenerate ? 0.f : __double2float_rn(15.0 / w);
+  // fp32 estimate needs a normal, finite reciprocal and range
+  p.slow = !p.degenerate && !(w > 1e-30 && w < 1e30 && fabs(lo) < 1e30 && fabs(hi) < 1e30);
+  return p;
+}
+
+// Code of x under (lo, hi): exact numpy semantics.  The fp32 estimate
+// t' = (x - lo) * 15/(hi-lo) + 0.5 has absolute error < 4e-6 for interior x
+// (|t'| < 16, three roundings of relative 2^-24 each on the range-scaled
+// quantities); when frac(t') is within NEAR of an integer the float64 codec
+// decides.  x <= lo gives code 0 and x >= hi code 15 exactly in the
+// reference (clip then floor(0 + .5) / floor(15 +- 1ulp + .5)).
+constexpr float NEAR = 1e-5f;
+
+__device__ __forceinline__ unsigned code_of(float x, const CodeParams& p, bool& need_exact) {
+  need_exact = false;
+  if (p.degenerate) return 0u;
+  if (x <= p.lo_rd) return 0u;
+  if (x >= p.hi_ru) return 15u;
+  if (p.slow) { need_exact = true; return 0u; }
+  float dlt = __fadd_rn(__fadd_rn(x, -p.lo_hi), -p.lo_lo);
+  float u = __fmaf_rn(dlt, p.inv, 0.5f);
+  float m = __fadd_rd(u, 8388608.f);            // 2^23 + floor(u)
+  float cf = __fadd_rn(m, -8388608.f);
+  float g = __fadd_rn(__fadd_rn(u, -cf), -0.5f); // frac(u) - 0.5
+  if (fabsf(g) > 0.5f - NEAR || cf < 0.f || cf > 15.f) need_exact = true;
+  return (unsigned)__float_as_uint(m) & 0xFu;
+}
+
+__device__ __forceinline__ unsigned code_exact(float x, const CodeParams& p) {
+  if (p.degenerate) return 0u;
+  return (unsigned)np_code((double)x, p.lo, p.hi, p.scale);
+}
+
+// Stored scale/bias bit patterns (uniform.py:80 dtype(scale), dtype(xmin)):
+// np.float16(double) and np.float32(double) both round once, to nearest-even.
+// The f16 bits leave the conversion through an opaque move: nvcc 12.9 folds
+// "cvt.rn.f16.f64 -> bits -> (uint8_t)(bits & 0xff)" into a numeric
+// F2I.U8.F16 conversion, which is wrong for a bit-pattern extraction.
+__device__ __forceinline__ uint32_t aux_bits_f16(double v) {
+  unsigned short h;
+  asm("cvt.rn.f16.f64 %0, %1;" : "=h"(h) : "d"(v));
+  uint32_t r;
+  asm volatile("cvt.u32.u16 %0, %1;" : "=r"(r) : "h"(h));
+  return r;
+}
+__device__ __forceinline__ uint32_t aux_bits_f32(double v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "f"(__double2float_rn(v)));
+  return r;
+}
+
+}  // namespace eq4

@@ -1,0 +1,186 @@
+"""GPU parity: libeq4.so (through the C ABI) against the reference fixtures and the C oracle.
+
+Bar (BASELINE.json north_star): packed bytes bit-exact; thresholds equal
+(float64, we require exact equality -- stricter than the 1e-6 relative bar);
+the only allowed exceptions would be rows whose reference competing losses tie
+within 1e-6 -- the exact re-decision path makes even those match, so every
+test here demands zero mismatching rows.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import rng
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+G = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def eq():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1911_02079_b200 as eq
+
+    eq.load()
+    return eq
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def _run(eq, x, method, aux="fp16", b=200, r=0.16):
+    p, rr = eq.quantize_pack_table4(_dev(x), method, aux, b, r, with_rows=True)
+    return p.buffer, rr.xmin.cpu().numpy(), rr.xmax.cpu().numpy(), rr.info0.cpu().numpy()
+
+
+def _mismatch_rows(a, b, stride):
+    a = a.reshape(-1, stride)
+    b = b.reshape(-1, stride)
+    return np.nonzero((a != b).any(1))[0]
+
+
+def test_config1_golden(eq):
+    f = np.load(os.path.join(G, "config1.npz"))
+    x = rng.sample_table("gaussian", 0.0, 1.0, 1911, 10000, 64)
+    buf, lo, hi, it = _run(eq, x, "greedy", "fp16")
+    assert _mismatch_rows(buf, f["greedy_fp16_packed"], 36).size == 0
+    assert np.array_equal(lo, f["greedy_lo"]) and np.array_equal(hi, f["greedy_hi"])
+    assert np.array_equal(np.where(it < 0, 0, 1 + 2 * it), f["greedy_evals"])
+    buf32, _, _, _ = _run(eq, x, "greedy", "fp32")
+    assert np.array_equal(buf32, f["greedy_fp32_packed"])
+    for aux in ("fp16", "fp32"):
+        b2, _, _, _ = _run(eq, x, "asym", aux)
+        assert np.array_equal(b2, f[f"asym_{aux}_packed"]), aux
+
+
+def test_edge_golden(eq):
+    f = np.load(os.path.join(G, "edge.npz"))
+    meta = json.loads(str(f["meta"]))
+    for k, m in enumerate(meta):
+        x = f[f"x_{k}"]
+        for aux in ("fp16", "fp32"):
+            b2, _, _, _ = _run(eq, x, "asym", aux)
+            assert np.array_equal(b2, f[f"asym_{aux}_{k}"]), (m["name"], aux)
+            if m["greedy_error"]:
+                with pytest.raises(ValueError, match="exceeds xmax"):
+                    eq.quantize_pack_table4(_dev(x), "greedy", aux, m["b"], m["r"])
+                continue
+            buf, lo, hi, it = _run(eq, x, "greedy", aux, m["b"], m["r"])
+            assert np.array_equal(buf, f[f"greedy_{aux}_{k}"]), (m["name"], aux)
+            assert np.array_equal(lo, f[f"greedy_lo_{k}"]), m["name"]
+            assert np.array_equal(hi, f[f"greedy_hi_{k}"]), m["name"]
+            assert np.array_equal(np.where(it < 0, 0, 1 + 2 * it), f[f"greedy_evals_{k}"]), m["name"]
+
+
+def test_quant_mse_golden(eq):
+    f = np.load(os.path.join(G, "quant_mse.npz"))
+    off = 0
+    for i, d in enumerate(f["dims"]):
+        x = f["x"][off:off + d]
+        off += d
+        if f["nbits"][i] != 4:
+            continue
+        got = eq.quant_mse_rows(_dev(x[None]), [f["lo"][i]], [f["hi"][i]])[0].item()
+        assert got == f["value"][i], (i, d)
+
+
+@pytest.mark.parametrize("d", [16, 32, 64, 128, 256, 512, 1024, 2048, 7, 17, 33, 100, 129, 300])
+def test_greedy_dims_vs_oracle(eq, d):
+    rows = max(64, 200_000 // d)
+    x = rng.sample_table("gaussian", 0.0, 1.0, 4000 + d, rows, d)
+    want = oracle.quantize_pack_table(x, "greedy", 200, 0.16, "fp16")
+    buf, lo, hi, it = _run(eq, x, "greedy", "fp16")
+    bad = _mismatch_rows(buf, want.packed, eq.packed_row_stride(d, "fp16"))
+    assert bad.size == 0, (d, bad[:10])
+    assert np.array_equal(lo, want.xmin) and np.array_equal(hi, want.xmax)
+    assert np.array_equal(it, want.info0)
+
+
+def test_greedy_mixed_d128_vs_oracle(eq):
+    x = rng.mixed_table(60_000, 128, 31)
+    want = oracle.quantize_pack_table(x, "greedy", 200, 0.16, "fp16")
+    buf, lo, hi, _ = _run(eq, x, "greedy", "fp16")
+    assert _mismatch_rows(buf, want.packed, 68).size == 0
+    assert np.array_equal(lo, want.xmin) and np.array_equal(hi, want.xmax)
+
+
+def test_greedy_gaussian_200k_vs_oracle(eq):
+    x = rng.sample_table("gaussian", 0.0, 1.0, 77, 200_000, 64)
+    want = oracle.quantize_pack_table(x, "greedy", 200, 0.16, "fp16")
+    buf, lo, hi, _ = _run(eq, x, "greedy", "fp16")
+    bad = _mismatch_rows(buf, want.packed, 36)
+    assert bad.size == 0, bad[:10]
+    assert np.array_equal(lo, want.xmin) and np.array_equal(hi, want.xmax)
+
+
+@pytest.mark.parametrize("d", [16, 64, 128, 2048, 5, 31, 65])
+def test_asym_dims_vs_oracle(eq, d):
+    x = rng.sample_table("laplacian", 0.0, 1.0, 900 + d, max(64, 400_000 // d), d)
+    for aux in ("fp16", "fp32"):
+        want = oracle.quantize_pack_table(x, "asym", aux=aux)
+        buf, lo, hi, _ = _run(eq, x, "asym", aux)
+        assert np.array_equal(buf, want.packed), (d, aux)
+        assert np.array_equal(lo, want.xmin)
+
+
+def test_host_path_equals_device_path(eq):
+    x = rng.mixed_table(70_001, 64, 5)
+    dev, _ = eq.quantize_pack_table4(_dev(x), "greedy", "fp16")
+    host, rr = eq.quantize_pack_table4(x, "greedy", "fp16", with_rows=True)
+    assert np.array_equal(dev.buffer, host.buffer)
+    want = oracle.quantize_pack_table(x[:5000], "greedy", 200, 0.16, "fp16")
+    assert np.array_equal(host.buffer[:5000 * 36], want.packed)
+    assert np.array_equal(rr.xmin[:5000], want.xmin)
+
+
+def test_public_api_drop_in(eq):
+    x = rng.sample_table("gaussian", 0.0, 1.0, 12, 300, 64)
+    t = eq.EmbeddingTable(x)
+    c = eq.WorkCounters()
+    q = eq.quantize_table(t, "greedy", 4, "fp16", counters=c)
+    want = oracle.quantize_pack_table(x, "greedy", 200, 0.16, "fp16")
+    assert np.array_equal(eq.pack_table4(q).buffer, want.packed)
+    assert c.loss_evals == int(np.sum(1 + 2 * want.info0))
+    # UniformQuantTable view decodes on the GPU and matches the oracle codec
+    codes, sc, bi = oracle.quantize_uniform(x[3], want.xmin[3], want.xmax[3], 4, "fp16")
+    assert np.array_equal(q.codes[3], codes) and q.scales[3] == sc and q.biases[3] == bi
+    # repacking a reference-style table goes through the GPU pack kernel
+    q2 = eq.UniformQuantTable(q.codes, q.scales, q.biases, 4, "fp16")
+    assert np.array_equal(eq.pack_table4(q2).buffer, want.packed)
+    r = eq.clip_range_greedy(x[5])
+    assert (r.xmin, r.xmax) == (want.xmin[5], want.xmax[5])
+    assert eq.clip_range_asym([-3.0, 1.0]) == eq.ClipRange(-3.0, 1.0)
+    assert eq.clip_range_greedy(np.arange(16.0), 4) == eq.ClipRange(0.0, 15.0)
+    assert eq.clip_range_greedy([4.0, 4.0], 4) == eq.ClipRange(4.0, 4.0)
+    assert eq.quant_mse([0.5], eq.ClipRange(0.0, 15.0), 4) == 0.25
+
+
+def test_nonfinite_rejected_on_device(eq):
+    x = np.ones((40, 64), np.float32)
+    x[17, 3] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        eq.quantize_pack_table4(_dev(x), "greedy", "fp16")
+    with pytest.raises(ValueError, match="non-finite"):
+        eq.quantize_pack_table4(x, "asym", "fp16")
+
+
+def test_pack_unpack_roundtrip(eq):
+    r = np.random.default_rng(0)
+    for d in (1, 7, 64, 129):
+        codes = r.integers(0, 16, size=(50, d)).astype(np.uint8)
+        sc = r.uniform(0.01, 2, 50).astype(np.float16)
+        bi = r.uniform(-3, 3, 50).astype(np.float16)
+        q = eq.UniformQuantTable(codes, sc, bi, 4, "fp16")
+        p = eq.pack_table4(q)
+        assert np.array_equal(p.buffer, oracle.pack_table4(codes, sc, bi, "fp16"))
+        c2, s2, b2 = p.unpack()
+        assert np.array_equal(c2.cpu().numpy(), codes)
+        assert np.array_equal(s2.cpu().numpy(), sc) and np.array_equal(b2.cpu().numpy(), bi)
