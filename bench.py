@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""Benchmark: 4-bit GREEDY row-wise quantization (b=200, r=0.16) of a 20M x 64 fp32 table.
+
+BASELINE.json metric: "rows/sec and GB/s for 4-bit GREEDY rowwise quant
+(20M x 64 fp32); % roofline" on config 5b (20,000,000 x 64, mixed
+"trained-embedding" distribution).  One step = one fused pass of the hot path
+(clip search + quantize + nibble pack + fp16 scale/bias) over the whole table
+resident in HBM.  Prints ONE JSON line (rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one process per GPU; every rank quantizes its own
+20M-row table (rows are independent: weak scaling, no collective on the data
+path) and the step time is the max over ranks.  ``--impl reference`` times the
+reference algorithm on the host CPU (the C restatement in oracle/, all host
+threads) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rows/sec and GB/s for 4-bit GREEDY rowwise quant (20M×64 fp32); % roofline"
+ROWS, DIM, B, R, AUX = 20_000_000, 64, 200, 0.16, "fp16"
+FLOP_PER_ELEM_EVAL = 13   # table.py:100-103 literal ops
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        load = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_reference_rate(rows_sample: int, seed: int = 1911, steps: int = 1, warmup: int = 0):
+    """GREEDY b=200 r=0.16 fp16 on the host (oracle C port, all threads): rows/s."""
+    import oracle
+    from oracle import rng
+
+    x = rng.mixed_table(rows_sample, DIM, seed)
+    nthreads = oracle.max_threads()
+    for _ in range(warmup):
+        oracle.quantize_pack_table(x[: max(1, rows_sample // 10)], "greedy", B, R, AUX, nthreads)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        oracle.quantize_pack_table(x, "greedy", B, R, AUX, nthreads)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    return rows_sample / t, nthreads, t
+
+
+def run_reference(args, rank: int):
+    if rank != 0:
+        return
+    sample = args.cpu_rows
+    rate, cores, t = cpu_reference_rate(sample, steps=args.steps, warmup=min(args.warmup, 1))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "rows/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "GREEDY b=200 r=0.16 fp16-aux, 20M x 64 mixed (config 5b); "
+                               f"each step a {sample}-row sample on the host",
+                   "rows": ROWS, "dim": DIM, "b": B, "r": R, "aux": AUX},
+        "cpu_baseline": {"value": rate, "unit": "rows/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} rows x {DIM} of the mixed generator "
+                                   "(oracle/eq4_oracle.c restatement of the reference, "
+                                   f"{cores} OpenMP threads)"},
+        "e2e": {"value": rate, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank: int, world: int):
+    import torch
+
+    import paper_1911_02079_b200 as eq
+    from paper_1911_02079_b200 import workloads
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    rows = args.rows
+    stride = eq.packed_row_stride(DIM, AUX)
+    x = workloads.mixed_table(rows, DIM, seed=1911 + rank, device=dev)
+    out = torch.empty(rows * stride, dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        eq.quantize_pack_table4(x, "greedy", AUX, B, R, out=out, status=status, stream=stream,
+                                check=False)
+
+    # algorithmic work: per-row loss evaluations from one untimed launch
+    rr = eq.RowResults(None, None, torch.empty(rows, dtype=torch.int32, device=dev), None, None)
+    eq.quantize_pack_table4(x, "greedy", AUX, B, R, out=out, rows_out=rr, stream=stream)
+    it = rr.info0.to(torch.int64)
+    evals = int(torch.where(it >= 0, 1 + 2 * it, torch.zeros_like(it)).sum().item())
+    del rr, it
+    flop_per_step = float(FLOP_PER_ELEM_EVAL) * DIM * evals
+    bytes_per_step = float(rows) * (4 * DIM + (DIM + 1) // 2 + 4)
+
+    for _ in range(args.warmup):
+        step()
+    dist = world > 1
+    if dist:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    if dist:
+        torch.distributed.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    st = int(status.item())
+    if st:
+        raise SystemExit(f"kernel status {st}: data error in the bench table")
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * rows / (ms * 1e-3)
+
+    # end to end through the public API: pinned host table in, packed bytes out
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty((rows, DIM), dtype=torch.float32, pin_memory=True)
+        xh.copy_(x)
+        oh = torch.empty(rows * stride, dtype=torch.uint8, pin_memory=True)
+        table = eq.EmbeddingTable(xh.numpy())   # validated once, like the reference's constructor
+        del x
+        torch.cuda.empty_cache()
+        outh = oh.numpy()
+        eq.quantize_pack_table4(table, "greedy", AUX, B, R, out=outh)
+        if dist:
+            torch.distributed.barrier()
+        e_steps = max(1, min(args.steps, args.e2e_steps))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            eq.quantize_pack_table4(table, "greedy", AUX, B, R, out=outh)
+        te = (time.perf_counter() - t0) / e_steps
+        if dist:
+            tt = torch.tensor([te], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": world * rows / te, "unit": "rows/s", "ms_per_step": te * 1e3,
+               "h2d_bytes_per_step": rows * DIM * 4, "d2h_bytes_per_step": rows * stride,
+               "path": "quantize_pack_table4(EmbeddingTable(pinned host), 'greedy', 'fp16') -> "
+                       "eq4_quantize_pack_host (chunked H2D/kernel/D2H overlap)"}
+
+    if rank != 0:
+        return
+    peaks = _peaks()
+    props = torch.cuda.get_device_properties(dev)
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
+    achieved = flop_per_step / (ms * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("greedy_20Mx64", {}).get("dram_bytes_per_launch")
+    cpu = None
+    if not args.no_cpu:
+        rate, cores, t = cpu_reference_rate(args.cpu_rows)
+        cpu = {"value": rate, "unit": "rows/s", "cores": cores, "kind": "port",
+               "sample": f"{args.cpu_rows} rows x {DIM} mixed, GREEDY b=200 r=0.16 fp16 "
+                         f"(oracle C restatement, {cores} threads, {t:.1f} s)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 (f64 exact re-decisions)", "data": "synthetic",
+        "config": {"workload": "GREEDY b=200 r=0.16 fp16-aux on 20,000,000 x 64 fp32 (config 5b, "
+                               "mixed trained-embedding generator) per GPU",
+                   "rows_per_gpu": rows, "dim": DIM, "b": B, "r": R, "aux": AUX,
+                   "l2": "input 5.12 GB per GPU >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"row-sharded x{world}, no data-path collective"},
+        "input_GBps": world * rows * DIM * 4 / (ms * 1e-3) / 1e9,
+        "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp32_peak, "traffic": traffic,
+                     "peak_source": "derived: SMs x 128 FP32 lanes x 2 x sm_max_mhz "
+                                    "(MEASURED_PEAKS.json has no FP32 figure)",
+                     "work": f"13 FLOP x d x loss evaluations ({evals} evals/step)",
+                     "hbm_floor_ms": bytes_per_step / (float(peaks.get('hbm_gbs', 6546.9)) * 1e9) * 1e3},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "clocks": clocks.summary(),
+    }
+    if args.secondary:
+        line["secondary"] = secondary(eq, workloads, torch, dev, peaks)
+    print(json.dumps(line), flush=True)
+
+
+def secondary(eq, workloads, torch, dev, peaks):
+    """Config 2 (ASYM 4M x 64 HBM path) and config 3 (GREEDY 4M x 128 mixed), device-timed."""
+    res = {}
+    for name, method, rows, d, gen in (("asym_4Mx64_config2", "asym", 4_194_304, 64, "gauss"),
+                                       ("greedy_4Mx128_mixed_config3", "greedy", 4_194_304, 128, "mixed")):
+        x = (workloads.gaussian_table if gen == "gauss" else workloads.mixed_table)(rows, d, 7, device=dev)
+        st = torch.zeros(1, dtype=torch.int32, device=dev)
+        out = torch.empty(rows * eq.packed_row_stride(d, AUX), dtype=torch.uint8, device=dev)
+        f = lambda: eq.quantize_pack_table4(x, method, AUX, B, R, out=out, status=st, check=False)
+        for _ in range(3):
+            f()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        n = 10
+        e0.record()
+        for _ in range(n):
+            f()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / n
+        byt = rows * (4 * d + (d + 1) // 2 + 4)
+        r = {"ms": ms, "rows_per_s": rows / ms * 1e3, "GBps": byt / ms / 1e6}
+        if method == "asym":
+            r["hbm_frac"] = r["GBps"] / float(peaks.get("hbm_gbs", 6546.9))
+        res[name] = r
+        del x, out
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--rows", type=int, default=ROWS)
+    ap.add_argument("--cpu-rows", type=int, default=200_000)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--secondary", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        torch.distributed.init_process_group("nccl")
+    try:
+        run_ours(args, rank, world)
+    finally:
+        if world > 1:
+            import torch
+
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
