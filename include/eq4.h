@@ -112,6 +112,11 @@ int eq4_unpack(const uint8_t *packed, int64_t rows, int64_t dim, int aux, uint8_
 int eq4_quant_mse(const float *x, int64_t rows, int64_t dim, int64_t ld, const double *xmin,
                   const double *xmax, double *out, void *stream);
 
+/* Diagnostics: internal arithmetic self-test on the current device (mismatch
+ * count, -1 on CUDA error).  which 0/1: the divide-free float64 w/15 used for
+ * scales against the IEEE divide, on float differences / full-range doubles. */
+long long eq4_selftest(int which, int64_t n, uint64_t seed);
+
 #ifdef __cplusplus
 }
 #endif

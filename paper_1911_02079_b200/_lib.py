@@ -36,6 +36,7 @@ EXPORTS = (
     "eq4_pack",
     "eq4_unpack",
     "eq4_quant_mse",
+    "eq4_selftest",
 )
 
 _lib = None
@@ -76,6 +77,8 @@ def load() -> ctypes.CDLL:
         L.eq4_unpack.restype = i32
         L.eq4_quant_mse.argtypes = [vp, i64, i64, i64, vp, vp, vp, vp]
         L.eq4_quant_mse.restype = i32
+        L.eq4_selftest.argtypes = [i32, i64, ctypes.c_uint64]
+        L.eq4_selftest.restype = ctypes.c_longlong
         _lib = L
     return _lib
 

@@ -296,6 +296,71 @@ __device__ __forceinline__ void store_tile(const Params& p, const uint8_t* codes
   __syncthreads();
 }
 
+// ASYM codes + aux for the vector path: lo = min, hi = max are floats, so
+// every element is interior and the code is floor(t + 1/2) with
+// t = (x - min) * 15/(max - min) evaluated in fp32 (|error| <= 90u < NEAR,
+// see code_of); near-boundary elements (|frac(t) - 1/2| < NEAR) take the float64
+// codec.  6 FMA-pipe + 1 ALU instruction per element, 1 ALU per 4 for packing.
+template <int LPR, int E>
+__device__ __forceinline__ void emit_asym_vec(const Params& p, const float (&v)[E], float mn,
+                                              float mx, bool ok, bool rvalid, int q, uint8_t* orow) {
+  const float w32 = __fadd_rn(mx, -mn);
+  const bool degenerate = !(mn != mx);                 // uniform.py:74-76 (also NaN rows)
+  const bool fast = ok && w32 > 1e-30f && w32 < 1e30f;
+  const float inv = fast ? __fdividef(15.f, w32) : 0.f;
+  float gmax = 0.f;
+#pragma unroll
+  for (int c = 0; c < E / 4; ++c) {
+    uint32_t mb[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float t = __fmul_rn(__fadd_rn(v[4 * c + k], -mn), inv);
+      const float m = __fadd_rd(__fadd_rn(t, 0.5f), MAGIC);   // 2^23 + floor(t + 1/2)
+      const float g = __fadd_rn(t, -__fadd_rn(m, -MAGIC));
+      gmax = fmaxf(gmax, fabsf(g));
+      mb[k] = __float_as_uint(m);
+    }
+    const uint32_t lo8 = (mb[0] & 0xFu) | ((mb[1] & 0xFu) << 4);
+    const uint32_t hi8 = (mb[2] & 0xFu) | ((mb[3] & 0xFu) << 4);
+    if (rvalid) *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = (uint16_t)(lo8 | (hi8 << 8));
+  }
+  const bool need = rvalid && ok && !degenerate && (!fast || gmax > 0.5f - NEAR);
+  if (__any_sync(FULL, need)) {   // rare: float64 codec (uniform.py:77-79) for flagged elements
+    if (need) {
+      const CodeParams cp = make_code_params((double)mn, (double)mx);
+      for (int i = 0; i < E; ++i) {
+        const float t = __fmul_rn(__fadd_rn(v[i], -mn), inv);
+        const float m = __fadd_rd(__fadd_rn(t, 0.5f), MAGIC);
+        const float g = __fadd_rn(t, -__fadd_rn(m, -MAGIC));
+        if (fast && !(fabsf(g) > 0.5f - NEAR)) continue;
+        const unsigned cc = code_exact(v[i], cp);
+        const int byte = 2 * (q + LPR * (i >> 2)) + ((i & 3) >> 1);
+        const int sh = (i & 1) * 4;
+        orow[byte] = (uint8_t)((orow[byte] & ~(0xF << sh)) | (cc << sh));
+      }
+    }
+  }
+  if (degenerate && rvalid) {
+#pragma unroll
+    for (int c = 0; c < E / 4; ++c) *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = 0;
+  }
+  if (q == 0 && rvalid) {
+    const double sc = (ok && !degenerate) ? div15(__dsub_rn((double)mx, (double)mn)) : 0.0;
+    uint8_t* a = orow + p.half;
+    if (p.aux == EQ4_AUX_FP16) {
+      const uint32_t w = aux_bits_f16(sc) | (aux_bits_f16((double)mn) << 16);
+      *reinterpret_cast<uint16_t*>(a) = (uint16_t)w;
+      *reinterpret_cast<uint16_t*>(a + 2) = (uint16_t)(w >> 16);
+    } else {
+      const uint32_t s32 = aux_bits_f32(sc), b32 = aux_bits_f32((double)mn);
+      *reinterpret_cast<uint16_t*>(a) = (uint16_t)s32;
+      *reinterpret_cast<uint16_t*>(a + 2) = (uint16_t)(s32 >> 16);
+      *reinterpret_cast<uint16_t*>(a + 4) = (uint16_t)b32;
+      *reinterpret_cast<uint16_t*>(a + 6) = (uint16_t)(b32 >> 16);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // ASYM: min/max -> codes -> pack (HBM-bound streaming kernel)
 // ---------------------------------------------------------------------------
@@ -331,8 +396,11 @@ k_asym(const Params p) {
     bool bad;
     row_minmax<LPR, E, VEC>(p, v, nv, rvalid, q, mn, mx, bad);
     const double lo = (double)mn, hi = (double)mx;   // clipping.py:61
-    emit_row<LPR, E, VEC>(p, v, nv, lo, hi, !bad, rvalid, q, out_tile + g * p.stride,
-                          codes_s + g * L::D);
+    if (VEC)
+      emit_asym_vec<LPR, E>(p, v, mn, mx, !bad, rvalid, q, out_tile + g * p.stride);
+    else
+      emit_row<LPR, E, VEC>(p, v, nv, lo, hi, !bad, rvalid, q, out_tile + g * p.stride,
+                            codes_s + g * L::D);
     if (rvalid) {
       if (q == 0) {
         if (p.lo_out) { p.lo_out[row] = lo; p.hi_out[row] = hi; }
@@ -719,6 +787,31 @@ __global__ void __launch_bounds__(NTHREADS) k_quant_mse(const float* x, int64_t 
   }
 }
 
+// Self-test kernel: div15 (Markstein) against the IEEE divide on n values.
+// which = 0: w = |f1 - f0| of random floats (the values div15 sees);
+// which = 1: random doubles over the whole normal exponent range.
+__global__ void k_selftest_div15(int which, int64_t n, uint64_t seed, unsigned long long* bad) {
+  unsigned long long local = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    double w;
+    if (which == 0) {
+      float a = __uint_as_float((uint32_t)z & 0xBFFFFFFFu);   // finite floats, both signs
+      float b = __uint_as_float((uint32_t)(z >> 32) & 0xBFFFFFFFu);
+      w = fabs((double)a - (double)b);
+    } else {
+      w = __longlong_as_double((long long)((z & 0x000FFFFFFFFFFFFFull) |
+                                           ((uint64_t)(1 + (z >> 52) % 2045) << 52)));
+    }
+    if (__double_as_longlong(div15(w)) != __double_as_longlong(__ddiv_rn(w, 15.0))) local++;
+  }
+  if (local) atomicAdd(bad, local);
+}
+
 }  // namespace eq4
 
 // ===========================================================================
@@ -848,7 +941,9 @@ int eq4_quantize_pack(const float* x, int64_t rows, int64_t dim, int64_t ld, int
   p.half = (int)((dim + 1) / 2);
   p.packed = packed; p.lo_out = xmin; p.hi_out = xmax; p.info0 = info0; p.info1 = info1;
   p.status = status;
-  const bool vec = (dim % 4 == 0) && (ld % 4 == 0) && (((uintptr_t)x & 15) == 0);
+  // vector path: 16-byte aligned rows in, 2-byte aligned packed rows out
+  const bool vec = (dim % 4 == 0) && (ld % 4 == 0) && (((uintptr_t)x & 15) == 0) &&
+                   (((uintptr_t)packed & 1) == 0);
   if (method == EQ4_METHOD_ASYM) return dispatch_rq<M_ASYM>(p, vec, s);
   if (method == EQ4_METHOD_GREEDY) {
     if (b > 65535) return fail(EQ4_EUNSUPPORTED, "b > 65535 is not supported by the B200 path");
@@ -1035,6 +1130,21 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
   }
   if (hstatus) cudaFreeHost(hstatus);
   return rc;
+}
+
+// Diagnostics: run an internal arithmetic self-test on the current device and
+// return the mismatch count (-1 on CUDA error).  which: 0/1 = div15 vs IEEE
+// divide on float-difference / full-range doubles.
+long long eq4_selftest(int which, int64_t n, uint64_t seed) {
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, 8) != cudaSuccess) return -1;
+  cudaMemset(d, 0, 8);
+  k_selftest_div15<<<sm_count() * 8, 256>>>(which, n, seed, d);
+  unsigned long long h = 0;
+  cudaError_t e = cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) { cuda_fail(e, "selftest"); return -1; }
+  return (long long)h;
 }
 
 }  // extern "C"

@@ -133,6 +133,16 @@ __device__ __noinline__ double warp_np_loss(const float* xs, int d, double lo, d
 // Codes for the final quantize pass (uniform.py:77-79), fast path + exact fix-up
 // ---------------------------------------------------------------------------
 
+// Correctly rounded w / 15 in float64 without a divide: q = RN(w * RN(1/15)),
+// r = w - 15 q (exact by FMA), RN(q + r * RN(1/15)) = RN(w / 15) (Markstein's
+// correction step; checked against __ddiv_rn by eq4_selftest).
+__device__ __forceinline__ double div15(double w) {
+  const double y = 0.06666666666666666666;          // RN(1/15)
+  const double q = __dmul_rn(w, y);
+  const double r = __fma_rn(-q, 15.0, w);
+  return __fma_rn(r, y, q);
+}
+
 struct CodeParams {
   double lo, hi, scale;   // float64 range and (hi - lo) / 15
   float lo_rd, hi_ru;     // largest float <= lo, smallest float >= hi
@@ -147,13 +157,13 @@ __device__ __forceinline__ CodeParams make_code_params(double lo, double hi) {
   p.lo = lo;
   p.hi = hi;
   p.degenerate = (hi == lo);
-  p.scale = p.degenerate ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+  p.scale = p.degenerate ? 0.0 : div15(__dsub_rn(hi, lo));
   p.lo_rd = __double2float_rd(lo);
   p.hi_ru = __double2float_ru(hi);
   p.lo_hi = __double2float_rn(lo);
   p.lo_lo = __double2float_rn(__dsub_rn(lo, (double)p.lo_hi));
   double w = __dsub_rn(hi, lo);
-  p.inv = p.degenerate ? 0.f : __double2float_rn(15.0 / w);
+  p.inv = p.degenerate ? 0.f : __fdividef(15.f, __double2float_rn(w));
   // fp32 estimate needs a normal, finite reciprocal and range
   p.slow = !p.degenerate && !(w > 1e-30 && w < 1e30 && fabs(lo) < 1e30 && fabs(hi) < 1e30);
   return p;
@@ -168,18 +178,19 @@ __device__ __forceinline__ CodeParams make_code_params(double lo, double hi) {
 constexpr float NEAR = 1e-5f;
 
 __device__ __forceinline__ unsigned code_of(float x, const CodeParams& p, bool& need_exact) {
-  need_exact = false;
-  if (p.degenerate) return 0u;
-  if (x <= p.lo_rd) return 0u;
-  if (x >= p.hi_ru) return 15u;
-  if (p.slow) { need_exact = true; return 0u; }
-  float dlt = __fadd_rn(__fadd_rn(x, -p.lo_hi), -p.lo_lo);
-  float u = __fmaf_rn(dlt, p.inv, 0.5f);
-  float m = __fadd_rd(u, 8388608.f);            // 2^23 + floor(u)
-  float cf = __fadd_rn(m, -8388608.f);
-  float g = __fadd_rn(__fadd_rn(u, -cf), -0.5f); // frac(u) - 0.5
-  if (fabsf(g) > 0.5f - NEAR || cf < 0.f || cf > 15.f) need_exact = true;
-  return (unsigned)__float_as_uint(m) & 0xFu;
+  // branch-free: every element runs the same instruction stream
+  const float dlt = __fadd_rn(__fadd_rn(x, -p.lo_hi), -p.lo_lo);
+  const float t = __fmul_rn(dlt, p.inv);
+  const float u = __fadd_rn(t, 0.5f);
+  const float m = __fadd_rd(u, 8388608.f);          // 2^23 + floor(u)
+  const float cf = __fadd_rn(m, -8388608.f);
+  const float g = __fadd_rn(t, -cf);                // in [-1/2, 1/2) unless near a boundary
+  const bool below = x <= p.lo_rd, above = x >= p.hi_ru;
+  const bool interior = !below && !above && !p.degenerate;
+  need_exact = interior && (p.slow || fabsf(g) > 0.5f - NEAR || cf < 0.f || cf > 15.f);
+  unsigned c = (unsigned)__float_as_uint(m) & 0xFu;
+  c = above ? 15u : c;
+  return (below || p.degenerate) ? 0u : c;
 }
 
 __device__ __forceinline__ unsigned code_exact(float x, const CodeParams& p) {

@@ -184,3 +184,9 @@ def test_pack_unpack_roundtrip(eq):
         c2, s2, b2 = p.unpack()
         assert np.array_equal(c2.cpu().numpy(), codes)
         assert np.array_equal(s2.cpu().numpy(), sc) and np.array_equal(b2.cpu().numpy(), bi)
+
+
+def test_div15_matches_ieee_divide(eq):
+    L = eq.load()
+    assert L.eq4_selftest(0, 1 << 28, 11) == 0
+    assert L.eq4_selftest(1, 1 << 28, 12) == 0
