@@ -419,23 +419,42 @@ k_asym(const Params p) {
 // Rarely-touched float64 state of one row's walk, kept in shared memory so the
 // hot loop holds only the row slice (Yh) and a few scalars in registers.
 struct RowShared {
-  double x0, x1, step, min_steps, kY2, best_ex, elo, ehi;
+  double x0, x1, step, min_steps, kY, kY2, best_ex, elo, ehi, pad;
 };
 
+// Per-warp shared-memory slice of the GREEDY kernel.  Warps run independently
+// (no block-wide barrier anywhere), so a warp that stalls on an exact
+// re-decision never holds up the others.
 template <int LPR, int E, bool VEC>
-struct LayoutG {
-  static constexpr int RPB = NTHREADS / LPR;
+struct WarpSliceG {
+  static constexpr int RPW = 32 / LPR;
   static constexpr int D = LPR * E;
-  __host__ __device__ static size_t xs_bytes() { return (size_t)RPB * D * 4; }
-  __host__ __device__ static size_t ys_off() { return xs_bytes(); }
-  __host__ __device__ static size_t rs_off() { return 2 * xs_bytes(); }
-  __host__ __device__ static size_t leaf_off() { return rs_off() + (size_t)RPB * sizeof(RowShared); }
-  __host__ __device__ static size_t codes_off() { return leaf_off() + (size_t)NWARPS * MAX_LEAVES * 16; }
+  static constexpr int E2CAP = D < 512 ? D : 512;
+  __host__ __device__ static size_t rs_off() { return (size_t)RPW * D * 4; }
+  __host__ __device__ static size_t e2_off() { return rs_off() + RPW * sizeof(RowShared); }
+  __host__ __device__ static size_t leaf_off() { return e2_off() + (size_t)E2CAP * 8; }
+  __host__ __device__ static size_t codes_off() { return leaf_off() + (size_t)MAX_LEAVES * 16; }
   __host__ __device__ static size_t out_off() {
-    return (codes_off() + (VEC ? 0 : (size_t)RPB * D) + 15) & ~(size_t)15;
+    return (codes_off() + (VEC ? 0 : (size_t)RPW * D) + 15) & ~(size_t)15;
   }
-  __host__ __device__ static size_t total(int stride) { return out_off() + (size_t)RPB * stride + 32; }
+  __host__ __device__ static size_t bytes(int stride) {
+    return (out_off() + (size_t)RPW * stride + 32 + 15) & ~(size_t)15;
+  }
 };
+
+// Warp-level copy of nbytes from shared src to global dst (equal modulo 16).
+__device__ __forceinline__ void warp_copy_out(uint8_t* dst, const uint8_t* src, int nbytes) {
+  const int lane = threadIdx.x & 31;
+  int head = (int)((16 - ((uintptr_t)dst & 15)) & 15);
+  if (head > nbytes) head = nbytes;
+  const int nvec = (nbytes - head) >> 4;
+  const int tail = head + (nvec << 4);
+  if (lane < head) dst[lane] = src[lane];
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  for (int i = lane; i < nvec; i += 32) d4[i] = s4[i];
+  for (int i = tail + lane; i < nbytes; i += 32) dst[i] = src[i];
+}
 
 // One fast candidate: approximate loss (Y units) of base B, width W.
 template <int E, bool MASKED>
@@ -481,15 +500,27 @@ __device__ __forceinline__ void eval_pair(const float (&Yh)[E], int nv, float BL
   aR = sR;
 }
 
+// Y coordinates on the exact fp32 grid of quantum qY (see file header).
+template <int LPR, int E, bool VEC>
+__device__ __forceinline__ void make_Y(const Params& p, const float* xr, int q, int nv, double x0,
+                                       double kY, bool active, float (&Yh)[E]) {
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const float x = (VEC || i < nv) ? xr[VEC ? 4 * (q + LPR * (i >> 2)) + (i & 3) : q + LPR * i] : 0.f;
+    const double Y = __dmul_rn(__dsub_rn((double)x, x0), kY);
+    Yh[i] = active ? (float)(rint(Y * p.inv_qY) * p.qY) : 0.f;
+  }
+}
+
 // Exact (reference) decision of one loop iteration for one row.  Warp-
-// collective: every lane passes the owning group's (broadcast) state.
+// collective: every lane passes the owning row's (broadcast) state.
 struct ExactOut {
   double vL, vR, vb;
   int flags;  // 1 = range error, 2 = move left, 4 = candidate better than best
 };
 
 __device__ __forceinline__ ExactOut exact_decide(RowShared* R, double nl, double nr, int bi, int bj,
-                                                 bool bvalid, const float* xs, int d,
+                                                 bool bvalid, const float* xs, int d, double* e2,
                                                  double* leaf_sum, int* leaf_st, int* leaf_ln) {
   ExactOut o;
   const double x0 = R->x0, x1 = R->x1, st = R->step;
@@ -497,11 +528,11 @@ __device__ __forceinline__ ExactOut exact_decide(RowShared* R, double nl, double
   o.vb = R->best_ex;
   o.flags = 0;
   // clipping.py:181-184 candidates; ClipRange validation table.py:70-74 (L first)
-  double lmin = __dadd_rn(x0, __dmul_rn(nl + 1.0, st)), lmax = __dsub_rn(x1, __dmul_rn(nr, st));
-  double rmin = __dadd_rn(x0, __dmul_rn(nl, st)), rmax = __dsub_rn(x1, __dmul_rn(nr + 1.0, st));
+  const double lmin = __dadd_rn(x0, __dmul_rn(nl + 1.0, st)), lmax = __dsub_rn(x1, __dmul_rn(nr, st));
+  const double rmin = __dadd_rn(x0, __dmul_rn(nl, st)), rmax = __dsub_rn(x1, __dmul_rn(nr + 1.0, st));
   const bool errL = !(lmin <= lmax);
   const bool errR = !(rmin <= rmax);
-  if (!errL) o.vL = warp_np_loss(xs, d, lmin, lmax, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
+  if (!errL) o.vL = warp_np_loss(xs, d, lmin, lmax, e2, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
   if (errL || errR) {
     if ((threadIdx.x & 31) == 0) {
       R->elo = errL ? lmin : rmin;
@@ -510,13 +541,13 @@ __device__ __forceinline__ ExactOut exact_decide(RowShared* R, double nl, double
     o.flags = 1;
     return o;
   }
-  o.vR = warp_np_loss(xs, d, rmin, rmax, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
+  o.vR = warp_np_loss(xs, d, rmin, rmax, e2, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
   const bool goL = o.vL < o.vR;                             // clipping.py:185
   const double vc = goL ? o.vL : o.vR;
   if (!bvalid) {
-    double blo = bi == 0 ? x0 : __dadd_rn(x0, __dmul_rn((double)bi, st));
-    double bhi = bj == 0 ? x1 : __dsub_rn(x1, __dmul_rn((double)bj, st));
-    o.vb = warp_np_loss(xs, d, blo, bhi, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
+    const double blo = bi == 0 ? x0 : __dadd_rn(x0, __dmul_rn((double)bi, st));
+    const double bhi = bj == 0 ? x1 : __dsub_rn(x1, __dmul_rn((double)bj, st));
+    o.vb = warp_np_loss(xs, d, blo, bhi, e2, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
   }
   o.flags = (goL ? 2 : 0) | (vc < o.vb ? 4 : 0);            // clipping.py:187,191
   return o;
@@ -526,36 +557,38 @@ enum : unsigned { F_ACTIVE = 1, F_EXACT_ONLY = 2, F_BEST_EX = 4, F_ERR = 8 };
 
 template <int LPR, int E, bool VEC>
 __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Params p) {
-  using L = LayoutG<LPR, E, VEC>;
-  constexpr int RPB = L::RPB;
-  constexpr int D = L::D;
-  constexpr int RPW = 32 / LPR;
+  using S = WarpSliceG<LPR, E, VEC>;
+  constexpr int RPW = S::RPW;
+  constexpr int D = S::D;
   static_assert(LPR >= 1 && LPR <= 32 && (LPR & (LPR - 1)) == 0, "LPR");
   extern __shared__ __align__(16) unsigned char smem[];
-  float* xs = reinterpret_cast<float*>(smem);
-  float* ys = reinterpret_cast<float*>(smem + L::ys_off());
-  RowShared* rs = reinterpret_cast<RowShared*>(smem + L::rs_off());
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = tid / LPR, q = tid % LPR;
-  double* leaf_sum = reinterpret_cast<double*>(smem + L::leaf_off()) + warp * MAX_LEAVES * 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = lane / LPR, q = lane % LPR;
+  unsigned char* ws = smem + warp * S::bytes(p.stride);
+  float* xs = reinterpret_cast<float*>(ws);
+  RowShared* rs = reinterpret_cast<RowShared*>(ws + S::rs_off());
+  double* e2 = reinterpret_cast<double*>(ws + S::e2_off());
+  double* leaf_sum = reinterpret_cast<double*>(ws + S::leaf_off());
   int* leaf_st = reinterpret_cast<int*>(leaf_sum + MAX_LEAVES);
   int* leaf_ln = leaf_st + MAX_LEAVES;
-  uint8_t* codes_s = smem + L::codes_off();
-  uint8_t* out_base = smem + L::out_off();
+  uint8_t* codes_w = ws + S::codes_off();
+  uint8_t* out_base = ws + S::out_off();
   const int d = p.d;
   const int nv = valid_slots<LPR, E, VEC>(q, d);
   const float hh = 0.5f / ALPHA;
-  const int64_t ntiles = (p.rows + RPB - 1) / RPB;
+  const float c1 = 4.2f * p.delta * sqrtf((float)d);
+  const float c0 = 2.1f * (float)d * p.delta * p.delta;
+  const int64_t nblocks = (p.rows + RPW - 1) / RPW;
+  const int64_t wstride = (int64_t)gridDim.x * NWARPS;
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t row0 = tile * RPB, row = row0 + g;
+  for (int64_t blk = (int64_t)blockIdx.x * NWARPS + warp; blk < nblocks; blk += wstride) {
+    const int64_t row0 = blk * RPW, row = row0 + gw;
     const bool rvalid = row < p.rows;
-    const int tile_rows = (int)min((int64_t)RPB, p.rows - row0);
+    const int blk_rows = (int)min((int64_t)RPW, p.rows - row0);
     const size_t gofs = (size_t)row0 * p.stride;
     uint8_t* out_tile = out_base + (((uintptr_t)p.packed + gofs) & 15);
-    RowShared& R = rs[g];
-    float* xr = xs + g * D;
-    float* yr = ys + g * D;
+    RowShared& R = rs[gw];
+    float* xr = xs + gw * D;
 
     float Yh[E];
     float mn, mx;
@@ -579,25 +612,14 @@ __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Para
       const double step = __ddiv_rn(Dw, (double)p.b);                               // :172
       const double kY = (x0 != x1) ? __ddiv_rn(15.0, step) : 0.0;
 #pragma unroll
-      for (int i = 0; i < E; ++i) {      // Y on the exact fp32 grid of quantum qY
-        double Y = __dmul_rn(__dsub_rn((double)v[i], x0), kY);
+      for (int i = 0; i < E; ++i) {
+        const double Y = __dmul_rn(__dsub_rn((double)v[i], x0), kY);
         Yh[i] = (float)(rint(Y * p.inv_qY) * p.qY);
-      }
-      // a copy in shared memory lets the rare exact path below clobber the
-      // registers: Yh is re-read after it instead of living across its calls
-      if (VEC) {
-#pragma unroll
-        for (int c = 0; c < E / 4; ++c)
-          *reinterpret_cast<float4*>(yr + 4 * (q + LPR * c)) =
-              make_float4(Yh[4 * c], Yh[4 * c + 1], Yh[4 * c + 2], Yh[4 * c + 3]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < E; ++i) yr[q + LPR * i] = Yh[i];
       }
       if (q == 0) {
         R.x0 = x0; R.x1 = x1; R.step = step;
         R.min_steps = __dmul_rn(__dmul_rn((double)p.b, __dsub_rn(1.0, p.r)), step);  // :173
-        R.kY2 = kY * kY; R.best_ex = 0.0; R.elo = 0.0; R.ehi = 0.0;
+        R.kY = kY; R.kY2 = kY * kY; R.best_ex = 0.0; R.elo = 0.0; R.ehi = 0.0;
       }
     }
     __syncwarp();
@@ -609,8 +631,6 @@ __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Para
       if (!(M <= 1e6f * Dwf)) flags |= F_EXACT_ONLY;   // reference grid rounds coarsely
       tau2 += 6e-14f * (M / Dwf);
     }
-    const float c1 = 4.2f * p.delta * sqrtf((float)d);
-    const float c0 = 2.1f * (float)d * p.delta * p.delta;
     float Lbest;
     {
       const float Wf = (float)p.b;                                                   // :174
@@ -632,11 +652,10 @@ __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Para
         float aL, aR;
         eval_pair<E, !VEC>(Yh, nv, (float)(15 * (nl + 1)), -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
         group_sum_pair<LPR>(aL, aR, SL, SR);
-        const float misW2 = p.kmis * Wf * Wf;
+        const float cw = c0 + p.kmis * Wf * Wf;
         const bool goL = SL < SR;
         const float cand = goL ? SL : SR;
         const float mlr = fmaxf(SL, SR), mb = fmaxf(cand, Lbest);
-        const float cw = c0 + misW2;
         const bool near_lr = fabsf(SL - SR) <= tau2 * mlr + c1 * sqrt_approx(mlr) + cw;
         const bool near_b = fabsf(cand - Lbest) <= tau2 * mb + c1 * sqrt_approx(mb) + cw;
         need_ex = (flags & F_ACTIVE) && ((flags & F_EXACT_ONLY) || near_lr || near_b);
@@ -651,45 +670,37 @@ __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Para
       }
       unsigned bal = __ballot_sync(FULL, need_ex && q == 0);
       if (bal) {
-      while (bal) {
-        const int leader = __ffs(bal) - 1;
-        bal &= bal - 1;
-        const int lg = warp * RPW + leader / LPR;
-        const ExactOut o = exact_decide(
-            &rs[lg], (double)__shfl_sync(FULL, nl, leader), (double)__shfl_sync(FULL, nr, leader),
-            __shfl_sync(FULL, bi, leader), __shfl_sync(FULL, bj, leader),
-            (__shfl_sync(FULL, flags, leader) & F_BEST_EX) != 0, xs + lg * D, d, leaf_sum, leaf_st,
-            leaf_ln);
-        if (lg == g) {
-          if (o.flags & 1) {
-            flags = (flags & ~F_ACTIVE) | F_ERR;
-          } else {
-            const bool goL = (o.flags & 2) != 0;
-            const double vc = goL ? o.vL : o.vR;
-            if (goL) ++nl; else ++nr;
-            if (o.flags & 4) {
-              bi = nl; bj = nr;
-              if (q == 0) R.best_ex = vc;
-              Lbest = (W >= 1) ? (goL ? SL : SR) : (float)(vc * R.kY2);
-            } else if (q == 0) {
-              R.best_ex = o.vb;
+        while (bal) {
+          const int leader = __ffs(bal) - 1;
+          bal &= bal - 1;
+          const int lg = leader / LPR;
+          const ExactOut o = exact_decide(
+              &rs[lg], (double)__shfl_sync(FULL, nl, leader), (double)__shfl_sync(FULL, nr, leader),
+              __shfl_sync(FULL, bi, leader), __shfl_sync(FULL, bj, leader),
+              (__shfl_sync(FULL, flags, leader) & F_BEST_EX) != 0, xs + lg * D, d, e2, leaf_sum,
+              leaf_st, leaf_ln);
+          if (lg == gw) {
+            if (o.flags & 1) {
+              flags = (flags & ~F_ACTIVE) | F_ERR;
+            } else {
+              const bool goL = (o.flags & 2) != 0;
+              const double vc = goL ? o.vL : o.vR;
+              if (goL) ++nl; else ++nr;
+              if (o.flags & 4) {
+                bi = nl; bj = nr;
+                if (q == 0) R.best_ex = vc;
+                Lbest = (W >= 1) ? (goL ? SL : SR) : (float)(vc * R.kY2);
+              } else if (q == 0) {
+                R.best_ex = o.vb;
+              }
+              flags |= F_BEST_EX;
+              ++iters;
             }
-            flags |= F_BEST_EX;
-            ++iters;
           }
+          __syncwarp();
         }
-        __syncwarp();
-      }
-      if (VEC) {
-#pragma unroll
-        for (int c = 0; c < E / 4; ++c) {
-          const float4 t = *reinterpret_cast<const float4*>(yr + 4 * (q + LPR * c));
-          Yh[4 * c] = t.x; Yh[4 * c + 1] = t.y; Yh[4 * c + 2] = t.z; Yh[4 * c + 3] = t.w;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < E; ++i) Yh[i] = yr[q + LPR * i];
-      }
+        // the exact path clobbered the registers: rebuild the row slice
+        make_Y<LPR, E, VEC>(p, xr, q, nv, R.x0, R.kY, (flags & F_ACTIVE) != 0, Yh);
       }
     }
 
@@ -707,18 +718,29 @@ __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Para
     {
       float v[E];
 #pragma unroll
-      for (int i = 0; i < E; ++i) v[i] = (VEC || i < nv) ? xr[VEC ? 4 * (q + LPR * (i >> 2)) + (i & 3) : q + LPR * i] : 0.f;
+      for (int i = 0; i < E; ++i)
+        v[i] = (VEC || i < nv) ? xr[VEC ? 4 * (q + LPR * (i >> 2)) + (i & 3) : q + LPR * i] : 0.f;
       emit_row<LPR, E, VEC>(p, v, nv, lo, hi, !bad && !(flags & F_ERR), rvalid, q,
-                            out_tile + g * p.stride, codes_s + g * D);
+                            out_tile + gw * p.stride, codes_w + gw * D);
     }
-    if (rvalid) {
-      if (q == 0) {
-        if (p.lo_out) { p.lo_out[row] = lo; p.hi_out[row] = hi; }
-        if (p.info0) p.info0[row] = info0;
-        if (p.info1) p.info1[row] = info1;
+    if (rvalid && q == 0) {
+      if (p.lo_out) { p.lo_out[row] = lo; p.hi_out[row] = hi; }
+      if (p.info0) p.info0[row] = info0;
+      if (p.info1) p.info1[row] = info1;
+    }
+    __syncwarp();
+    if (!VEC) {
+      const int nb = blk_rows * p.half;
+      for (int t = lane; t < nb; t += 32) {
+        const int rr = t / p.half, m = t - rr * p.half;
+        const unsigned c0b = codes_w[rr * D + 2 * m];
+        const unsigned c1b = (2 * m + 1 < d) ? codes_w[rr * D + 2 * m + 1] : 0u;  // packed.py:75-76
+        out_tile[rr * p.stride + m] = (uint8_t)(c0b | (c1b << 4));
       }
+      __syncwarp();
     }
-    store_tile<D, VEC>(p, codes_s, out_tile, tile_rows, gofs);
+    warp_copy_out(p.packed + gofs, out_tile, blk_rows * p.stride);
+    __syncwarp();
   }
 }
 
@@ -773,15 +795,18 @@ __global__ void __launch_bounds__(NTHREADS) k_quant_mse(const float* x, int64_t 
                                                         const double* hi, double* out) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* leaf_sum = reinterpret_cast<double*>(smem) + warp * MAX_LEAVES * 2;
+  const size_t per_warp = (size_t)MAX_LEAVES * 16 + 512 * 8 + (((size_t)d * 4 + 15) & ~(size_t)15);
+  unsigned char* ws = smem + warp * per_warp;
+  double* leaf_sum = reinterpret_cast<double*>(ws);
   int* leaf_st = reinterpret_cast<int*>(leaf_sum + MAX_LEAVES);
   int* leaf_ln = leaf_st + MAX_LEAVES;
-  float* xs = reinterpret_cast<float*>(smem + (size_t)NWARPS * MAX_LEAVES * 16) + (size_t)warp * d;
+  double* e2 = reinterpret_cast<double*>(ws + MAX_LEAVES * 16);
+  float* xs = reinterpret_cast<float*>(ws + MAX_LEAVES * 16 + 512 * 8);
   for (int64_t row = blockIdx.x * (int64_t)NWARPS + warp; row < rows;
        row += (int64_t)gridDim.x * NWARPS) {
     for (int k = lane; k < d; k += 32) xs[k] = x[row * ld + k];
     __syncwarp();
-    double v = warp_np_loss(xs, d, lo[row], hi[row], leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
+    double v = warp_np_loss(xs, d, lo[row], hi[row], e2, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
     if (lane == 0) out[row] = v;
     __syncwarp();
   }
@@ -860,9 +885,9 @@ static int launch_rq(const Params& p, cudaStream_t s) {
     return launch_persistent(k_asym<LPR, E, VEC>, L::total(p.stride), (p.rows + L::RPB - 1) / L::RPB,
                              p, s, "k_asym");
   } else {
-    using L = LayoutG<LPR, E, VEC>;
-    return launch_persistent(k_greedy<LPR, E, VEC>, L::total(p.stride),
-                             (p.rows + L::RPB - 1) / L::RPB, p, s, "k_greedy");
+    using S = WarpSliceG<LPR, E, VEC>;
+    return launch_persistent(k_greedy<LPR, E, VEC>, NWARPS * S::bytes(p.stride),
+                             (p.rows + S::RPW * NWARPS - 1) / (S::RPW * NWARPS), p, s, "k_greedy");
   }
 }
 
@@ -1001,7 +1026,7 @@ int eq4_quant_mse(const float* x, int64_t rows, int64_t dim, int64_t ld, const d
                   const double* xmax, double* out, void* stream) {
   if (rows < 1 || dim < 1 || ld < dim) return fail(EQ4_EINVAL, "bad shape");
   if (dim > 4096) return fail(EQ4_EUNSUPPORTED, "quant_mse: dim > 4096");
-  size_t smem = (size_t)NWARPS * MAX_LEAVES * 16 + (size_t)NWARPS * dim * 4;
+  size_t smem = (size_t)NWARPS * ((size_t)MAX_LEAVES * 16 + 512 * 8 + (((size_t)dim * 4 + 15) & ~(size_t)15));
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_quant_mse, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);

@@ -22,6 +22,16 @@ constexpr unsigned FULL = 0xffffffffu;
 // Exact (numpy float64) tier
 // ---------------------------------------------------------------------------
 
+// Correctly rounded w / 15 in float64 without a divide: q = RN(w * RN(1/15)),
+// r = w - 15 q (exact by FMA), RN(q + r * RN(1/15)) = RN(w / 15) (Markstein's
+// correction step; checked against __ddiv_rn by eq4_selftest).
+__device__ __forceinline__ double div15(double w) {
+  const double y = 0.06666666666666666666;          // RN(1/15)
+  const double q = __dmul_rn(w, y);
+  const double r = __fma_rn(-q, 15.0, w);
+  return __fma_rn(r, y, q);
+}
+
 // np.clip(x, lo, hi) == minimum(maximum(x, lo), hi) for finite operands.
 __device__ __forceinline__ double np_clip(double x, double lo, double hi) {
   double t = x > lo ? x : lo;
@@ -84,12 +94,18 @@ __device__ __noinline__ double np_combine(int n, const double* leaf_sum, int* li
 // Warp-cooperative, bit-exact quant_mse (table.py:81-103) of one row whose
 // fp32 values sit in shared memory `xs[0..d)`.  All 32 lanes must call it
 // with identical arguments; every lane returns the same value.
-// scratch: per-warp shared buffer of >= 3*max_leaves doubles/ints.
+// Scratch (per warp, shared): e2[e2cap] doubles with e2cap >= min(d, 512),
+// leaf_sum/leaf_start/leaf_len[max_leaves].
+// Element errors are computed by all 32 lanes into e2, then numpy's
+// pairwise order is replayed: per leaf, 8 lanes run the 8 sequential
+// accumulator chains, a 3-level butterfly forms ((r0+r1)+(r2+r3))+(...),
+// lane 0 adds the leaf's remainder, and lane 0 combines leaf sums in the
+// recursion's association order.
 __device__ __noinline__ double warp_np_loss(const float* xs, int d, double lo, double hi,
-                                            double* leaf_sum, int* leaf_start, int* leaf_len,
-                                            int max_leaves) {
+                                            double* e2, double* leaf_sum, int* leaf_start,
+                                            int* leaf_len, int max_leaves) {
   const int lane = threadIdx.x & 31;
-  double scale = (hi == lo) ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+  const double scale = (hi == lo) ? 0.0 : div15(__dsub_rn(hi, lo));   // table.py:99
   if (d < 8) {  // numpy: res = 0.; res += a[i] sequentially
     double res = 0.0;
     if (lane == 0)
@@ -97,29 +113,34 @@ __device__ __noinline__ double warp_np_loss(const float* xs, int d, double lo, d
     res = __shfl_sync(FULL, res, 0);
     return __dadd_rn(0.0, res);
   }
-  int nl = np_leaves(d, leaf_start, leaf_len, max_leaves);
+  int nl = 0;
+  if (lane == 0) nl = np_leaves(d, leaf_start, leaf_len, max_leaves);
+  nl = __shfl_sync(FULL, nl, 0);
   __syncwarp();
   const int g = lane >> 3, m = lane & 7;
   for (int base = 0; base < nl; base += 4) {
-    int li = base + g;
-    bool ok = li < nl;
-    int a = ok ? leaf_start[li] : 0;
-    int len = ok ? leaf_len[li] : 8;
-    int nfull = len - (len % 8);
-    // chain m: r[m] = a[m] + a[m+8] + ... (sequential), loops_utils.h.src
-    double r = ok ? np_err2((double)xs[a + m], lo, hi, scale) : 0.0;
-    for (int i = 8 + m; i < nfull; i += 8)
-      r = __dadd_rn(r, np_err2((double)xs[a + i], lo, hi, scale));
+    const int last = min(base + 4, nl) - 1;
+    const int r0 = leaf_start[base], r1 = leaf_start[last] + leaf_len[last];
+    for (int k = lane; k < r1 - r0; k += 32) e2[k] = np_err2((double)xs[r0 + k], lo, hi, scale);
+    __syncwarp();
+    const int li = base + g;
+    const bool ok = li < nl;
+    const int a = ok ? leaf_start[li] - r0 : 0;
+    const int len = ok ? leaf_len[li] : 8;
+    const int nfull = len - (len % 8);
+    // chain m: r[m] = a[m] + a[m+8] + ... sequentially (loops_utils.h.src)
+    double r = ok ? e2[a + m] : 0.0;
+    for (int i = 8 + m; i < nfull; i += 8) r = __dadd_rn(r, e2[a + i]);
     // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)); a+b == b+a bitwise
     r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 1));
     r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 2));
     r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 4));
     if (ok && m == 0) {
-      for (int i = nfull; i < len; i++) r = __dadd_rn(r, np_err2((double)xs[a + i], lo, hi, scale));
+      for (int i = nfull; i < len; i++) r = __dadd_rn(r, e2[a + i]);
       leaf_sum[li] = r;
     }
+    __syncwarp();
   }
-  __syncwarp();
   double total = 0.0;
   if (lane == 0) {
     int li = 0;
@@ -132,16 +153,6 @@ __device__ __noinline__ double warp_np_loss(const float* xs, int d, double lo, d
 // ---------------------------------------------------------------------------
 // Codes for the final quantize pass (uniform.py:77-79), fast path + exact fix-up
 // ---------------------------------------------------------------------------
-
-// Correctly rounded w / 15 in float64 without a divide: q = RN(w * RN(1/15)),
-// r = w - 15 q (exact by FMA), RN(q + r * RN(1/15)) = RN(w / 15) (Markstein's
-// correction step; checked against __ddiv_rn by eq4_selftest).
-__device__ __forceinline__ double div15(double w) {
-  const double y = 0.06666666666666666666;          // RN(1/15)
-  const double q = __dmul_rn(w, y);
-  const double r = __fma_rn(-q, 15.0, w);
-  return __fma_rn(r, y, q);
-}
 
 struct CodeParams {
   double lo, hi, scale;   // float64 range and (hi - lo) / 15
