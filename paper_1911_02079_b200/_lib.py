@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libeq4.so")
+LIB_PATH = os.environ.get("EQ4_LIB") or os.path.join(HERE, "libeq4.so")
 
 EQ4_OK = 0
 EQ4_EINVAL = 1

@@ -40,6 +40,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -50,10 +51,18 @@ namespace eq4 {
 
 constexpr int NTHREADS = 256;
 constexpr int NWARPS = NTHREADS / 32;
+#ifndef G_THREADS
+#define G_THREADS 128
+#endif
+constexpr int NTHREADS_G = G_THREADS;         // GREEDY blocks (warps are independent)
+constexpr int NWARPS_G = NTHREADS_G / 32;
 constexpr int MAX_LEAVES = 64;          // numpy pairwise leaves for d <= 4096
 constexpr float ALPHA = 15.75f;         // saturation scale for the code FFMA
 constexpr float MAGIC = 8388608.f;      // 2^23
 enum { M_ASYM = 0, M_GREEDY = 1 };
+#ifndef GREEDY_MINB
+#define GREEDY_MINB 4
+#endif
 
 struct Params {
   const float* x;
@@ -75,8 +84,10 @@ struct Params {
   int it_exact_from;  // loop iterations < this have a provably true condition
   double qY, inv_qY;  // Y grid quantum and inverse
   float delta;        // qY / 2
-  float tau2;         // relative band coefficient, both sides
+  float tau2;         // relative band coefficient, both sides (incl. reference grid rounding)
   float kmis;         // misround band per W^2, both sides
+  float c1;           // Yh quantisation band: 4.2 * delta * sqrt(d)
+  float c0;           // 2.1 * d * delta^2
 };
 
 // Copy nbytes from shared src to global dst; src and dst agree modulo 16.
@@ -430,7 +441,8 @@ struct WarpSliceG {
   static constexpr int RPW = 32 / LPR;
   static constexpr int D = LPR * E;
   static constexpr int E2CAP = D < 512 ? D : 512;
-  __host__ __device__ static size_t rs_off() { return (size_t)RPW * D * 4; }
+  __host__ __device__ static size_t ys_off() { return (size_t)RPW * D * 4; }          // E/4 x 32 float4
+  __host__ __device__ static size_t rs_off() { return ys_off() + (size_t)E * 32 * 4; }
   __host__ __device__ static size_t e2_off() { return rs_off() + RPW * sizeof(RowShared); }
   __host__ __device__ static size_t leaf_off() { return e2_off() + (size_t)E2CAP * 8; }
   __host__ __device__ static size_t codes_off() { return leaf_off() + (size_t)MAX_LEAVES * 16; }
@@ -456,19 +468,32 @@ __device__ __forceinline__ void warp_copy_out(uint8_t* dst, const uint8_t* src, 
   for (int i = tail + lane; i < nbytes; i += 32) dst[i] = src[i];
 }
 
-// One fast candidate: approximate loss (Y units) of base B, width W.
+#ifndef G_UNROLL
+#define G_UNROLL 4
+#endif
+constexpr int kGUnroll = G_UNROLL;   // float4 chunks per trip of the element loop
+
+// One fast candidate: approximate loss (Y units) of base B, width W.  The row
+// slice is read from shared memory (ys4[c * 32 + lane] holds slots 4c..4c+3)
+// so that registers hold one chunk of temporaries, not the whole slice.
 template <int E, bool MASKED>
-__device__ __forceinline__ float eval_one(const float (&Yh)[E], int nv, float B, float nW, float kW,
+__device__ __forceinline__ float eval_one(const float4* ys4, int nv, float B, float nW, float kW,
                                           float h) {
+  const int lane = threadIdx.x & 31;
   float s = 0.f;
+#pragma unroll kGUnroll
+  for (int c = 0; c < E / 4; ++c) {
+    const float4 y4 = ys4[c * 32 + lane];
+    const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
 #pragma unroll
-  for (int i = 0; i < E; ++i) {
-    float z = __fadd_rn(Yh[i], -B);
-    float t = sat_fma(z, kW, h);
-    float m = __fmaf_rd(t, ALPHA, MAGIC);
-    float c = __fadd_rn(m, -MAGIC);
-    float e = __fmaf_rn(c, nW, z);
-    if (!MASKED || i < nv) s = __fmaf_rn(e, e, s);
+    for (int k = 0; k < 4; ++k) {
+      float z = __fadd_rn(yv[k], -B);
+      float t = sat_fma(z, kW, h);
+      float m = __fmaf_rd(t, ALPHA, MAGIC);
+      float cc = __fadd_rn(m, -MAGIC);
+      float e = __fmaf_rn(cc, nW, z);
+      if (!MASKED || 4 * c + k < nv) s = __fmaf_rn(e, e, s);
+    }
   }
   return s;
 }
@@ -476,24 +501,30 @@ __device__ __forceinline__ float eval_one(const float (&Yh)[E], int nv, float B,
 // The two candidates of one iteration share W: L = (BL, W), R = (BL - 15, W).
 // 6 fp32 instructions per element and candidate.
 template <int E, bool MASKED>
-__device__ __forceinline__ void eval_pair(const float (&Yh)[E], int nv, float BL, float nW, float kW,
+__device__ __forceinline__ void eval_pair(const float4* ys4, int nv, float BL, float nW, float kW,
                                           float h, float& aL, float& aR) {
+  const int lane = threadIdx.x & 31;
   float sL = 0.f, sR = 0.f;
+#pragma unroll kGUnroll
+  for (int c = 0; c < E / 4; ++c) {
+    const float4 y4 = ys4[c * 32 + lane];
+    const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
 #pragma unroll
-  for (int i = 0; i < E; ++i) {
-    float zL = __fadd_rn(Yh[i], -BL);
-    float zR = __fadd_rn(zL, 15.f);                       // exact
-    float tL = sat_fma(zL, kW, h);
-    float tR = sat_fma(zR, kW, h);
-    float mL = __fmaf_rd(tL, ALPHA, MAGIC);               // 2^23 + floor(alpha * t)
-    float mR = __fmaf_rd(tR, ALPHA, MAGIC);
-    float cL = __fadd_rn(mL, -MAGIC);
-    float cR = __fadd_rn(mR, -MAGIC);
-    float eL = __fmaf_rn(cL, nW, zL);                     // exact
-    float eR = __fmaf_rn(cR, nW, zR);
-    if (!MASKED || i < nv) {
-      sL = __fmaf_rn(eL, eL, sL);
-      sR = __fmaf_rn(eR, eR, sR);
+    for (int k = 0; k < 4; ++k) {
+      float zL = __fadd_rn(yv[k], -BL);
+      float zR = __fadd_rn(zL, 15.f);                     // exact
+      float tL = sat_fma(zL, kW, h);
+      float tR = sat_fma(zR, kW, h);
+      float mL = __fmaf_rd(tL, ALPHA, MAGIC);             // 2^23 + floor(alpha * t)
+      float mR = __fmaf_rd(tR, ALPHA, MAGIC);
+      float cL = __fadd_rn(mL, -MAGIC);
+      float cR = __fadd_rn(mR, -MAGIC);
+      float eL = __fmaf_rn(cL, nW, zL);                   // exact
+      float eR = __fmaf_rn(cR, nW, zR);
+      if (!MASKED || 4 * c + k < nv) {
+        sL = __fmaf_rn(eL, eL, sL);
+        sR = __fmaf_rn(eR, eR, sR);
+      }
     }
   }
   aL = sL;
@@ -553,10 +584,127 @@ __device__ __forceinline__ ExactOut exact_decide(RowShared* R, double nl, double
   return o;
 }
 
+// GREEDY codes from the row slice: with the winning pair (bi, bj) the codes are
+// c = clamp(floor((Y - B)/Wb + 1/2), 0, 15), B = 15 bi, Wb = b - bi - bj, i.e.
+// the same saturating FFMA + round-down FFMA as the search.  Yh is within
+// delta = qY/2 of Y, so an element whose fractional part is within
+// NEAR + delta/Wb of a rounding boundary gets its code from the float64 codec
+// instead (clamping at lo/hi cannot flip a code: codes are continuous there).
+// Warp-collective.
+template <int LPR, int E, bool VEC>
+__device__ __forceinline__ void emit_greedy(const Params& p, const float4* ys4, int nv, int q,
+                                            double lo, double hi, int bi, int bj, bool fast_ok,
+                                            bool ok, bool rvalid, const float* xr, uint8_t* orow,
+                                            uint8_t* crow) {
+  const int Wb = p.b - bi - bj;
+  const float B = (float)(15 * bi);
+  const float Wf = (float)(Wb > 0 ? Wb : 1);
+  const float kW = __fdividef(1.f, Wf * ALPHA);
+  const float h = 0.5f / ALPHA;
+  const float nb = NEAR + p.delta / Wf;
+  const bool fast = fast_ok && Wb >= 1 && ok;
+  unsigned long long need = 0ull;
+  uint32_t mb[E];
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const float4 y4 = ys4[(i >> 2) * 32 + lane];
+    const float yi = (i & 3) == 0 ? y4.x : (i & 3) == 1 ? y4.y : (i & 3) == 2 ? y4.z : y4.w;
+    const float z = __fadd_rn(yi, -B);
+    const float s = sat_fma(z, kW, h);
+    const float m = __fmaf_rd(s, ALPHA, MAGIC);
+    const float f = __fmaf_rn(s, ALPHA, -__fadd_rn(m, -MAGIC));   // frac of alpha*s, exact
+    const bool nr_ = s > 0.f && s < 1.f && (f < nb || f > 1.f - nb);
+    need |= (unsigned long long)(nr_ && (VEC || i < nv)) << i;
+    mb[i] = __float_as_uint(m) & 0xFu;
+  }
+  if (!fast) need = ok ? ((nv >= 64) ? ~0ull : ((1ull << nv) - 1ull)) : 0ull;
+  if (!rvalid) need = 0ull;
+  if (__any_sync(FULL, need != 0ull)) {   // rare: float64 codec for flagged elements
+    if (need) {
+      const CodeParams cp = make_code_params(lo, hi);
+      for (int i = 0; i < E; ++i)
+        if ((need >> i) & 1ull)
+          mb[i] = code_exact(xr[VEC ? 4 * (q + LPR * (i >> 2)) + (i & 3) : q + LPR * i], cp);
+    }
+  }
+  if (!ok) {
+#pragma unroll
+    for (int i = 0; i < E; ++i) mb[i] = 0u;
+  }
+  if (rvalid) {
+    if (VEC) {
+#pragma unroll
+      for (int c = 0; c < E / 4; ++c) {
+        const uint32_t w = mb[4 * c] | (mb[4 * c + 1] << 4) | (mb[4 * c + 2] << 8) | (mb[4 * c + 3] << 12);
+        *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = (uint16_t)w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i)
+        if (i < nv) crow[q + LPR * i] = (uint8_t)mb[i];
+    }
+    if (q == 0) {
+      const double sc = (ok && hi != lo) ? div15(__dsub_rn(hi, lo)) : 0.0;   // uniform.py:74-80
+      uint8_t* a = orow + p.half;
+      if (p.aux == EQ4_AUX_FP16) {
+        const uint32_t s16 = aux_bits_f16(sc), b16 = aux_bits_f16(lo);
+        a[0] = s16 & 0xff; a[1] = s16 >> 8; a[2] = b16 & 0xff; a[3] = b16 >> 8;
+      } else {
+        const uint32_t s32 = aux_bits_f32(sc), b32 = aux_bits_f32(lo);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { a[k] = (s32 >> (8 * k)) & 0xff; a[4 + k] = (b32 >> (8 * k)) & 0xff; }
+      }
+    }
+  }
+}
+
 enum : unsigned { F_ACTIVE = 1, F_EXACT_ONLY = 2, F_BEST_EX = 4, F_ERR = 8 };
 
+// The rare path of one loop iteration: rows flagged need_ex are re-decided one
+// at a time by the whole warp with the bit-exact float64 restatement.
 template <int LPR, int E, bool VEC>
-__global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Params p) {
+__device__ __forceinline__ void exact_block(const Params& p, bool need_ex, int q, int gw, int W,
+                                            float SL, float SR, RowShared* rs, const float* xs,
+                                            int D, int d, double* e2, double* leaf_sum,
+                                            int* leaf_st, int* leaf_ln, int& nl, int& nr, int& bi,
+                                            int& bj, int& iters, unsigned& flags, float& Lbest,
+                                            float& BLf) {
+  unsigned bal = __ballot_sync(FULL, need_ex && q == 0);
+  while (bal) {
+    const int leader = __ffs(bal) - 1;
+    bal &= bal - 1;
+    const int lg = leader / LPR;
+    const ExactOut o = exact_decide(
+        &rs[lg], (double)__shfl_sync(FULL, nl, leader), (double)__shfl_sync(FULL, nr, leader),
+        __shfl_sync(FULL, bi, leader), __shfl_sync(FULL, bj, leader),
+        (__shfl_sync(FULL, flags, leader) & F_BEST_EX) != 0, xs + lg * D, d, e2, leaf_sum, leaf_st,
+        leaf_ln);
+    if (lg == gw) {
+      if (o.flags & 1) {
+        flags = (flags & ~F_ACTIVE) | F_ERR;
+      } else {
+        const bool goL = (o.flags & 2) != 0;
+        const double vc = goL ? o.vL : o.vR;
+        if (goL) { ++nl; BLf += 15.f; } else { ++nr; }
+        if (o.flags & 4) {
+          bi = nl; bj = nr;
+          if (q == 0) rs[gw].best_ex = vc;
+          Lbest = (W >= 1) ? (goL ? SL : SR) : (float)(vc * rs[gw].kY2);
+        } else if (q == 0) {
+          rs[gw].best_ex = o.vb;
+        }
+        flags |= F_BEST_EX;
+        ++iters;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+
+template <int LPR, int E, bool VEC>
+__global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ? GREEDY_MINB * 2 / 3 : GREEDY_MINB / 3)) k_greedy(const Params p) {
   using S = WarpSliceG<LPR, E, VEC>;
   constexpr int RPW = S::RPW;
   constexpr int D = S::D;
@@ -566,6 +714,7 @@ __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Para
   const int gw = lane / LPR, q = lane % LPR;
   unsigned char* ws = smem + warp * S::bytes(p.stride);
   float* xs = reinterpret_cast<float*>(ws);
+  float4* ys4 = reinterpret_cast<float4*>(ws + S::ys_off());
   RowShared* rs = reinterpret_cast<RowShared*>(ws + S::rs_off());
   double* e2 = reinterpret_cast<double*>(ws + S::e2_off());
   double* leaf_sum = reinterpret_cast<double*>(ws + S::leaf_off());
@@ -576,24 +725,19 @@ __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Para
   const int d = p.d;
   const int nv = valid_slots<LPR, E, VEC>(q, d);
   const float hh = 0.5f / ALPHA;
-  const float c1 = 4.2f * p.delta * sqrtf((float)d);
-  const float c0 = 2.1f * (float)d * p.delta * p.delta;
   const int64_t nblocks = (p.rows + RPW - 1) / RPW;
-  const int64_t wstride = (int64_t)gridDim.x * NWARPS;
+  const int64_t wstride = (int64_t)gridDim.x * NWARPS_G;
 
-  for (int64_t blk = (int64_t)blockIdx.x * NWARPS + warp; blk < nblocks; blk += wstride) {
+  for (int64_t blk = (int64_t)blockIdx.x * NWARPS_G + warp; blk < nblocks; blk += wstride) {
     const int64_t row0 = blk * RPW, row = row0 + gw;
     const bool rvalid = row < p.rows;
-    const int blk_rows = (int)min((int64_t)RPW, p.rows - row0);
-    const size_t gofs = (size_t)row0 * p.stride;
-    uint8_t* out_tile = out_base + (((uintptr_t)p.packed + gofs) & 15);
     RowShared& R = rs[gw];
     float* xr = xs + gw * D;
 
-    float Yh[E];
     float mn, mx;
     bool bad;
     {
+      float Yh[E];
       float v[E];
       load_row<LPR, E, VEC>(p, row, rvalid, q, nv, v);
       if (VEC) {
@@ -616,6 +760,9 @@ __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Para
         const double Y = __dmul_rn(__dsub_rn((double)v[i], x0), kY);
         Yh[i] = (float)(rint(Y * p.inv_qY) * p.qY);
       }
+#pragma unroll
+      for (int c = 0; c < E / 4; ++c)
+        ys4[c * 32 + lane] = make_float4(Yh[4 * c], Yh[4 * c + 1], Yh[4 * c + 2], Yh[4 * c + 3]);
       if (q == 0) {
         R.x0 = x0; R.x1 = x1; R.step = step;
         R.min_steps = __dmul_rn(__dmul_rn((double)p.b, __dsub_rn(1.0, p.r)), step);  // :173
@@ -624,20 +771,66 @@ __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Para
     }
     __syncwarp();
     unsigned flags = 0;
-    float tau2 = p.tau2;
     if (rvalid && !bad && mn != mx) {                                                // :164-165
       flags = F_ACTIVE;
       const float M = fmaxf(fabsf(mn), fabsf(mx)), Dwf = mx - mn;
       if (!(M <= 1e6f * Dwf)) flags |= F_EXACT_ONLY;   // reference grid rounds coarsely
-      tau2 += 6e-14f * (M / Dwf);
     }
     float Lbest;
     {
       const float Wf = (float)p.b;                                                   // :174
-      Lbest = group_sum<LPR>(eval_one<E, !VEC>(Yh, nv, 0.f, -Wf, rcp_approx(Wf * ALPHA), hh));
+      Lbest = group_sum<LPR>(eval_one<E, !VEC>(ys4, nv, 0.f, -Wf, rcp_approx(Wf * ALPHA), hh));
     }
     int nl = 0, nr = 0, bi = 0, bj = 0, iters = 0;
-    for (int it = 0;; ++it) {
+    float BLf = 15.f;                       // base of the L candidate, 15 * (nl + 1)
+    int it = 0;
+    // Phase A: for it < it_exact_from every active row provably stays in the
+    // loop (its float64 condition holds by >= 2 steps) and W >= 1, so the body
+    // is straight-line: evaluate, reduce, decide.  An iteration that needs an
+    // exact re-decision leaves the inner loop; the rare path runs outside it so
+    // the hot loop's registers are not shaped by the calls it makes.
+    const int itA = __any_sync(FULL, flags & F_EXACT_ONLY) ? 0 : min(p.it_exact_from, p.b - 1);
+    while (it < itA) {
+      bool need_ex = false, goL = false;
+      float SL = 0.f, SR = 0.f, cand = 0.f;
+      for (; it < itA; ++it) {
+        const float Wf = (float)(p.b - it - 1);
+        float aL, aR;
+        eval_pair<E, !VEC>(ys4, nv, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+        group_sum_pair<LPR>(aL, aR, SL, SR);
+        goL = SL < SR;                                                   // clipping.py:185
+        cand = goL ? SL : SR;
+        const float mall = fmaxf(fmaxf(SL, SR), Lbest);
+        const float band = p.tau2 * mall + p.c1 * sqrt_approx(mall) + (p.c0 + p.kmis * Wf * Wf);
+        need_ex = (flags & F_ACTIVE) && (fabsf(SL - SR) <= band || fabsf(cand - Lbest) <= band);
+        if (__any_sync(FULL, need_ex)) break;
+        const bool upd = (flags & F_ACTIVE) != 0;
+        const bool mvL = upd && goL;
+        nl += mvL;
+        nr += upd && !goL;
+        BLf += mvL ? 15.f : 0.f;
+        const bool better = upd && cand < Lbest;                         // clipping.py:187,191
+        Lbest = better ? cand : Lbest;
+        bi = better ? nl : bi;
+        bj = better ? nr : bj;
+        flags = better ? (flags & ~F_BEST_EX) : flags;
+        iters += upd;
+      }
+      if (it >= itA) break;
+      // iteration `it` has rows to re-decide exactly; the others apply the fast decision
+      const bool upd = (flags & F_ACTIVE) && !need_ex;
+      if (upd) {
+        if (goL) { ++nl; BLf += 15.f; } else { ++nr; }
+        if (cand < Lbest) { Lbest = cand; bi = nl; bj = nr; flags &= ~F_BEST_EX; }
+        ++iters;
+      }
+      exact_block<LPR, E, VEC>(p, need_ex, q, gw, p.b - it - 1, SL, SR, rs, xs, D, d, e2, leaf_sum,
+                               leaf_st, leaf_ln, nl, nr, bi, bj, iters, flags, Lbest, BLf);
+      ++it;
+    }
+    // Phase B: the remaining iterations, with the float64 loop condition
+    // (clipping.py:180) and widths down to W <= 0 (exact decisions only).
+    for (;; ++it) {
       if ((flags & F_ACTIVE) && (it >= p.it_exact_from || (flags & F_EXACT_ONLY))) {   // :180
         const double lhs = __dadd_rn(__dadd_rn(R.x0, __dmul_rn((double)nl, R.step)), R.min_steps);
         const double rhs = __dsub_rn(R.x1, __dmul_rn((double)nr, R.step));
@@ -650,17 +843,16 @@ __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Para
       if (W >= 1) {
         const float Wf = (float)W;
         float aL, aR;
-        eval_pair<E, !VEC>(Yh, nv, (float)(15 * (nl + 1)), -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+        eval_pair<E, !VEC>(ys4, nv, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
         group_sum_pair<LPR>(aL, aR, SL, SR);
-        const float cw = c0 + p.kmis * Wf * Wf;
         const bool goL = SL < SR;
         const float cand = goL ? SL : SR;
-        const float mlr = fmaxf(SL, SR), mb = fmaxf(cand, Lbest);
-        const bool near_lr = fabsf(SL - SR) <= tau2 * mlr + c1 * sqrt_approx(mlr) + cw;
-        const bool near_b = fabsf(cand - Lbest) <= tau2 * mb + c1 * sqrt_approx(mb) + cw;
-        need_ex = (flags & F_ACTIVE) && ((flags & F_EXACT_ONLY) || near_lr || near_b);
+        const float mall = fmaxf(fmaxf(SL, SR), Lbest);
+        const float band = p.tau2 * mall + p.c1 * sqrt_approx(mall) + (p.c0 + p.kmis * Wf * Wf);
+        need_ex = (flags & F_ACTIVE) &&
+                  ((flags & F_EXACT_ONLY) || fabsf(SL - SR) <= band || fabsf(cand - Lbest) <= band);
         if ((flags & F_ACTIVE) && !need_ex) {
-          if (goL) ++nl; else ++nr;
+          if (goL) { ++nl; BLf += 15.f; } else { ++nr; }
           if (cand < Lbest) {
             Lbest = cand; bi = nl; bj = nr;
             flags &= ~F_BEST_EX;
@@ -668,40 +860,9 @@ __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Para
           ++iters;
         }
       }
-      unsigned bal = __ballot_sync(FULL, need_ex && q == 0);
-      if (bal) {
-        while (bal) {
-          const int leader = __ffs(bal) - 1;
-          bal &= bal - 1;
-          const int lg = leader / LPR;
-          const ExactOut o = exact_decide(
-              &rs[lg], (double)__shfl_sync(FULL, nl, leader), (double)__shfl_sync(FULL, nr, leader),
-              __shfl_sync(FULL, bi, leader), __shfl_sync(FULL, bj, leader),
-              (__shfl_sync(FULL, flags, leader) & F_BEST_EX) != 0, xs + lg * D, d, e2, leaf_sum,
-              leaf_st, leaf_ln);
-          if (lg == gw) {
-            if (o.flags & 1) {
-              flags = (flags & ~F_ACTIVE) | F_ERR;
-            } else {
-              const bool goL = (o.flags & 2) != 0;
-              const double vc = goL ? o.vL : o.vR;
-              if (goL) ++nl; else ++nr;
-              if (o.flags & 4) {
-                bi = nl; bj = nr;
-                if (q == 0) R.best_ex = vc;
-                Lbest = (W >= 1) ? (goL ? SL : SR) : (float)(vc * R.kY2);
-              } else if (q == 0) {
-                R.best_ex = o.vb;
-              }
-              flags |= F_BEST_EX;
-              ++iters;
-            }
-          }
-          __syncwarp();
-        }
-        // the exact path clobbered the registers: rebuild the row slice
-        make_Y<LPR, E, VEC>(p, xr, q, nv, R.x0, R.kY, (flags & F_ACTIVE) != 0, Yh);
-      }
+      if (__any_sync(FULL, need_ex))
+        exact_block<LPR, E, VEC>(p, need_ex, q, gw, W, SL, SR, rs, xs, D, d, e2, leaf_sum, leaf_st,
+                                 leaf_ln, nl, nr, bi, bj, iters, flags, Lbest, BLf);
     }
 
     // ---- result, codes, pack ----
@@ -715,14 +876,12 @@ __global__ void __launch_bounds__(NTHREADS, E <= 32 ? 2 : 1) k_greedy(const Para
       hi = bj == 0 ? R.x1 : __dsub_rn(R.x1, __dmul_rn((double)bj, R.step));
       if (rvalid && !bad && mn != mx) { info0 = iters; info1 = (bi << 16) | bj; }
     }
-    {
-      float v[E];
-#pragma unroll
-      for (int i = 0; i < E; ++i)
-        v[i] = (VEC || i < nv) ? xr[VEC ? 4 * (q + LPR * (i >> 2)) + (i & 3) : q + LPR * i] : 0.f;
-      emit_row<LPR, E, VEC>(p, v, nv, lo, hi, !bad && !(flags & F_ERR), rvalid, q,
-                            out_tile + gw * p.stride, codes_w + gw * D);
-    }
+    const int blk_rows = (int)min((int64_t)RPW, p.rows - row0);
+    const size_t gofs = (size_t)row0 * p.stride;
+    uint8_t* out_tile = out_base + (((uintptr_t)p.packed + gofs) & 15);
+    emit_greedy<LPR, E, VEC>(p, ys4, nv, q, lo, hi, bi, bj, mn != mx,
+                             rvalid && !bad && !(flags & F_ERR), rvalid, xr,
+                             out_tile + gw * p.stride, codes_w + gw * D);
     if (rvalid && q == 0) {
       if (p.lo_out) { p.lo_out[row] = lo; p.hi_out[row] = hi; }
       if (p.info0) p.info0[row] = info0;
@@ -862,17 +1021,17 @@ static int sm_count() {
 
 template <typename Kern>
 static int launch_persistent(Kern kern, size_t smem, int64_t ntiles, const Params& p, cudaStream_t s,
-                             const char* name) {
+                             const char* name, int nthreads = NTHREADS) {
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   }
   int occ = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NTHREADS, smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthreads, smem);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy");
   if (occ < 1) occ = 1;
   int64_t grid = std::min<int64_t>(ntiles, (int64_t)sm_count() * occ);
-  kern<<<(unsigned)grid, NTHREADS, smem, s>>>(p);
+  kern<<<(unsigned)grid, nthreads, smem, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, name);
   return EQ4_OK;
@@ -886,8 +1045,9 @@ static int launch_rq(const Params& p, cudaStream_t s) {
                              p, s, "k_asym");
   } else {
     using S = WarpSliceG<LPR, E, VEC>;
-    return launch_persistent(k_greedy<LPR, E, VEC>, NWARPS * S::bytes(p.stride),
-                             (p.rows + S::RPW * NWARPS - 1) / (S::RPW * NWARPS), p, s, "k_greedy");
+    return launch_persistent(k_greedy<LPR, E, VEC>, NWARPS_G * S::bytes(p.stride),
+                             (p.rows + S::RPW * NWARPS_G - 1) / (S::RPW * NWARPS_G), p, s, "k_greedy",
+                             NTHREADS_G);
   }
 }
 
@@ -899,7 +1059,9 @@ static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
       case 16: return METHOD == M_ASYM ? launch_rq<METHOD, 2, 8, true>(p, s)
                                        : launch_rq<METHOD, 1, 16, true>(p, s);
       case 32: return launch_rq<METHOD, 2, 16, true>(p, s);
-      case 64: return launch_rq<METHOD, 4, 16, true>(p, s);
+      case 64:
+        if (METHOD == M_GREEDY && getenv("EQ4_G64_E32")) return launch_rq<METHOD, 2, 32, true>(p, s);
+        return launch_rq<METHOD, 4, 16, true>(p, s);
       case 128: return launch_rq<METHOD, 8, 16, true>(p, s);
       case 256: return launch_rq<METHOD, 16, 16, true>(p, s);
       case 512: return launch_rq<METHOD, 32, 16, true>(p, s);
@@ -990,6 +1152,11 @@ int eq4_quantize_pack(const float* x, int64_t rows, int64_t dim, int64_t ld, int
     // boundary, each adding <= 2*eta*W^2 to the loss; allow 2 per side, both
     // sides.
     p.kmis = (float)(2.0 * 2.0 * 2.0 * 4.0 * 5.9604645e-8 * 15.75);
+    // rows with max|x| <= 1e6 (max - min) (others run exact_only): the
+    // reference's rounded grid moves its losses by <= 3e-14 * 1e6 relative
+    p.tau2 += (float)(2.0 * 3e-14 * 1e6);
+    p.c1 = (float)(4.2 * p.delta * std::sqrt((double)dim));
+    p.c0 = (float)(2.1 * (double)dim * p.delta * p.delta);
     return dispatch_rq<M_GREEDY>(p, vec, s);
   }
   if (method == EQ4_METHOD_HIST_BRUTE)
