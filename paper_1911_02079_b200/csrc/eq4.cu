@@ -63,6 +63,9 @@ enum { M_ASYM = 0, M_GREEDY = 1 };
 #ifndef GREEDY_MINB
 #define GREEDY_MINB 4
 #endif
+#ifndef G_MINB32
+#define G_MINB32 3
+#endif
 
 struct Params {
   const float* x;
@@ -704,7 +707,7 @@ __device__ __forceinline__ void exact_block(const Params& p, bool need_ex, int q
 
 
 template <int LPR, int E, bool VEC>
-__global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ? GREEDY_MINB * 2 / 3 : GREEDY_MINB / 3)) k_greedy(const Params p) {
+__global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ? G_MINB32 : GREEDY_MINB / 3)) k_greedy(const Params p) {
   using S = WarpSliceG<LPR, E, VEC>;
   constexpr int RPW = S::RPW;
   constexpr int D = S::D;
@@ -1039,7 +1042,7 @@ static int launch_persistent(Kern kern, size_t smem, int64_t ntiles, const Param
 
 template <int METHOD, int LPR, int E, bool VEC>
 static int launch_rq(const Params& p, cudaStream_t s) {
-  if (METHOD == M_ASYM) {
+  if constexpr (METHOD == M_ASYM) {
     using L = LayoutA<LPR, E, VEC>;
     return launch_persistent(k_asym<LPR, E, VEC>, L::total(p.stride), (p.rows + L::RPB - 1) / L::RPB,
                              p, s, "k_asym");
@@ -1054,17 +1057,41 @@ static int launch_rq(const Params& p, cudaStream_t s) {
 template <int METHOD>
 static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
   const int d = p.d;
+  if constexpr (METHOD == M_ASYM) {
+    if (vec) {
+      switch (d) {
+        case 16: return launch_rq<METHOD, 2, 8, true>(p, s);
+        case 32: return launch_rq<METHOD, 2, 16, true>(p, s);
+        case 64: return launch_rq<METHOD, 4, 16, true>(p, s);
+        case 128: return launch_rq<METHOD, 8, 16, true>(p, s);
+        case 256: return launch_rq<METHOD, 16, 16, true>(p, s);
+        case 512: return launch_rq<METHOD, 32, 16, true>(p, s);
+        case 1024: return launch_rq<METHOD, 32, 32, true>(p, s);
+        case 2048: return launch_rq<METHOD, 32, 64, true>(p, s);
+        default: break;
+      }
+    }
+    if (d <= 8) return launch_rq<METHOD, 1, 8, false>(p, s);
+    if (d <= 16) return launch_rq<METHOD, 1, 16, false>(p, s);
+    if (d <= 32) return launch_rq<METHOD, 2, 16, false>(p, s);
+    if (d <= 64) return launch_rq<METHOD, 4, 16, false>(p, s);
+    if (d <= 128) return launch_rq<METHOD, 8, 16, false>(p, s);
+    if (d <= 256) return launch_rq<METHOD, 16, 16, false>(p, s);
+    if (d <= 512) return launch_rq<METHOD, 32, 16, false>(p, s);
+    if (d <= 1024) return launch_rq<METHOD, 32, 32, false>(p, s);
+    if (d <= 2048) return launch_rq<METHOD, 32, 64, false>(p, s);
+    return fail(EQ4_EUNSUPPORTED, "dim > 2048 is not supported by the B200 path");
+  } else {
+  // GREEDY: 32 elements per lane amortise the per-iteration decision work
+  // (measured best on 20M x 64; the row slice lives in shared memory)
   if (vec) {
     switch (d) {
-      case 16: return METHOD == M_ASYM ? launch_rq<METHOD, 2, 8, true>(p, s)
-                                       : launch_rq<METHOD, 1, 16, true>(p, s);
-      case 32: return launch_rq<METHOD, 2, 16, true>(p, s);
-      case 64:
-        if (METHOD == M_GREEDY && getenv("EQ4_G64_E32")) return launch_rq<METHOD, 2, 32, true>(p, s);
-        return launch_rq<METHOD, 4, 16, true>(p, s);
-      case 128: return launch_rq<METHOD, 8, 16, true>(p, s);
-      case 256: return launch_rq<METHOD, 16, 16, true>(p, s);
-      case 512: return launch_rq<METHOD, 32, 16, true>(p, s);
+      case 16: return launch_rq<METHOD, 1, 16, true>(p, s);
+      case 32: return launch_rq<METHOD, 1, 32, true>(p, s);
+      case 64: return launch_rq<METHOD, 2, 32, true>(p, s);
+      case 128: return launch_rq<METHOD, 4, 32, true>(p, s);
+      case 256: return launch_rq<METHOD, 8, 32, true>(p, s);
+      case 512: return launch_rq<METHOD, 16, 32, true>(p, s);
       case 1024: return launch_rq<METHOD, 32, 32, true>(p, s);
       case 2048: return launch_rq<METHOD, 32, 64, true>(p, s);
       default: break;
@@ -1072,14 +1099,15 @@ static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
   }
   if (d <= 8) return launch_rq<METHOD, 1, 8, false>(p, s);
   if (d <= 16) return launch_rq<METHOD, 1, 16, false>(p, s);
-  if (d <= 32) return launch_rq<METHOD, 2, 16, false>(p, s);
-  if (d <= 64) return launch_rq<METHOD, 4, 16, false>(p, s);
-  if (d <= 128) return launch_rq<METHOD, 8, 16, false>(p, s);
-  if (d <= 256) return launch_rq<METHOD, 16, 16, false>(p, s);
-  if (d <= 512) return launch_rq<METHOD, 32, 16, false>(p, s);
+  if (d <= 32) return launch_rq<METHOD, 1, 32, false>(p, s);
+  if (d <= 64) return launch_rq<METHOD, 2, 32, false>(p, s);
+  if (d <= 128) return launch_rq<METHOD, 4, 32, false>(p, s);
+  if (d <= 256) return launch_rq<METHOD, 8, 32, false>(p, s);
+  if (d <= 512) return launch_rq<METHOD, 16, 32, false>(p, s);
   if (d <= 1024) return launch_rq<METHOD, 32, 32, false>(p, s);
   if (d <= 2048) return launch_rq<METHOD, 32, 64, false>(p, s);
   return fail(EQ4_EUNSUPPORTED, "dim > 2048 is not supported by the B200 path");
+  }
 }
 
 // GREEDY error-band constants: per side, the fp32
@@ -1088,8 +1116,8 @@ static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
 static float tau2_for(int d) {
   int lpr, e;
   if (d <= 16) { lpr = 1; e = 16; }
-  else if (d <= 512) { lpr = 1; while (lpr * 16 < d) lpr *= 2; e = 16; }
-  else if (d <= 1024) { lpr = 32; e = 32; }
+  else if (d <= 32) { lpr = 1; e = 32; }
+  else if (d <= 1024) { lpr = 1; while (lpr * 32 < d) lpr *= 2; e = 32; }
   else { lpr = 32; e = 64; }
   int lg = 0;
   while ((1 << lg) < lpr) lg++;
@@ -1134,12 +1162,15 @@ int eq4_quantize_pack(const float* x, int64_t rows, int64_t dim, int64_t ld, int
   if (method == EQ4_METHOD_ASYM) return dispatch_rq<M_ASYM>(p, vec, s);
   if (method == EQ4_METHOD_GREEDY) {
     if (b > 65535) return fail(EQ4_EUNSUPPORTED, "b > 65535 is not supported by the B200 path");
-    // loop iterations it with it <= b - b(1-r) - 3 have a condition that holds
-    // by a margin of >= 2 steps, far above float64 rounding of the row
-    // (rows where rounding could matter run exact_only).
-    double B1 = (double)b * (1.0 - r);
-    double T = (double)b - B1;
-    p.it_exact_from = std::max(0, (int)std::floor(T) - 3);
+    // Loop condition (clipping.py:180) at iteration it, i.e. after it moves
+    // (nl + nr == it): exactly  (it + b(1-r)) * step < x1 - x0  <=>  it < T with
+    // T = b - b(1-r).  For it <= T - 1 the two sides differ by >= one step,
+    // far beyond the float64 rounding of a row with max|x| <= 1e6 (max - min)
+    // (wider-magnitude rows run exact_only and always evaluate it), so the
+    // first iteration that needs the float64 test is floor(T).
+    const double B1 = (double)b * (1.0 - r);
+    const double T = (double)b - B1;
+    p.it_exact_from = T >= 1.0 ? (int)std::floor(T) : 0;
     int ey = 0;
     while (std::ldexp(1.0, ey) <= 15.0 * b) ey++;
     p.qY = std::ldexp(1.0, ey - 24);
