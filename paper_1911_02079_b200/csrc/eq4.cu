@@ -471,6 +471,36 @@ __device__ __forceinline__ void warp_copy_out(uint8_t* dst, const uint8_t* src, 
   for (int i = tail + lane; i < nbytes; i += 32) dst[i] = src[i];
 }
 
+// ---------------------------------------------------------------------------
+// Packed fp32x2 arithmetic (sm_100: one instruction, two IEEE fp32 lanes).
+// The FP32 pipe throughput is unchanged, but every packed instruction frees
+// an issue slot for the search's bookkeeping.
+// ---------------------------------------------------------------------------
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t pk2(float a, float b) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(f2_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2_t fma2_rm(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
 #ifndef G_UNROLL
 #define G_UNROLL 4
 #endif
@@ -532,6 +562,45 @@ __device__ __forceinline__ void eval_pair(const float4* ys4, int nv, float BL, f
   }
   aL = sL;
   aR = sR;
+}
+
+// Packed variant of eval_pair (vector kernels): element pairs share one
+// instruction for z, the round-down code, the code removal, the error and the
+// accumulation; only the saturating FFMA stays scalar (no .sat for f32x2).
+// 3.5 issue slots per element and candidate instead of 6.
+template <int E>
+__device__ __forceinline__ void eval_pair_x2(const float4* ys4, float BL, float nW, float kW,
+                                             float h, float& aL, float& aR) {
+  const int lane = threadIdx.x & 31;
+  const f2_t nBL2 = pk2(-BL, -BL), c15 = pk2(15.f, 15.f), al2 = pk2(ALPHA, ALPHA);
+  const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
+  f2_t sL = pk2(0.f, 0.f), sR = pk2(0.f, 0.f);
+#pragma unroll kGUnroll
+  for (int c = 0; c < E / 4; ++c) {
+    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32 + lane);
+#pragma unroll
+    for (int hlf = 0; hlf < 2; ++hlf) {
+      const f2_t y2 = hlf ? yy.y : yy.x;
+      const f2_t zL = add2(y2, nBL2);
+      const f2_t zR = add2(zL, c15);                                   // exact
+      float a0, a1, b0, b1;
+      upk2(zL, a0, a1);
+      upk2(zR, b0, b1);
+      const f2_t tL = pk2(sat_fma(a0, kW, h), sat_fma(a1, kW, h));
+      const f2_t tR = pk2(sat_fma(b0, kW, h), sat_fma(b1, kW, h));
+      const f2_t cL = add2(fma2_rm(tL, al2, mg2), nmg2);              // floor(alpha * t)
+      const f2_t cR = add2(fma2_rm(tR, al2, mg2), nmg2);
+      const f2_t eL = fma2(cL, nW2, zL);                               // exact
+      const f2_t eR = fma2(cR, nW2, zR);
+      sL = fma2(eL, eL, sL);
+      sR = fma2(eR, eR, sR);
+    }
+  }
+  float l0, l1, r0, r1;
+  upk2(sL, l0, l1);
+  upk2(sR, r0, r1);
+  aL = __fadd_rn(l0, l1);
+  aR = __fadd_rn(r0, r1);
 }
 
 // Y coordinates on the exact fp32 grid of quantum qY (see file header).
@@ -799,7 +868,10 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       for (; it < itA; ++it) {
         const float Wf = (float)(p.b - it - 1);
         float aL, aR;
-        eval_pair<E, !VEC>(ys4, nv, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+        if constexpr (VEC)
+          eval_pair_x2<E>(ys4, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+        else
+          eval_pair<E, true>(ys4, nv, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
         group_sum_pair<LPR>(aL, aR, SL, SR);
         goL = SL < SR;                                                   // clipping.py:185
         cand = goL ? SL : SR;
