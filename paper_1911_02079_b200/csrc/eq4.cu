@@ -64,7 +64,10 @@ enum { M_ASYM = 0, M_GREEDY = 1 };
 #define GREEDY_MINB 4
 #endif
 #ifndef G_MINB32
-#define G_MINB32 3
+#define G_MINB32 4
+#endif
+#ifndef G_MINB64
+#define G_MINB64 1
 #endif
 
 struct Params {
@@ -675,58 +678,61 @@ __device__ __forceinline__ void emit_greedy(const Params& p, const float4* ys4, 
   const float h = 0.5f / ALPHA;
   const float nb = NEAR + p.delta / Wf;
   const bool fast = fast_ok && Wb >= 1 && ok;
-  unsigned long long need = 0ull;
-  uint32_t mb[E];
   const int lane = threadIdx.x & 31;
+  unsigned long long need = 0ull;
+  // streamed chunk by chunk (no per-slot arrays): codes go straight to the
+  // staged row; flagged slots are rewritten below
 #pragma unroll
-  for (int i = 0; i < E; ++i) {
-    const float4 y4 = ys4[(i >> 2) * 32 + lane];
-    const float yi = (i & 3) == 0 ? y4.x : (i & 3) == 1 ? y4.y : (i & 3) == 2 ? y4.z : y4.w;
-    const float z = __fadd_rn(yi, -B);
-    const float s = sat_fma(z, kW, h);
-    const float m = __fmaf_rd(s, ALPHA, MAGIC);
-    const float f = __fmaf_rn(s, ALPHA, -__fadd_rn(m, -MAGIC));   // frac of alpha*s, exact
-    const bool nr_ = s > 0.f && s < 1.f && (f < nb || f > 1.f - nb);
-    need |= (unsigned long long)(nr_ && (VEC || i < nv)) << i;
-    mb[i] = __float_as_uint(m) & 0xFu;
+  for (int c = 0; c < E / 4; ++c) {
+    const float4 y4 = ys4[c * 32 + lane];
+    const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
+    uint32_t w = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = 4 * c + k;
+      const float z = __fadd_rn(yv[k], -B);
+      const float sv = sat_fma(z, kW, h);
+      const float m = __fmaf_rd(sv, ALPHA, MAGIC);
+      const float f = __fmaf_rn(sv, ALPHA, -__fadd_rn(m, -MAGIC));   // frac of alpha*s, exact
+      const bool nr_ = sv > 0.f && sv < 1.f && (f < nb || f > 1.f - nb);
+      need |= (unsigned long long)(nr_ && (VEC || i < nv)) << i;
+      const uint32_t code = ok ? (__float_as_uint(m) & 0xFu) : 0u;
+      if (VEC) {
+        w |= code << (4 * k);
+      } else if (rvalid && i < nv) {
+        crow[q + LPR * i] = (uint8_t)code;
+      }
+    }
+    if (VEC && rvalid) *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = (uint16_t)w;
   }
   if (!fast) need = ok ? ((nv >= 64) ? ~0ull : ((1ull << nv) - 1ull)) : 0ull;
   if (!rvalid) need = 0ull;
-  if (__any_sync(FULL, need != 0ull)) {   // rare: float64 codec for flagged elements
+  if (__any_sync(FULL, need != 0ull)) {   // rare: float64 codec (uniform.py:77-79)
     if (need) {
       const CodeParams cp = make_code_params(lo, hi);
-      for (int i = 0; i < E; ++i)
-        if ((need >> i) & 1ull)
-          mb[i] = code_exact(xr[VEC ? 4 * (q + LPR * (i >> 2)) + (i & 3) : q + LPR * i], cp);
+      for (int i = 0; i < E; ++i) {
+        if (!((need >> i) & 1ull)) continue;
+        const unsigned cc = code_exact(xr[VEC ? 4 * (q + LPR * (i >> 2)) + (i & 3) : q + LPR * i], cp);
+        if (VEC) {
+          const int byte = 2 * (q + LPR * (i >> 2)) + ((i & 3) >> 1);
+          const int sh = (i & 1) * 4;
+          orow[byte] = (uint8_t)((orow[byte] & ~(0xF << sh)) | (cc << sh));
+        } else {
+          crow[q + LPR * i] = (uint8_t)cc;
+        }
+      }
     }
   }
-  if (!ok) {
-#pragma unroll
-    for (int i = 0; i < E; ++i) mb[i] = 0u;
-  }
-  if (rvalid) {
-    if (VEC) {
-#pragma unroll
-      for (int c = 0; c < E / 4; ++c) {
-        const uint32_t w = mb[4 * c] | (mb[4 * c + 1] << 4) | (mb[4 * c + 2] << 8) | (mb[4 * c + 3] << 12);
-        *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = (uint16_t)w;
-      }
+  if (rvalid && q == 0) {
+    const double sc = (ok && hi != lo) ? div15(__dsub_rn(hi, lo)) : 0.0;   // uniform.py:74-80
+    uint8_t* a = orow + p.half;
+    if (p.aux == EQ4_AUX_FP16) {
+      const uint32_t s16 = aux_bits_f16(sc), b16 = aux_bits_f16(lo);
+      a[0] = s16 & 0xff; a[1] = s16 >> 8; a[2] = b16 & 0xff; a[3] = b16 >> 8;
     } else {
+      const uint32_t s32 = aux_bits_f32(sc), b32 = aux_bits_f32(lo);
 #pragma unroll
-      for (int i = 0; i < E; ++i)
-        if (i < nv) crow[q + LPR * i] = (uint8_t)mb[i];
-    }
-    if (q == 0) {
-      const double sc = (ok && hi != lo) ? div15(__dsub_rn(hi, lo)) : 0.0;   // uniform.py:74-80
-      uint8_t* a = orow + p.half;
-      if (p.aux == EQ4_AUX_FP16) {
-        const uint32_t s16 = aux_bits_f16(sc), b16 = aux_bits_f16(lo);
-        a[0] = s16 & 0xff; a[1] = s16 >> 8; a[2] = b16 & 0xff; a[3] = b16 >> 8;
-      } else {
-        const uint32_t s32 = aux_bits_f32(sc), b32 = aux_bits_f32(lo);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) { a[k] = (s32 >> (8 * k)) & 0xff; a[4 + k] = (b32 >> (8 * k)) & 0xff; }
-      }
+      for (int k = 0; k < 4; ++k) { a[k] = (s32 >> (8 * k)) & 0xff; a[4 + k] = (b32 >> (8 * k)) & 0xff; }
     }
   }
 }
@@ -776,7 +782,7 @@ __device__ __forceinline__ void exact_block(const Params& p, bool need_ex, int q
 
 
 template <int LPR, int E, bool VEC>
-__global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ? G_MINB32 : GREEDY_MINB / 3)) k_greedy(const Params p) {
+__global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ? G_MINB32 : G_MINB64)) k_greedy(const Params p) {
   using S = WarpSliceG<LPR, E, VEC>;
   constexpr int RPW = S::RPW;
   constexpr int D = S::D;
@@ -809,7 +815,6 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
     float mn, mx;
     bool bad;
     {
-      float Yh[E];
       float v[E];
       load_row<LPR, E, VEC>(p, row, rvalid, q, nv, v);
       if (VEC) {
@@ -827,14 +832,19 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       const double Dw = __dsub_rn(x1, x0);
       const double step = __ddiv_rn(Dw, (double)p.b);                               // :172
       const double kY = (x0 != x1) ? __ddiv_rn(15.0, step) : 0.0;
+      // Y on the exact fp32 grid of quantum qY: Y + C rounds to a multiple of qY
+      // (C = 1.5 * 2^52 * qY, same ties-to-even result as rint(Y / qY) * qY)
+      const double cY = 6755399441055744.0 * p.qY;
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const double Y = __dmul_rn(__dsub_rn((double)v[i], x0), kY);
-        Yh[i] = (float)(rint(Y * p.inv_qY) * p.qY);
+      for (int c = 0; c < E / 4; ++c) {
+        float y[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double Y = __dmul_rn(__dsub_rn((double)v[4 * c + k], x0), kY);
+          y[k] = (float)__dsub_rn(__dadd_rn(Y, cY), cY);
+        }
+        ys4[c * 32 + lane] = make_float4(y[0], y[1], y[2], y[3]);
       }
-#pragma unroll
-      for (int c = 0; c < E / 4; ++c)
-        ys4[c * 32 + lane] = make_float4(Yh[4 * c], Yh[4 * c + 1], Yh[4 * c + 2], Yh[4 * c + 3]);
       if (q == 0) {
         R.x0 = x0; R.x1 = x1; R.step = step;
         R.min_steps = __dmul_rn(__dmul_rn((double)p.b, __dsub_rn(1.0, p.r)), step);  // :173
@@ -1160,7 +1170,12 @@ static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
     switch (d) {
       case 16: return launch_rq<METHOD, 1, 16, true>(p, s);
       case 32: return launch_rq<METHOD, 1, 32, true>(p, s);
-      case 64: return launch_rq<METHOD, 2, 32, true>(p, s);
+      case 64: {
+        const char* v = getenv("EQ4_G64");
+        if (v && v[0] == '1') return launch_rq<METHOD, 1, 64, true>(p, s);
+        if (v && v[0] == '4') return launch_rq<METHOD, 4, 16, true>(p, s);
+        return launch_rq<METHOD, 2, 32, true>(p, s);
+      }
       case 128: return launch_rq<METHOD, 4, 32, true>(p, s);
       case 256: return launch_rq<METHOD, 8, 32, true>(p, s);
       case 512: return launch_rq<METHOD, 16, 32, true>(p, s);
