@@ -71,6 +71,7 @@ def lib():
         L.eqo_bin_l2_norm.restype = dbl
         L.eqo_offset_unit_norms.argtypes = [vp, i64, dbl, dbl, vp]
         L.eqo_hist_brute.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.eqo_hist_window_norm.argtypes = [vp, i64, i32, i32, i32, vp, vp]
         L.eqo_quantize_uniform.argtypes = [vp, i64, dbl, dbl, i32, i32, vp, vp, vp]
         L.eqo_pack_table4.argtypes = [vp, i64, i64, i32, vp, vp, vp]
         L.eqo_packed_row_stride.argtypes = [i64, i32]
@@ -171,6 +172,17 @@ def hist_brute_search(x, b: int = 200) -> HistResult:
         raise OracleError(rc)
     return HistResult(float(lo[0]), float(hi[0]), int(st[0]), int(ns[0]), float(norm[0]),
                       int(ce[0]), int(bv[0]))
+
+
+def hist_window_norm(x, b: int, start: int, n: int) -> float:
+    """Norm of one (start, n) window as histclip.py:152-161 computes it (test helper)."""
+    x = _f32(x)
+    out = np.zeros(1)
+    scratch = np.empty(max(16, 5 * b), np.float64)
+    rc = lib().eqo_hist_window_norm(_p(x), x.size, b, start, n, _p(out), _p(scratch))
+    if rc:
+        raise OracleError(rc)
+    return float(out[0])
 
 
 def quantize_uniform(x, xmin: float, xmax: float, nbits: int = 4, aux: str = "fp32"):

@@ -283,6 +283,29 @@ int eqo_hist_brute(const float *x, long d, int b, double *lo, double *hi, int *s
     return EQO_OK;
 }
 
+/* Norm of one window (start s, width n) as histclip.py:152-161 computes it
+ * (plain ascending-j sum in place of BLAS).  Used by tests to classify a
+ * differing selection as a norm tie.  scratch: >= 5*b doubles. */
+int eqo_hist_window_norm(const float *x, long d, int b, int s, int n, double *out, double *scratch) {
+    if (b < 1 || n < 1 || s < 0 || s + n > b) return EQO_EB;
+    int64_t *counts = (int64_t *)malloc(sizeof(int64_t) * (size_t)b);
+    if (!counts) return EQO_EALLOC;
+    double lo, hi;
+    eqo_build_histogram(x, d, b, &lo, &hi, counts);
+    if (lo == hi) { *out = 0.0; free(counts); return EQO_OK; }
+    double w = (hi - lo) / (double)b;
+    double *density = scratch, *offsets = scratch + b, *contrib = scratch + 3 * (long)b;
+    for (int j = 0; j < b; j++) density[j] = (double)counts[j] / w;
+    for (int i = 0; i < 2 * b - 1; i++) offsets[i] = (double)(i - (b - 1));
+    double dst_w = w * (double)n / (double)(DST_NBINS - 1);
+    eqo_offset_unit_norms(offsets, 2 * b - 1, w, dst_w, contrib);
+    double acc = 0.0;
+    for (int j = 0; j < b; j++) acc += density[j] * contrib[(j - s) + (b - 1)];
+    *out = acc;
+    free(counts);
+    return EQO_OK;
+}
+
 /* uniform.py:60-80 quantize_uniform; aux 0 = fp32, 1 = fp16 (uniform.py:19-35).
  * scale/bias are written as the stored aux value (little-endian bytes). */
 int eqo_quantize_uniform(const float *xf, long d, double xmin, double xmax, int nbits, int aux,

@@ -46,6 +46,7 @@
 
 #include "../../include/eq4.h"
 #include "eq4_device.cuh"
+#include "eq4_internal.h"
 
 namespace eq4 {
 
@@ -1277,8 +1278,12 @@ int eq4_quantize_pack(const float* x, int64_t rows, int64_t dim, int64_t ld, int
     p.c0 = (float)(2.1 * (double)dim * p.delta * p.delta);
     return dispatch_rq<M_GREEDY>(p, vec, s);
   }
-  if (method == EQ4_METHOD_HIST_BRUTE)
-    return fail(EQ4_EUNSUPPORTED, "hist-brute not built yet");
+  if (method == EQ4_METHOD_HIST_BRUTE) {
+    std::string err;
+    const int rc = eq4_hist_launch(x, rows, dim, ld, b, aux, packed, xmin, xmax, info0, info1, norm,
+                                   status, s, err);
+    return rc == EQ4_OK ? rc : fail(rc, err);
+  }
   return fail(EQ4_EINVAL, "unknown method " + std::to_string(method));
 }
 

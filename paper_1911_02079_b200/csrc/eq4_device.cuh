@@ -82,7 +82,7 @@ __device__ __forceinline__ int np_leaves(int n, int* starts, int* lens, int max_
 }
 
 // Combine leaf sums in the recursion's association order.
-__device__ __noinline__ double np_combine(int n, const double* leaf_sum, int* li) {
+static __device__ __noinline__ double np_combine(int n, const double* leaf_sum, int* li) {
   if (n <= 128) return leaf_sum[(*li)++];
   int n2 = n / 2;
   n2 -= n2 % 8;
@@ -101,7 +101,7 @@ __device__ __noinline__ double np_combine(int n, const double* leaf_sum, int* li
 // accumulator chains, a 3-level butterfly forms ((r0+r1)+(r2+r3))+(...),
 // lane 0 adds the leaf's remainder, and lane 0 combines leaf sums in the
 // recursion's association order.
-__device__ __noinline__ double warp_np_loss(const float* xs, int d, double lo, double hi,
+static __device__ __noinline__ double warp_np_loss(const float* xs, int d, double lo, double hi,
                                             double* e2, double* leaf_sum, int* leaf_start,
                                             int* leaf_len, int max_leaves) {
   const int lane = threadIdx.x & 31;

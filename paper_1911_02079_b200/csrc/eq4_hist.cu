@@ -1,0 +1,280 @@
+// eq4_hist.cu -- HIST-BRUTE (histclip.py:136-178) window search on sm_100a.
+//
+// Reference: for every width n = 1..b and start s = 0..b-n the window's norm is
+//   norm(s, n) = sum_j density[j] * contrib_n[j - s]            (histclip.py:157-161)
+// with density = counts / w and contrib_n from _offset_unit_norms
+// (histclip.py:85-109), which scales exactly as w^3 * U_n(k) with U_n the
+// bin-width-1 table.  So norm = w^2 * sum_j counts[j] U_n(j - s) and the
+// argmin does not depend on w.  U_n(k) has closed forms outside the window:
+//   k < 0 :  ((k+1)^3 - k^3) / 3                (both ends clip to dst point 0)
+//   k >= n:  ((k+1-n)^3 - (k-n)^3) / 3          (both ends clip to dst point 15)
+// so the outside part of every window is a prefix/suffix sum over the
+// non-empty bins (integer arithmetic, exact in float64), and only the bins
+// inside the window need the U table:
+//   norm / w^2 = (A3[s] + R3[s + n]) / 3 + sum_{s <= j < s+n} counts[j] U_n(j - s).
+// The U table (b(b+1)/2 doubles) is built once per b on the device and cached.
+// Work per row: b(b+1)/2 windows x (non-empty bins inside) fused
+// multiply-adds instead of the reference's b * b(b+1)/2 bin visits.
+//
+// Float64 throughout; the first minimum in (n ascending, s ascending) order is
+// kept (histclip.py:165-168) with a lexicographic warp reduction.  The
+// reference's norms come from BLAS dot products whose summation order is CPU
+// specific, so only windows whose norms tie to ~1e-13 relative can select
+// differently.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "../../include/eq4.h"
+#include "eq4_device.cuh"
+#include "eq4_internal.h"
+
+namespace eq4 {
+
+__device__ __forceinline__ double cube(double x) { return __dmul_rn(__dmul_rn(x, x), x); }
+
+// histclip.py:70-82 bin_l2_norm with density 1
+__device__ __forceinline__ double l2unit(double db, double de) {
+  return __ddiv_rn(__dsub_rn(cube(de), cube(db)), 3.0);
+}
+
+// U[(n-1)n/2 + k] = _offset_unit_norms(k, 1, n/15) for k in [0, n)   (histclip.py:85-109)
+__global__ void k_hist_table(int b, double* U) {
+  const int n = blockIdx.x + 1;
+  if (n > b) return;
+  const double dst_w = __ddiv_rn((double)n, 15.0);   // histclip.py:158 (w * n / 15, w = 1)
+  const double half = __dmul_rn(0.5, dst_w);
+  double* Un = U + (size_t)(n - 1) * n / 2;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const double begin = (double)k, end = __dadd_rn(begin, 1.0);
+    const double dob = np_clip(floor(__ddiv_rn(__dadd_rn(begin, half), dst_w)), 0.0, 15.0);
+    const double doe = np_clip(floor(__ddiv_rn(__dadd_rn(end, half), dst_w)), 0.0, 15.0);
+    const double bc = __dmul_rn(dob, dst_w), ec = __dmul_rn(doe, dst_w);
+    const double db = __dsub_rn(begin, bc);
+    const double same = l2unit(db, __dsub_rn(end, bc));
+    const double split = __dadd_rn(__dadd_rn(l2unit(db, half),
+                                             __dmul_rn(__dsub_rn(__dsub_rn(doe, dob), 1.0),
+                                                       l2unit(-half, half))),
+                                   l2unit(-half, __dsub_rn(end, ec)));
+    Un[k] = (dob == doe) ? same : split;
+  }
+}
+
+struct HistParams {
+  const float* x;
+  int64_t rows, ld;
+  int d, b, aux, stride, half;
+  uint8_t* packed;
+  double *lo_out, *hi_out, *norm_out;
+  int32_t *info0, *info1, *status;
+  const double* U;
+};
+
+// Shared-memory slice of one row (one warp per block).
+struct HistSlice {
+  int b, d;
+  __host__ __device__ size_t cnt_off() const { return 0; }                                   // int[b]
+  __host__ __device__ size_t nzj_off() const { return cnt_off() + (size_t)b * 4; }          // int[b]
+  __host__ __device__ size_t lb_off() const { return nzj_off() + (size_t)b * 4; }           // int[b+1]
+  __host__ __device__ size_t a3_off() const { return (lb_off() + (size_t)(b + 1) * 4 + 7) & ~(size_t)7; }
+  __host__ __device__ size_t r3_off() const { return a3_off() + (size_t)(b + 1) * 8; }
+  __host__ __device__ size_t nzc_off() const { return r3_off() + (size_t)(b + 1) * 8; }     // double[b]
+  __host__ __device__ size_t xs_off() const { return nzc_off() + (size_t)b * 8; }           // float[d]
+  __host__ __device__ size_t codes_off() const { return xs_off() + (size_t)d * 4; }         // u8[d]
+  __host__ __device__ size_t bytes() const { return (codes_off() + (size_t)d + 15) & ~(size_t)15; }
+};
+
+__global__ void __launch_bounds__(32) k_hist(const HistParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const HistSlice S{p.b, p.d};
+  int* cnt = reinterpret_cast<int*>(smem + S.cnt_off());
+  int* nzj = reinterpret_cast<int*>(smem + S.nzj_off());
+  int* lb = reinterpret_cast<int*>(smem + S.lb_off());
+  double* A3 = reinterpret_cast<double*>(smem + S.a3_off());
+  double* R3 = reinterpret_cast<double*>(smem + S.r3_off());
+  double* nzc = reinterpret_cast<double*>(smem + S.nzc_off());
+  float* xs = reinterpret_cast<float*>(smem + S.xs_off());
+  uint8_t* codes = smem + S.codes_off();
+  const int lane = threadIdx.x;
+  const int b = p.b, d = p.d;
+
+  for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+    // ---- row, min/max, finiteness ----
+    float mn = INFINITY, mx = -INFINITY;
+    bool bad = false;
+    for (int k = lane; k < d; k += 32) {
+      const float v = p.x[row * p.ld + k];
+      xs[k] = v;
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+      bad |= !isfinite(v);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(FULL, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+    }
+    bad = __any_sync(FULL, bad);
+    if (bad && lane == 0 && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
+    const double lo = (double)mn, hi = (double)mx;
+    double wlo = lo, whi = hi, norm = 0.0;
+    int best_s = 0, best_n = 1;
+    if (!bad && lo != hi) {
+      // ---- histogram (histclip.py:52-67), float64 bin index ----
+      const double w = __ddiv_rn(__dsub_rn(hi, lo), (double)b);
+      for (int j = lane; j < b; j += 32) cnt[j] = 0;
+      __syncwarp();
+      for (int k = lane; k < d; k += 32) {
+        const double q = floor(__ddiv_rn(__dsub_rn((double)xs[k], lo), w));
+        const int idx = (int)np_clip(q, 0.0, (double)(b - 1));
+        atomicAdd(&cnt[idx], 1);
+      }
+      __syncwarp();
+      // ---- non-empty bins (ascending) and lb[x] = #non-empty bins below x ----
+      if (lane == 0) {
+        int m = 0;
+        for (int j = 0; j < b; j++) {
+          lb[j] = m;
+          if (cnt[j]) { nzj[m] = j; nzc[m] = (double)cnt[j]; m++; }
+        }
+        lb[b] = m;
+      }
+      __syncwarp();
+      const int nnz = lb[b];
+      // ---- outside-window parts: 3L(s) and 3R(e), exact integers in float64 ----
+      for (int t = lane; t <= b; t += 32) {
+        double a = 0.0, r = 0.0;
+        for (int i = 0; i < nnz; i++) {
+          const int j = nzj[i];
+          const double c = nzc[i];
+          if (j < t) {
+            const double m = (double)(t - j);                       // k = j - s = -m
+            a += c * (3.0 * m * m - 3.0 * m + 1.0);
+          } else {
+            const double k = (double)(j - t);                       // k - n >= 0
+            r += c * (3.0 * k * k + 3.0 * k + 1.0);
+          }
+        }
+        A3[t] = a;
+        R3[t] = r;
+      }
+      __syncwarp();
+      // ---- every window, first minimum in (n asc, s asc) order ----
+      double bv = INFINITY;
+      int bn = 1 << 30, bs = 1 << 30;
+      for (int n = 1; n <= b; n++) {
+        const double* Un = p.U + (size_t)(n - 1) * n / 2;
+        for (int s = lane; s <= b - n; s += 32) {
+          double acc = 0.0;
+          const int i1 = lb[s + n];
+          for (int i = lb[s]; i < i1; i++) acc = fma(nzc[i], __ldg(Un + (nzj[i] - s)), acc);
+          const double v = (A3[s] + R3[s + n]) * (1.0 / 3.0) + acc;
+          if (v < bv) { bv = v; bn = n; bs = s; }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const double ov = __shfl_xor_sync(FULL, bv, o);
+        const int on = __shfl_xor_sync(FULL, bn, o), os = __shfl_xor_sync(FULL, bs, o);
+        if (ov < bv || (ov == bv && (on < bn || (on == bn && os < bs)))) { bv = ov; bn = on; bs = os; }
+      }
+      best_s = bs;
+      best_n = bn;
+      wlo = __dadd_rn(lo, __dmul_rn(w, (double)bs));                 // histclip.py:170
+      whi = __dadd_rn(lo, __dmul_rn(w, (double)(bs + bn)));
+      norm = bv * w * w;
+    }
+    // ---- codes (uniform.py:60-80) + packed row (packed.py:68-83) ----
+    const bool ok = !bad;
+    const CodeParams cp = make_code_params(ok ? wlo : 0.0, ok ? whi : 0.0);
+    for (int k = lane; k < d; k += 32) {
+      bool ne;
+      unsigned c = code_of(xs[k], cp, ne);
+      if (ne) c = code_exact(xs[k], cp);
+      codes[k] = ok ? (uint8_t)c : 0;
+    }
+    __syncwarp();
+    uint8_t* orow = p.packed + row * (int64_t)p.stride;
+    for (int m = lane; m < p.half; m += 32) {
+      const unsigned c0 = codes[2 * m];
+      const unsigned c1 = (2 * m + 1 < d) ? codes[2 * m + 1] : 0u;
+      orow[m] = (uint8_t)(c0 | (c1 << 4));
+    }
+    if (lane == 0) {
+      const double sc = (ok && whi != wlo) ? div15(__dsub_rn(whi, wlo)) : 0.0;
+      uint8_t* a = orow + p.half;
+      if (p.aux == EQ4_AUX_FP16) {
+        const uint32_t s16 = aux_bits_f16(sc), b16 = aux_bits_f16(wlo);
+        a[0] = s16 & 0xff; a[1] = s16 >> 8; a[2] = b16 & 0xff; a[3] = b16 >> 8;
+      } else {
+        const uint32_t s32 = aux_bits_f32(sc), b32 = aux_bits_f32(wlo);
+        for (int k = 0; k < 4; ++k) { a[k] = (s32 >> (8 * k)) & 0xff; a[4 + k] = (b32 >> (8 * k)) & 0xff; }
+      }
+      if (p.lo_out) { p.lo_out[row] = wlo; p.hi_out[row] = whi; }
+      if (p.info0) p.info0[row] = best_s;
+      if (p.info1) p.info1[row] = best_n;
+      if (p.norm_out) p.norm_out[row] = norm;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace eq4
+
+using namespace eq4;
+
+// U tables cached per (device, b); built once with k_hist_table.
+static std::mutex g_u_mu;
+static std::map<std::pair<int, int>, double*> g_u_tables;
+
+static const double* hist_table(int b, cudaStream_t s, std::string& err) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_u_mu);
+  auto key = std::make_pair(dev, b);
+  auto it = g_u_tables.find(key);
+  if (it != g_u_tables.end()) return it->second;
+  double* U = nullptr;
+  cudaError_t e = cudaMalloc(&U, sizeof(double) * (size_t)b * (b + 1) / 2);
+  if (e != cudaSuccess) { err = std::string("cudaMalloc U: ") + cudaGetErrorString(e); return nullptr; }
+  k_hist_table<<<b, 128, 0, s>>>(b, U);
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) { err = std::string("U table: ") + cudaGetErrorString(e); cudaFree(U); return nullptr; }
+  g_u_tables[key] = U;
+  return U;
+}
+
+int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b, int aux,
+                    uint8_t* packed, double* xmin, double* xmax, int32_t* info0, int32_t* info1,
+                    double* norm, int32_t* status, cudaStream_t s, std::string& err) {
+  if (b > 4096) { err = "hist-brute with b > 4096 is not supported by the B200 path"; return EQ4_EUNSUPPORTED; }
+  const double* U = hist_table(b, s, err);
+  if (!U) return EQ4_ECUDA;
+  HistParams p;
+  p.x = x; p.rows = rows; p.ld = ld; p.d = (int)dim; p.b = b; p.aux = aux;
+  p.stride = (int)eq4_packed_row_stride(dim, aux);
+  p.half = (int)((dim + 1) / 2);
+  p.packed = packed; p.lo_out = xmin; p.hi_out = xmax; p.norm_out = norm;
+  p.info0 = info0; p.info1 = info1; p.status = status; p.U = U;
+  const HistSlice S{b, (int)dim};
+  const size_t smem = S.bytes();
+  if (smem > 227 * 1024) { err = "hist-brute: row does not fit in shared memory"; return EQ4_EUNSUPPORTED; }
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) { err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+  }
+  int occ = 0, dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hist, 32, smem);
+  if (occ < 1) occ = 1;
+  const int64_t grid = std::min<int64_t>(rows, (int64_t)sms * occ);
+  k_hist<<<(unsigned)grid, 32, smem, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { err = std::string("k_hist launch: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+  return EQ4_OK;
+}

@@ -1,0 +1,12 @@
+// eq4_internal.h -- launchers shared between the translation units of libeq4.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+// HIST-BRUTE fused search + quantize + pack (eq4_hist.cu).  Returns an EQ4_* code;
+// on failure err holds the message.
+int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b, int aux,
+                    uint8_t* packed, double* xmin, double* xmax, int32_t* info0, int32_t* info1,
+                    double* norm, int32_t* status, cudaStream_t s, std::string& err);

@@ -190,3 +190,60 @@ def test_div15_matches_ieee_divide(eq):
     L = eq.load()
     assert L.eq4_selftest(0, 1 << 28, 11) == 0
     assert L.eq4_selftest(1, 1 << 28, 12) == 0
+
+
+HIST_TIE_REL = 1e-12   # reference norms this close are a tie decided by BLAS rounding
+
+
+def _hist_compare(x, b, got_s, got_n, want_s, want_n):
+    """Rows whose window differs from the reference must be norm ties; returns their indices."""
+    ties = []
+    for i in np.nonzero((got_s != want_s) | (got_n != want_n))[0]:
+        a = oracle.hist_window_norm(x[i], b, int(want_s[i]), int(want_n[i]))
+        g = oracle.hist_window_norm(x[i], b, int(got_s[i]), int(got_n[i]))
+        assert abs(a - g) <= HIST_TIE_REL * max(abs(a), abs(g)), (i, (want_s[i], want_n[i]), (got_s[i], got_n[i]), a, g)
+        ties.append(int(i))
+    return ties
+
+
+def test_hist_brute_golden(eq):
+    f = np.load(os.path.join(G, "hist.npz"))
+    meta = json.loads(str(f["meta"]))
+    nties = 0
+    for k, m in enumerate(meta):
+        x = f[f"x_{k}"]
+        b = m["b"]
+        p, rr = eq.quantize_pack_table4(_dev(x), "hist-brute", "fp16", b, with_rows=True)
+        st, nn = rr.info0.cpu().numpy(), rr.info1.cpu().numpy()
+        ties = _hist_compare(x, b, st, nn, f[f"start_{k}"], f[f"n_{k}"])
+        nties += len(ties)
+        keep = np.setdiff1d(np.arange(x.shape[0]), ties)
+        assert np.array_equal(rr.xmin.cpu().numpy()[keep], f[f"lo_{k}"][keep]), m["name"]
+        assert np.array_equal(rr.xmax.cpu().numpy()[keep], f[f"hi_{k}"][keep]), m["name"]
+        np.testing.assert_allclose(rr.norm.cpu().numpy(), f[f"norm_{k}"], rtol=1e-9, atol=1e-300)
+        stride = eq.packed_row_stride(x.shape[1], "fp16")
+        assert np.array_equal(p.buffer.reshape(-1, stride)[keep], f[f"packed_{k}"].reshape(-1, stride)[keep])
+    print(f"hist-brute golden: {nties} norm-tie exception(s)")
+    assert nties <= 2
+
+
+def test_hist_brute_vs_oracle_config4_sample(eq):
+    x = rng.sample_table("gaussian", 0.0, 1.0, 4040, 1024, 64)
+    want = oracle.quantize_pack_table(x, "hist-brute", 200, aux="fp16")
+    p, rr = eq.quantize_pack_table4(_dev(x), "hist-brute", "fp16", 200, with_rows=True)
+    ties = _hist_compare(x, 200, rr.info0.cpu().numpy(), rr.info1.cpu().numpy(), want.info0, want.info1)
+    keep = np.setdiff1d(np.arange(x.shape[0]), ties)
+    assert np.array_equal(p.buffer.reshape(-1, 36)[keep], want.packed.reshape(-1, 36)[keep])
+    np.testing.assert_allclose(rr.norm.cpu().numpy(), want.norm, rtol=1e-9)
+    assert len(ties) <= 1
+
+
+def test_hist_brute_api_counters(eq):
+    x = rng.gaussian_row(5, 64)
+    c = eq.WorkCounters()
+    w = eq.hist_brute_search(x, 200, counters=c)
+    h = oracle.hist_brute_search(x, 200)
+    assert (w.start_bin, w.nbins_selected) == (h.start_bin, h.nbins_selected)
+    assert w.clip_range == eq.ClipRange(h.xmin, h.xmax)
+    assert (c.candidate_evals, c.bin_visits) == (h.candidate_evals, h.bin_visits)
+    assert eq.clip_range_hist_brute([4.0, 4.0, 4.0], 16) == eq.ClipRange(4.0, 4.0)
