@@ -990,6 +990,157 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
 }
 
 // ---------------------------------------------------------------------------
+// ASYM vector kernel: warp-autonomous (per-warp staging, no block barriers),
+// the next row block's loads in flight while the current one is coded, and
+// the per-element code arithmetic on packed fp32x2.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ f2_t sub2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t add2_rm(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+template <int LPR, int E>
+struct SliceA {
+  static constexpr int RPW = 32 / LPR;
+  __host__ __device__ static size_t bytes(int) { return 0; }
+};
+
+template <int LPR, int E>
+__device__ __forceinline__ void asym_load(const float* rowp, bool ok, int q, float4 (&v)[E / 4]) {
+  const float4* src = reinterpret_cast<const float4*>(rowp);
+#pragma unroll
+  for (int c = 0; c < E / 4; ++c)
+    if (ok) v[c] = __ldcs(src + q + LPR * c);
+}
+
+// Code + pack one row slice (E elements of lane q) straight to the packed row
+// in global memory (2-byte stores; L2 merges a row's partial sectors).
+template <int LPR, int E>
+__device__ __forceinline__ void asym_row(const Params& p, const float4 (&cur)[E / 4], int64_t row,
+                                         int q) {
+  const bool rvalid = row < p.rows;
+  // ---- min / max / finiteness (clipping.py:58-61, table.py:28-29) ----
+  float mn = INFINITY, mx = -INFINITY, sm = 0.f;
+#pragma unroll
+  for (int c = 0; c < E / 4; ++c) {
+    mn = fminf(mn, fminf(fminf(cur[c].x, cur[c].y), fminf(cur[c].z, cur[c].w)));
+    mx = fmaxf(mx, fmaxf(fmaxf(cur[c].x, cur[c].y), fmaxf(cur[c].z, cur[c].w)));
+    sm = __fadd_rn(sm, __fadd_rn(__fadd_rn(cur[c].x, cur[c].y), __fadd_rn(cur[c].z, cur[c].w)));
+  }
+  mn = group_min<LPR>(mn);
+  mx = group_max<LPR>(mx);
+  sm = group_sum<LPR>(sm);
+  bool bad = false;
+  if (__any_sync(FULL, !isfinite(sm) && rvalid)) {
+    bool lb = false;
+#pragma unroll
+    for (int c = 0; c < E / 4; ++c)
+      lb |= !isfinite(cur[c].x) || !isfinite(cur[c].y) || !isfinite(cur[c].z) || !isfinite(cur[c].w);
+    bad = group_any<LPR>(lb) && rvalid;
+    if (bad && q == 0 && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
+  }
+  // ---- codes: u = (x - min) * 15/(max - min) + 1/2, code = floor(u) ----
+  const float w32 = __fadd_rn(mx, -mn);
+  const bool degenerate = !(mn != mx);                     // uniform.py:74-76: all codes 0
+  const bool fast = !bad && w32 > 1e-30f && w32 < 1e30f;
+  const float inv = fast ? __fdividef(15.f, w32) : 0.f;    // 0 -> u = 1/2 -> code 0
+  const f2_t nmn2 = pk2(-mn, -mn), inv2 = pk2(inv, inv), h2 = pk2(0.5f, 0.5f);
+  const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC);
+  float gmin = 0.5f, gmax = 0.5f;
+  uint8_t* orow = p.packed + (rvalid ? row : 0) * (int64_t)p.stride;
+  uint32_t w16[E / 4];
+#pragma unroll
+  for (int c = 0; c < E / 4; ++c) {
+    const f2_t xa = pk2(cur[c].x, cur[c].y), xb = pk2(cur[c].z, cur[c].w);
+    const f2_t ua = fma2(add2(xa, nmn2), inv2, h2), ub = fma2(add2(xb, nmn2), inv2, h2);
+    const f2_t ma = add2_rm(ua, mg2), mb = add2_rm(ub, mg2);            // 2^23 + floor(u)
+    const f2_t ga = sub2(ua, add2(ma, nmg2)), gb = sub2(ub, add2(mb, nmg2));   // frac(u), exact
+    float g0, g1, g2, g3;
+    upk2(ga, g0, g1);
+    upk2(gb, g2, g3);
+    gmin = fminf(gmin, fminf(fminf(g0, g1), fminf(g2, g3)));
+    gmax = fmaxf(gmax, fmaxf(fmaxf(g0, g1), fmaxf(g2, g3)));
+    float m0, m1, m2, m3;
+    upk2(ma, m0, m1);
+    upk2(mb, m2, m3);
+    // low nibbles of the four 2^23 + code bit patterns -> one 16-bit word
+    w16[c] = __byte_perm(__float_as_uint(m0) | (__float_as_uint(m1) << 4),
+                         __float_as_uint(m2) | (__float_as_uint(m3) << 4), 0x40) & 0xFFFFu;
+  }
+  const bool need = rvalid && !bad && !degenerate && (!fast || gmin < NEAR || gmax > 1.f - NEAR);
+  if (__any_sync(FULL, need)) {   // rare: float64 codec (uniform.py:77-79) for flagged elements
+    if (need) {
+      const CodeParams cp = make_code_params((double)mn, (double)mx);
+      for (int i = 0; i < E; ++i) {
+        const float4 v4 = cur[i >> 2];
+        const float x = (i & 3) == 0 ? v4.x : (i & 3) == 1 ? v4.y : (i & 3) == 2 ? v4.z : v4.w;
+        const float u = __fmaf_rn(__fadd_rn(x, -mn), inv, 0.5f);
+        const float g = __fadd_rn(u, -__fadd_rn(__fadd_rd(u, MAGIC), -MAGIC));
+        if (fast && g >= NEAR && g <= 1.f - NEAR) continue;
+        const uint32_t cc = code_exact(x, cp);
+        const int sh = 4 * (i & 3);
+        w16[i >> 2] = (w16[i >> 2] & ~(0xFu << sh)) | (cc << sh);
+      }
+    }
+  }
+  if (rvalid) {
+#pragma unroll
+    for (int c = 0; c < E / 4; ++c)
+      *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = (uint16_t)(bad ? 0u : w16[c]);
+    if (q == 0) {
+      const double sc = (!bad && !degenerate) ? div15(__dsub_rn((double)mx, (double)mn)) : 0.0;
+      uint8_t* a = orow + p.half;
+      if (p.aux == EQ4_AUX_FP16) {
+        *reinterpret_cast<uint16_t*>(a) = (uint16_t)aux_bits_f16(sc);
+        *reinterpret_cast<uint16_t*>(a + 2) = (uint16_t)aux_bits_f16((double)mn);
+      } else {
+        const uint32_t s32 = aux_bits_f32(sc), b32 = aux_bits_f32((double)mn);
+        *reinterpret_cast<uint16_t*>(a) = (uint16_t)s32;
+        *reinterpret_cast<uint16_t*>(a + 2) = (uint16_t)(s32 >> 16);
+        *reinterpret_cast<uint16_t*>(a + 4) = (uint16_t)b32;
+        *reinterpret_cast<uint16_t*>(a + 6) = (uint16_t)(b32 >> 16);
+      }
+      if (p.lo_out) { p.lo_out[row] = (double)mn; p.hi_out[row] = (double)mx; }
+      if (p.info0) p.info0[row] = 0;
+      if (p.info1) p.info1[row] = 0;
+    }
+  }
+}
+
+// ASYM vector kernel: warps are independent; each warp keeps the next row
+// block's loads in flight (double buffer A/B) while it codes the current one.
+template <int LPR, int E>
+__global__ void __launch_bounds__(NTHREADS, 3) k_asym_vec(const Params p) {
+  constexpr int RPW = 32 / LPR;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = lane / LPR, q = lane % LPR;
+  const int64_t nblocks = (p.rows + RPW - 1) / RPW;
+  const int64_t wstride = (int64_t)gridDim.x * NWARPS;
+  int64_t blk = (int64_t)blockIdx.x * NWARPS + warp;
+  const int64_t rstep = wstride * RPW * p.ld;               // floats between a warp's blocks
+  const float* xp = p.x + (blk * RPW + gw) * p.ld;
+  float4 a[E / 4], b[E / 4];
+  if (blk < nblocks) asym_load<LPR, E>(xp, blk * RPW + gw < p.rows, q, a);
+  while (blk < nblocks) {
+    if (blk + wstride < nblocks) asym_load<LPR, E>(xp + rstep, (blk + wstride) * RPW + gw < p.rows, q, b);
+    asym_row<LPR, E>(p, a, blk * RPW + gw, q);
+    blk += wstride;
+    xp += rstep;
+    if (blk >= nblocks) break;
+    if (blk + wstride < nblocks) asym_load<LPR, E>(xp + rstep, (blk + wstride) * RPW + gw < p.rows, q, a);
+    asym_row<LPR, E>(p, b, blk * RPW + gw, q);
+    blk += wstride;
+    xp += rstep;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // pack / unpack / quant_mse utility kernels
 // ---------------------------------------------------------------------------
 __global__ void k_pack(const uint8_t* codes, int64_t rows, int d, int aux, const uint8_t* sc,
@@ -1126,6 +1277,11 @@ static int launch_persistent(Kern kern, size_t smem, int64_t ntiles, const Param
 template <int METHOD, int LPR, int E, bool VEC>
 static int launch_rq(const Params& p, cudaStream_t s) {
   if constexpr (METHOD == M_ASYM) {
+    if constexpr (VEC && E <= 16) {
+      using S = SliceA<LPR, E>;
+      return launch_persistent(k_asym_vec<LPR, E>, 0,
+                               (p.rows + S::RPW * NWARPS - 1) / (S::RPW * NWARPS), p, s, "k_asym_vec");
+    }
     using L = LayoutA<LPR, E, VEC>;
     return launch_persistent(k_asym<LPR, E, VEC>, L::total(p.stride), (p.rows + L::RPB - 1) / L::RPB,
                              p, s, "k_asym");
