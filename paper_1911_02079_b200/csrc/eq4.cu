@@ -499,6 +499,16 @@ __device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
 }
+__device__ __forceinline__ f2_t sub2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t add2_rm(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ f2_t fma2_rm(f2_t a, f2_t b, f2_t c) {
   f2_t r;
   asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
@@ -607,6 +617,84 @@ __device__ __forceinline__ void eval_pair_x2(const float4* ys4, float BL, float 
   aR = __fadd_rn(r0, r1);
 }
 
+// Packed pair evaluation with R derived from L (valid for W > 15): the R grid
+// is the L grid shifted by 15 < W, so zR = zL + 15 moves every code by at
+// most one:  cR = min(cL + [eL + 15 >= W/2], 15)  (below-window elements have
+// eL + 15 < W/2, top-code elements keep 15), hence
+//   eR = (eL + 15) - W * min([eL + 15 >= W/2], [cL < 15]),
+// all exact in fp32.  R costs 3 FMA-pipe + 3 ALU instructions per element
+// pair instead of 7 FMA-pipe ones.
+__device__ __forceinline__ float set_ge(float a, float b) {
+  float r;
+  asm("set.ge.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float set_lt(float a, float b) {
+  float r;
+  asm("set.lt.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+template <int E>
+__device__ __forceinline__ void eval_pair_x2_shift(const float4* ys4, float BL, float nW, float kW,
+                                                   float h, float& aL, float& aR) {
+  const int lane = threadIdx.x & 31;
+  const f2_t nBL2 = pk2(-BL, -BL), c15 = pk2(15.f, 15.f), al2 = pk2(ALPHA, ALPHA);
+  const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
+  const float hW = -0.5f * nW, top = MAGIC + 15.f;   // ulp(2^23) = 1: mL < 2^23 + 15 <=> cL < 15
+  f2_t sL = pk2(0.f, 0.f), sR = pk2(0.f, 0.f);
+#pragma unroll kGUnroll
+  for (int c = 0; c < E / 4; ++c) {
+    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32 + lane);
+#pragma unroll
+    for (int hlf = 0; hlf < 2; ++hlf) {
+      const f2_t zL = add2(hlf ? yy.y : yy.x, nBL2);
+      float a0, a1;
+      upk2(zL, a0, a1);
+      const f2_t mL = fma2_rm(pk2(sat_fma(a0, kW, h), sat_fma(a1, kW, h)), al2, mg2);   // 2^23 + cL
+      const f2_t eL = fma2(add2(mL, nmg2), nW2, zL);                                    // exact
+      const f2_t tR = add2(eL, c15);                                                    // zR - cL W
+      float t0, t1, m0, m1;
+      upk2(tR, t0, t1);
+      upk2(mL, m0, m1);
+      const f2_t k2 = pk2(fminf(set_ge(t0, hW), set_lt(m0, top)), fminf(set_ge(t1, hW), set_lt(m1, top)));
+      const f2_t eR = fma2(k2, nW2, tR);                                                // exact
+      sL = fma2(eL, eL, sL);
+      sR = fma2(eR, eR, sR);
+    }
+  }
+  float l0, l1, r0, r1;
+  upk2(sL, l0, l1);
+  upk2(sR, r0, r1);
+  aL = __fadd_rn(l0, l1);
+  aR = __fadd_rn(r0, r1);
+}
+
+// Packed single-candidate loss (the full range, clipping.py:174).
+template <int E>
+__device__ __forceinline__ float eval_one_x2(const float4* ys4, float B, float nW, float kW, float h) {
+  const int lane = threadIdx.x & 31;
+  const f2_t nB2 = pk2(-B, -B), al2 = pk2(ALPHA, ALPHA);
+  const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
+  f2_t acc = pk2(0.f, 0.f);
+#pragma unroll kGUnroll
+  for (int c = 0; c < E / 4; ++c) {
+    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32 + lane);
+#pragma unroll
+    for (int hlf = 0; hlf < 2; ++hlf) {
+      const f2_t z = add2(hlf ? yy.y : yy.x, nB2);
+      float a0, a1;
+      upk2(z, a0, a1);
+      const f2_t t = pk2(sat_fma(a0, kW, h), sat_fma(a1, kW, h));
+      const f2_t e = fma2(add2(fma2_rm(t, al2, mg2), nmg2), nW2, z);
+      acc = fma2(e, e, acc);
+    }
+  }
+  float l0, l1;
+  upk2(acc, l0, l1);
+  return __fadd_rn(l0, l1);
+}
+
 // Y coordinates on the exact fp32 grid of quantum qY (see file header).
 template <int LPR, int E, bool VEC>
 __device__ __forceinline__ void make_Y(const Params& p, const float* xr, int q, int nv, double x0,
@@ -683,25 +771,36 @@ __device__ __forceinline__ void emit_greedy(const Params& p, const float4* ys4, 
   unsigned long long need = 0ull;
   // streamed chunk by chunk (no per-slot arrays): codes go straight to the
   // staged row; flagged slots are rewritten below
+  const f2_t nB2 = pk2(-B, -B), al2 = pk2(ALPHA, ALPHA);
+  const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC);
 #pragma unroll
   for (int c = 0; c < E / 4; ++c) {
-    const float4 y4 = ys4[c * 32 + lane];
-    const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
+    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32 + lane);
     uint32_t w = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = 4 * c + k;
-      const float z = __fadd_rn(yv[k], -B);
-      const float sv = sat_fma(z, kW, h);
-      const float m = __fmaf_rd(sv, ALPHA, MAGIC);
-      const float f = __fmaf_rn(sv, ALPHA, -__fadd_rn(m, -MAGIC));   // frac of alpha*s, exact
-      const bool nr_ = sv > 0.f && sv < 1.f && (f < nb || f > 1.f - nb);
-      need |= (unsigned long long)(nr_ && (VEC || i < nv)) << i;
-      const uint32_t code = ok ? (__float_as_uint(m) & 0xFu) : 0u;
+    for (int hlf = 0; hlf < 2; ++hlf) {
+      const f2_t z = add2(hlf ? yy.y : yy.x, nB2);
+      float z0, z1;
+      upk2(z, z0, z1);
+      const float s0 = sat_fma(z0, kW, h), s1 = sat_fma(z1, kW, h);
+      const f2_t sv = pk2(s0, s1);
+      const f2_t m = fma2_rm(sv, al2, mg2);
+      const f2_t fr = sub2(fma2(sv, al2, pk2(0.f, 0.f)), add2(m, nmg2));   // frac of alpha*s
+      float m0, m1, f0, f1;
+      upk2(m, m0, m1);
+      upk2(fr, f0, f1);
+      const int i0 = 4 * c + 2 * hlf;
+      const bool n0 = s0 > 0.f && s0 < 1.f && (f0 < nb || f0 > 1.f - nb);
+      const bool n1 = s1 > 0.f && s1 < 1.f && (f1 < nb || f1 > 1.f - nb);
+      need |= ((unsigned long long)(n0 && (VEC || i0 < nv)) << i0) |
+              ((unsigned long long)(n1 && (VEC || i0 + 1 < nv)) << (i0 + 1));
+      const uint32_t c0 = ok ? (__float_as_uint(m0) & 0xFu) : 0u;
+      const uint32_t c1 = ok ? (__float_as_uint(m1) & 0xFu) : 0u;
       if (VEC) {
-        w |= code << (4 * k);
-      } else if (rvalid && i < nv) {
-        crow[q + LPR * i] = (uint8_t)code;
+        w |= (c0 | (c1 << 4)) << (8 * hlf);
+      } else if (rvalid) {
+        if (i0 < nv) crow[q + LPR * i0] = (uint8_t)c0;
+        if (i0 + 1 < nv) crow[q + LPR * (i0 + 1)] = (uint8_t)c1;
       }
     }
     if (VEC && rvalid) *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = (uint16_t)w;
@@ -862,7 +961,12 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
     float Lbest;
     {
       const float Wf = (float)p.b;                                                   // :174
-      Lbest = group_sum<LPR>(eval_one<E, !VEC>(ys4, nv, 0.f, -Wf, rcp_approx(Wf * ALPHA), hh));
+      float a0;
+      if constexpr (VEC)
+        a0 = eval_one_x2<E>(ys4, 0.f, -Wf, rcp_approx(Wf * ALPHA), hh);
+      else
+        a0 = eval_one<E, true>(ys4, nv, 0.f, -Wf, rcp_approx(Wf * ALPHA), hh);
+      Lbest = group_sum<LPR>(a0);
     }
     int nl = 0, nr = 0, bi = 0, bj = 0, iters = 0;
     float BLf = 15.f;                       // base of the L candidate, 15 * (nl + 1)
@@ -879,10 +983,14 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       for (; it < itA; ++it) {
         const float Wf = (float)(p.b - it - 1);
         float aL, aR;
-        if constexpr (VEC)
-          eval_pair_x2<E>(ys4, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
-        else
+        if constexpr (VEC) {
+          if (Wf >= 17.f)   // codes move by at most one under the 15-shift
+            eval_pair_x2_shift<E>(ys4, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+          else
+            eval_pair_x2<E>(ys4, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+        } else {
           eval_pair<E, true>(ys4, nv, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+        }
         group_sum_pair<LPR>(aL, aR, SL, SR);
         goL = SL < SR;                                                   // clipping.py:185
         cand = goL ? SL : SR;
@@ -929,7 +1037,10 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       if (W >= 1) {
         const float Wf = (float)W;
         float aL, aR;
-        eval_pair<E, !VEC>(ys4, nv, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+        if constexpr (VEC)
+          eval_pair_x2<E>(ys4, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+        else
+          eval_pair<E, true>(ys4, nv, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
         group_sum_pair<LPR>(aL, aR, SL, SR);
         const bool goL = SL < SR;
         const float cand = goL ? SL : SR;
@@ -994,16 +1105,6 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
 // the next row block's loads in flight while the current one is coded, and
 // the per-element code arithmetic on packed fp32x2.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ f2_t sub2(f2_t a, f2_t b) {
-  f2_t r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f2_t add2_rm(f2_t a, f2_t b) {
-  f2_t r;
-  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
 
 template <int LPR, int E>
 struct SliceA {
