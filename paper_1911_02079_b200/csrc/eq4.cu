@@ -68,7 +68,7 @@ enum { M_ASYM = 0, M_GREEDY = 1 };
 #define G_MINB32 4
 #endif
 #ifndef G_MINB64
-#define G_MINB64 1
+#define G_MINB64 4
 #endif
 
 struct Params {
@@ -448,7 +448,7 @@ struct WarpSliceG {
   static constexpr int RPW = 32 / LPR;
   static constexpr int D = LPR * E;
   static constexpr int E2CAP = D < 512 ? D : 512;
-  __host__ __device__ static size_t ys_off() { return (size_t)RPW * D * 4; }          // E/4 x 32 float4
+  __host__ __device__ static size_t ys_off() { return 0; }                            // E/4 x 32 float4
   __host__ __device__ static size_t rs_off() { return ys_off() + (size_t)E * 32 * 4; }
   __host__ __device__ static size_t e2_off() { return rs_off() + RPW * sizeof(RowShared); }
   __host__ __device__ static size_t leaf_off() { return e2_off() + (size_t)E2CAP * 8; }
@@ -843,8 +843,8 @@ enum : unsigned { F_ACTIVE = 1, F_EXACT_ONLY = 2, F_BEST_EX = 4, F_ERR = 8 };
 // at a time by the whole warp with the bit-exact float64 restatement.
 template <int LPR, int E, bool VEC>
 __device__ __forceinline__ void exact_block(const Params& p, bool need_ex, int q, int gw, int W,
-                                            float SL, float SR, RowShared* rs, const float* xs,
-                                            int D, int d, double* e2, double* leaf_sum,
+                                            float SL, float SR, RowShared* rs, const float* xblk,
+                                            int64_t ld, int d, double* e2, double* leaf_sum,
                                             int* leaf_st, int* leaf_ln, int& nl, int& nr, int& bi,
                                             int& bj, int& iters, unsigned& flags, float& Lbest,
                                             float& BLf) {
@@ -856,7 +856,7 @@ __device__ __forceinline__ void exact_block(const Params& p, bool need_ex, int q
     const ExactOut o = exact_decide(
         &rs[lg], (double)__shfl_sync(FULL, nl, leader), (double)__shfl_sync(FULL, nr, leader),
         __shfl_sync(FULL, bi, leader), __shfl_sync(FULL, bj, leader),
-        (__shfl_sync(FULL, flags, leader) & F_BEST_EX) != 0, xs + lg * D, d, e2, leaf_sum, leaf_st,
+        (__shfl_sync(FULL, flags, leader) & F_BEST_EX) != 0, xblk + lg * ld, d, e2, leaf_sum, leaf_st,
         leaf_ln);
     if (lg == gw) {
       if (o.flags & 1) {
@@ -891,7 +891,6 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = lane / LPR, q = lane % LPR;
   unsigned char* ws = smem + warp * S::bytes(p.stride);
-  float* xs = reinterpret_cast<float*>(ws);
   float4* ys4 = reinterpret_cast<float4*>(ws + S::ys_off());
   RowShared* rs = reinterpret_cast<RowShared*>(ws + S::rs_off());
   double* e2 = reinterpret_cast<double*>(ws + S::e2_off());
@@ -910,40 +909,75 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
     const int64_t row0 = blk * RPW, row = row0 + gw;
     const bool rvalid = row < p.rows;
     RowShared& R = rs[gw];
-    float* xr = xs + gw * D;
+    // the raw rows stay in global memory (L1/L2-resident while the block is
+    // searched): only the rare exact decisions and code fix-ups read them
+    const float* xblk = p.x + row0 * p.ld;
+    const float* xr = xblk + (rvalid ? gw : 0) * p.ld;
 
     float mn, mx;
     bool bad;
     {
-      float v[E];
-      load_row<LPR, E, VEC>(p, row, rvalid, q, nv, v);
-      if (VEC) {
-#pragma unroll
-        for (int c = 0; c < E / 4; ++c)
-          *reinterpret_cast<float4*>(xr + 4 * (q + LPR * c)) =
-              make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < E; ++i)
-          if (i < nv) xr[q + LPR * i] = v[i];
-      }
-      row_minmax<LPR, E, VEC>(p, v, nv, rvalid, q, mn, mx, bad);
-      const double x0 = (double)mn, x1 = (double)mx;
-      const double Dw = __dsub_rn(x1, x0);
-      const double step = __ddiv_rn(Dw, (double)p.b);                               // :172
-      const double kY = (x0 != x1) ? __ddiv_rn(15.0, step) : 0.0;
       // Y on the exact fp32 grid of quantum qY: Y + C rounds to a multiple of qY
       // (C = 1.5 * 2^52 * qY, same ties-to-even result as rint(Y / qY) * qY)
       const double cY = 6755399441055744.0 * p.qY;
+      double x0, x1, step, kY;
+      if constexpr (VEC) {
+        // two streaming passes over the row slice (the second hits L1/L2), so
+        // no E-element register array is live across the float64 setup
+        const float4* src = reinterpret_cast<const float4*>(xr) + q;
+        float lmn = INFINITY, lmx = -INFINITY, sm = 0.f;
 #pragma unroll
-      for (int c = 0; c < E / 4; ++c) {
-        float y[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double Y = __dmul_rn(__dsub_rn((double)v[4 * c + k], x0), kY);
-          y[k] = (float)__dsub_rn(__dadd_rn(Y, cY), cY);
+        for (int c = 0; c < E / 4; ++c) {
+          const float4 t = __ldg(src + LPR * c);
+          lmn = fminf(lmn, fminf(fminf(t.x, t.y), fminf(t.z, t.w)));
+          lmx = fmaxf(lmx, fmaxf(fmaxf(t.x, t.y), fmaxf(t.z, t.w)));
+          sm = __fadd_rn(sm, __fadd_rn(__fadd_rn(t.x, t.y), __fadd_rn(t.z, t.w)));
         }
-        ys4[c * 32 + lane] = make_float4(y[0], y[1], y[2], y[3]);
+        mn = group_min<LPR>(lmn);
+        mx = group_max<LPR>(lmx);
+        sm = group_sum<LPR>(sm);
+        bad = false;
+        if (__any_sync(FULL, !isfinite(sm) && rvalid)) {   // NaN/Inf (or a false alarm on overflow)
+          bool lb = false;
+          for (int c = 0; c < E / 4; ++c) {
+            const float4 t = __ldg(src + LPR * c);
+            lb |= !isfinite(t.x) || !isfinite(t.y) || !isfinite(t.z) || !isfinite(t.w);
+          }
+          bad = group_any<LPR>(lb) && rvalid;
+          if (bad && q == 0 && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
+        }
+        x0 = (double)mn; x1 = (double)mx;
+        step = __ddiv_rn(__dsub_rn(x1, x0), (double)p.b);                           // :172
+        kY = (x0 != x1) ? __ddiv_rn(15.0, step) : 0.0;
+#pragma unroll 4
+        for (int c = 0; c < E / 4; ++c) {
+          const float4 t = __ldg(src + LPR * c);
+          const float tv[4] = {t.x, t.y, t.z, t.w};
+          float y[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double Y = __dmul_rn(__dsub_rn((double)tv[k], x0), kY);
+            y[k] = (float)__dsub_rn(__dadd_rn(Y, cY), cY);
+          }
+          ys4[c * 32 + lane] = make_float4(y[0], y[1], y[2], y[3]);
+        }
+      } else {
+        float v[E];
+        load_row<LPR, E, VEC>(p, row, rvalid, q, nv, v);
+        row_minmax<LPR, E, VEC>(p, v, nv, rvalid, q, mn, mx, bad);
+        x0 = (double)mn; x1 = (double)mx;
+        step = __ddiv_rn(__dsub_rn(x1, x0), (double)p.b);                           // :172
+        kY = (x0 != x1) ? __ddiv_rn(15.0, step) : 0.0;
+#pragma unroll
+        for (int c = 0; c < E / 4; ++c) {
+          float y[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double Y = __dmul_rn(__dsub_rn((double)v[4 * c + k], x0), kY);
+            y[k] = (float)__dsub_rn(__dadd_rn(Y, cY), cY);
+          }
+          ys4[c * 32 + lane] = make_float4(y[0], y[1], y[2], y[3]);
+        }
       }
       if (q == 0) {
         R.x0 = x0; R.x1 = x1; R.step = step;
@@ -1018,7 +1052,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         if (cand < Lbest) { Lbest = cand; bi = nl; bj = nr; flags &= ~F_BEST_EX; }
         ++iters;
       }
-      exact_block<LPR, E, VEC>(p, need_ex, q, gw, p.b - it - 1, SL, SR, rs, xs, D, d, e2, leaf_sum,
+      exact_block<LPR, E, VEC>(p, need_ex, q, gw, p.b - it - 1, SL, SR, rs, xblk, p.ld, d, e2, leaf_sum,
                                leaf_st, leaf_ln, nl, nr, bi, bj, iters, flags, Lbest, BLf);
       ++it;
     }
@@ -1058,7 +1092,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         }
       }
       if (__any_sync(FULL, need_ex))
-        exact_block<LPR, E, VEC>(p, need_ex, q, gw, W, SL, SR, rs, xs, D, d, e2, leaf_sum, leaf_st,
+        exact_block<LPR, E, VEC>(p, need_ex, q, gw, W, SL, SR, rs, xblk, p.ld, d, e2, leaf_sum, leaf_st,
                                  leaf_ln, nl, nr, bi, bj, iters, flags, Lbest, BLf);
     }
 
@@ -1429,15 +1463,30 @@ static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
       case 16: return launch_rq<METHOD, 1, 16, true>(p, s);
       case 32: return launch_rq<METHOD, 1, 32, true>(p, s);
       case 64: {
-        const char* v = getenv("EQ4_G64");
-        if (v && v[0] == '1') return launch_rq<METHOD, 1, 64, true>(p, s);
-        if (v && v[0] == '4') return launch_rq<METHOD, 4, 16, true>(p, s);
-        return launch_rq<METHOD, 2, 32, true>(p, s);
+        const char* v = getenv("EQ4_G64");   // layout experiments
+        if (v && v[0] == '2') return launch_rq<METHOD, 2, 32, true>(p, s);
+        return launch_rq<METHOD, 1, 64, true>(p, s);
       }
-      case 128: return launch_rq<METHOD, 4, 32, true>(p, s);
-      case 256: return launch_rq<METHOD, 8, 32, true>(p, s);
-      case 512: return launch_rq<METHOD, 16, 32, true>(p, s);
-      case 1024: return launch_rq<METHOD, 32, 32, true>(p, s);
+      case 128: {
+        const char* v = getenv("EQ4_G128");
+        if (v && v[0] == '4') return launch_rq<METHOD, 4, 32, true>(p, s);
+        return launch_rq<METHOD, 2, 64, true>(p, s);
+      }
+      case 256: {
+        const char* v = getenv("EQ4_GW");
+        if (v && v[0] == '1') return launch_rq<METHOD, 8, 32, true>(p, s);
+        return launch_rq<METHOD, 4, 64, true>(p, s);
+      }
+      case 512: {
+        const char* v = getenv("EQ4_GW");
+        if (v && v[0] == '1') return launch_rq<METHOD, 16, 32, true>(p, s);
+        return launch_rq<METHOD, 8, 64, true>(p, s);
+      }
+      case 1024: {
+        const char* v = getenv("EQ4_GW");
+        if (v && v[0] == '1') return launch_rq<METHOD, 32, 32, true>(p, s);
+        return launch_rq<METHOD, 16, 64, true>(p, s);
+      }
       case 2048: return launch_rq<METHOD, 32, 64, true>(p, s);
       default: break;
     }
