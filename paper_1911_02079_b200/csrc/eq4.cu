@@ -621,17 +621,17 @@ __device__ __forceinline__ void eval_pair_x2(const float4* ys4, float BL, float 
 // is the L grid shifted by 15 < W, so zR = zL + 15 moves every code by at
 // most one:  cR = min(cL + [eL + 15 >= W/2], 15)  (below-window elements have
 // eL + 15 < W/2, top-code elements keep 15), hence
-//   eR = (eL + 15) - W * min([eL + 15 >= W/2], [cL < 15]),
-// all exact in fp32.  R costs 3 FMA-pipe + 3 ALU instructions per element
-// pair instead of 7 FMA-pipe ones.
-__device__ __forceinline__ float set_ge(float a, float b) {
+//   eR = eL + (15 - W [eL >= W/2 - 15 and cL < 15]),
+// all exact in fp32 (eL and the constants are multiples of qY well below
+// 2^24 qY).  R costs 2 FMA-pipe instructions per element pair (add, square-
+// accumulate) + 3 ALU ones per element, instead of 7 FMA-pipe ones per pair.
+// (e >= thr and m < top) ? a : b -- one FSETP, one FSETP with the first
+// predicate folded into its boolean combine, one FSEL.
+__device__ __forceinline__ float sel_ge_lt(float e, float thr, float m, float top, float a, float b) {
   float r;
-  asm("set.ge.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float set_lt(float a, float b) {
-  float r;
-  asm("set.lt.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  asm("{\n\t.reg .pred p, q;\n\tsetp.lt.f32 p, %2, %3;\n\tsetp.ge.and.f32 q, %1, %4, p;\n\t"
+      "selp.f32 %0, %5, %6, q;\n\t}"
+      : "=f"(r) : "f"(e), "f"(m), "f"(top), "f"(thr), "f"(a), "f"(b));
   return r;
 }
 
@@ -639,9 +639,10 @@ template <int E>
 __device__ __forceinline__ void eval_pair_x2_shift(const float4* ys4, float BL, float nW, float kW,
                                                    float h, float& aL, float& aR) {
   const int lane = threadIdx.x & 31;
-  const f2_t nBL2 = pk2(-BL, -BL), c15 = pk2(15.f, 15.f), al2 = pk2(ALPHA, ALPHA);
+  const f2_t nBL2 = pk2(-BL, -BL), al2 = pk2(ALPHA, ALPHA);
   const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
-  const float hW = -0.5f * nW, top = MAGIC + 15.f;   // ulp(2^23) = 1: mL < 2^23 + 15 <=> cL < 15
+  // eR = eL + (15 - W k):  k = [eL + 15 >= W/2] and [cL < 15]
+  const float thr = -0.5f * nW - 15.f, cW = 15.f + nW, top = MAGIC + 15.f;   // ulp(2^23) = 1
   f2_t sL = pk2(0.f, 0.f), sR = pk2(0.f, 0.f);
 #pragma unroll kGUnroll
   for (int c = 0; c < E / 4; ++c) {
@@ -653,12 +654,12 @@ __device__ __forceinline__ void eval_pair_x2_shift(const float4* ys4, float BL, 
       upk2(zL, a0, a1);
       const f2_t mL = fma2_rm(pk2(sat_fma(a0, kW, h), sat_fma(a1, kW, h)), al2, mg2);   // 2^23 + cL
       const f2_t eL = fma2(add2(mL, nmg2), nW2, zL);                                    // exact
-      const f2_t tR = add2(eL, c15);                                                    // zR - cL W
-      float t0, t1, m0, m1;
-      upk2(tR, t0, t1);
+      float e0, e1, m0, m1;
+      upk2(eL, e0, e1);
       upk2(mL, m0, m1);
-      const f2_t k2 = pk2(fminf(set_ge(t0, hW), set_lt(m0, top)), fminf(set_ge(t1, hW), set_lt(m1, top)));
-      const f2_t eR = fma2(k2, nW2, tR);                                                // exact
+      const float c0 = sel_ge_lt(e0, thr, m0, top, cW, 15.f);
+      const float c1 = sel_ge_lt(e1, thr, m1, top, cW, 15.f);
+      const f2_t eR = add2(eL, pk2(c0, c1));                                            // exact
       sL = fma2(eL, eL, sL);
       sR = fma2(eR, eR, sR);
     }
