@@ -133,7 +133,7 @@ __device__ __forceinline__ bool group_any(bool v) {
   unsigned bal = __ballot_sync(FULL, v);
   if (LPR == 32) return bal != 0;
   const int lane = threadIdx.x & 31;
-  unsigned gm = ((1u << LPR) - 1u) << (lane & ~(LPR - 1));
+  const unsigned gm = (unsigned)((1ull << LPR) - 1ull) << (lane & ~(LPR - 1));
   return (bal & gm) != 0;
 }
 
@@ -715,6 +715,7 @@ struct ExactOut {
   int flags;  // 1 = range error, 2 = move left, 4 = candidate better than best
 };
 
+template <bool INLINE_LEAF>
 __device__ __forceinline__ ExactOut exact_decide(RowShared* R, double nl, double nr, int bi, int bj,
                                                  bool bvalid, const float* xs, int d, double* e2,
                                                  double* leaf_sum, int* leaf_st, int* leaf_ln) {
@@ -728,6 +729,19 @@ __device__ __forceinline__ ExactOut exact_decide(RowShared* R, double nl, double
   const double rmin = __dadd_rn(x0, __dmul_rn(nl, st)), rmax = __dsub_rn(x1, __dmul_rn(nr + 1.0, st));
   const bool errL = !(lmin <= lmax);
   const bool errR = !(rmin <= rmax);
+  if (d >= 8 && d <= 128 && !errL && !errR) {   // one pairwise leaf: all ranges at once
+    const double blo = bi == 0 ? x0 : __dadd_rn(x0, __dmul_rn((double)bi, st));
+    const double bhi = bj == 0 ? x1 : __dsub_rn(x1, __dmul_rn((double)bj, st));
+    double vb;
+    if constexpr (INLINE_LEAF)   // small kernels: the call overhead outweighs the register cost
+      warp_np_loss3_leaf(xs, d, bvalid ? 2 : 3, lmin, lmax, rmin, rmax, blo, bhi, o.vL, o.vR, vb);
+    else
+      warp_np_loss3_leaf_ool(xs, d, bvalid ? 2 : 3, lmin, lmax, rmin, rmax, blo, bhi, o.vL, o.vR, vb);
+    if (!bvalid) o.vb = vb;
+    const bool goL = o.vL < o.vR;                           // clipping.py:185
+    o.flags = (goL ? 2 : 0) | ((goL ? o.vL : o.vR) < o.vb ? 4 : 0);   // clipping.py:187,191
+    return o;
+  }
   if (!errL) o.vL = warp_np_loss(xs, d, lmin, lmax, e2, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
   if (errL || errR) {
     if ((threadIdx.x & 31) == 0) {
@@ -854,7 +868,7 @@ __device__ __forceinline__ void exact_block(const Params& p, bool need_ex, int q
     const int leader = __ffs(bal) - 1;
     bal &= bal - 1;
     const int lg = leader / LPR;
-    const ExactOut o = exact_decide(
+    const ExactOut o = exact_decide<(E <= 16)>(
         &rs[lg], (double)__shfl_sync(FULL, nl, leader), (double)__shfl_sync(FULL, nr, leader),
         __shfl_sync(FULL, bi, leader), __shfl_sync(FULL, bj, leader),
         (__shfl_sync(FULL, flags, leader) & F_BEST_EX) != 0, xblk + lg * ld, d, e2, leaf_sum, leaf_st,

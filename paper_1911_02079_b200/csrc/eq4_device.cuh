@@ -150,6 +150,48 @@ static __device__ __noinline__ double warp_np_loss(const float* xs, int d, doubl
   return __dadd_rn(0.0, total);
 }
 
+// Bit-exact quant_mse (table.py:81-103) of up to three clip ranges of one row
+// with 8 <= d <= 128, i.e. a single numpy pairwise leaf: the 8 accumulator
+// chains r[m] = a[m] + a[m+8] + ... of range k run on lanes 8k..8k+7 (each
+// lane computes its own chain's element errors, in order), then
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by butterfly and the d % 8 remainder
+// on the chain-0 lane -- the same association as warp_np_loss, with the three
+// ranges in flight at once and no shared scratch.  Warp-collective; every lane
+// returns all values (ranges k >= nr are not evaluated and return 0).
+__device__ __forceinline__ void warp_np_loss3_leaf(const float* xs, int d, int nr, double lo0,
+                                                   double hi0, double lo1, double hi1, double lo2,
+                                                   double hi2, double& v0, double& v1,
+                                                   double& v2) {
+  const int lane = threadIdx.x & 31;
+  const int k = lane >> 3, m = lane & 7;
+  const double lo = k == 0 ? lo0 : (k == 1 ? lo1 : lo2);
+  const double hi = k == 0 ? hi0 : (k == 1 ? hi1 : hi2);
+  const bool act = k < nr;
+  const double scale = (hi == lo) ? 0.0 : div15(__dsub_rn(hi, lo));   // table.py:99
+  const int nfull = d - (d % 8);
+  double r = 0.0;
+  if (act) {
+    r = np_err2((double)xs[m], lo, hi, scale);
+    for (int i = 8 + m; i < nfull; i += 8) r = __dadd_rn(r, np_err2((double)xs[i], lo, hi, scale));
+  }
+  r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 1));
+  r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 2));
+  r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 4));
+  if (act && m == 0)
+    for (int i = nfull; i < d; i++) r = __dadd_rn(r, np_err2((double)xs[i], lo, hi, scale));
+  v0 = __dadd_rn(0.0, __shfl_sync(FULL, r, 0));
+  v1 = __dadd_rn(0.0, __shfl_sync(FULL, r, 8));
+  v2 = __dadd_rn(0.0, __shfl_sync(FULL, r, 16));
+}
+
+// Out-of-line copy (keeps the rare path from shaping a big kernel's registers).
+static __device__ __noinline__ void warp_np_loss3_leaf_ool(const float* xs, int d, int nr,
+                                                           double lo0, double hi0, double lo1,
+                                                           double hi1, double lo2, double hi2,
+                                                           double& v0, double& v1, double& v2) {
+  warp_np_loss3_leaf(xs, d, nr, lo0, hi0, lo1, hi1, lo2, hi2, v0, v1, v2);
+}
+
 // ---------------------------------------------------------------------------
 // Codes for the final quantize pass (uniform.py:77-79), fast path + exact fix-up
 // ---------------------------------------------------------------------------
