@@ -65,10 +65,10 @@ enum { M_ASYM = 0, M_GREEDY = 1 };
 #define GREEDY_MINB 4
 #endif
 #ifndef G_MINB32
-#define G_MINB32 4
+#define G_MINB32 3
 #endif
 #ifndef G_MINB64
-#define G_MINB64 4
+#define G_MINB64 3   // 170 registers: the phase-A loop state stays out of local memory
 #endif
 
 struct Params {
@@ -585,13 +585,12 @@ __device__ __forceinline__ void eval_pair(const float4* ys4, int nv, float BL, f
 template <int E>
 __device__ __forceinline__ void eval_pair_x2(const float4* ys4, float BL, float nW, float kW,
                                              float h, float& aL, float& aR) {
-  const int lane = threadIdx.x & 31;
   const f2_t nBL2 = pk2(-BL, -BL), c15 = pk2(15.f, 15.f), al2 = pk2(ALPHA, ALPHA);
   const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
   f2_t sL = pk2(0.f, 0.f), sR = pk2(0.f, 0.f);
 #pragma unroll kGUnroll
   for (int c = 0; c < E / 4; ++c) {
-    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32 + lane);
+    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32);
 #pragma unroll
     for (int hlf = 0; hlf < 2; ++hlf) {
       const f2_t y2 = hlf ? yy.y : yy.x;
@@ -638,7 +637,6 @@ __device__ __forceinline__ float sel_ge_lt(float e, float thr, float m, float to
 template <int E>
 __device__ __forceinline__ void eval_pair_x2_shift(const float4* ys4, float BL, float nW, float kW,
                                                    float h, float& aL, float& aR) {
-  const int lane = threadIdx.x & 31;
   const f2_t nBL2 = pk2(-BL, -BL), al2 = pk2(ALPHA, ALPHA);
   const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
   // eR = eL + (15 - W k):  k = [eL + 15 >= W/2] and [cL < 15]
@@ -646,7 +644,7 @@ __device__ __forceinline__ void eval_pair_x2_shift(const float4* ys4, float BL, 
   f2_t sL = pk2(0.f, 0.f), sR = pk2(0.f, 0.f);
 #pragma unroll kGUnroll
   for (int c = 0; c < E / 4; ++c) {
-    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32 + lane);
+    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32);
 #pragma unroll
     for (int hlf = 0; hlf < 2; ++hlf) {
       const f2_t zL = add2(hlf ? yy.y : yy.x, nBL2);
@@ -674,13 +672,12 @@ __device__ __forceinline__ void eval_pair_x2_shift(const float4* ys4, float BL, 
 // Packed single-candidate loss (the full range, clipping.py:174).
 template <int E>
 __device__ __forceinline__ float eval_one_x2(const float4* ys4, float B, float nW, float kW, float h) {
-  const int lane = threadIdx.x & 31;
   const f2_t nB2 = pk2(-B, -B), al2 = pk2(ALPHA, ALPHA);
   const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
   f2_t acc = pk2(0.f, 0.f);
 #pragma unroll kGUnroll
   for (int c = 0; c < E / 4; ++c) {
-    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32 + lane);
+    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32);
 #pragma unroll
     for (int hlf = 0; hlf < 2; ++hlf) {
       const f2_t z = add2(hlf ? yy.y : yy.x, nB2);
@@ -766,9 +763,10 @@ __device__ __forceinline__ ExactOut exact_decide(RowShared* R, double nl, double
 // GREEDY codes from the row slice: with the winning pair (bi, bj) the codes are
 // c = clamp(floor((Y - B)/Wb + 1/2), 0, 15), B = 15 bi, Wb = b - bi - bj, i.e.
 // the same saturating FFMA + round-down FFMA as the search.  Yh is within
-// delta = qY/2 of Y, so an element whose fractional part is within
-// NEAR + delta/Wb of a rounding boundary gets its code from the float64 codec
-// instead (clamping at lo/hi cannot flip a code: codes are continuous there).
+// delta = qY/2 of Y, so when any element's fractional part is within
+// NEAR + delta/Wb of a rounding boundary the row slice takes all its codes from
+// the float64 codec instead (rare; clamping at lo/hi cannot flip a code: codes
+// are continuous there).  ys4 is the lane's column of the slice.
 // Warp-collective.
 template <int LPR, int E, bool VEC>
 __device__ __forceinline__ void emit_greedy(const Params& p, const float4* ys4, int nv, int q,
@@ -782,15 +780,14 @@ __device__ __forceinline__ void emit_greedy(const Params& p, const float4* ys4, 
   const float h = 0.5f / ALPHA;
   const float nb = NEAR + p.delta / Wf;
   const bool fast = fast_ok && Wb >= 1 && ok;
-  const int lane = threadIdx.x & 31;
-  unsigned long long need = 0ull;
+  bool near = false;
   // streamed chunk by chunk (no per-slot arrays): codes go straight to the
-  // staged row; flagged slots are rewritten below
+  // staged row; a flagged slice is rewritten below
   const f2_t nB2 = pk2(-B, -B), al2 = pk2(ALPHA, ALPHA);
   const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC);
 #pragma unroll
   for (int c = 0; c < E / 4; ++c) {
-    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32 + lane);
+    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32);
     uint32_t w = 0;
 #pragma unroll
     for (int hlf = 0; hlf < 2; ++hlf) {
@@ -805,10 +802,10 @@ __device__ __forceinline__ void emit_greedy(const Params& p, const float4* ys4, 
       upk2(m, m0, m1);
       upk2(fr, f0, f1);
       const int i0 = 4 * c + 2 * hlf;
-      const bool n0 = s0 > 0.f && s0 < 1.f && (f0 < nb || f0 > 1.f - nb);
-      const bool n1 = s1 > 0.f && s1 < 1.f && (f1 < nb || f1 > 1.f - nb);
-      need |= ((unsigned long long)(n0 && (VEC || i0 < nv)) << i0) |
-              ((unsigned long long)(n1 && (VEC || i0 + 1 < nv)) << (i0 + 1));
+      // |frac - 1/2| > 1/2 - nb  <=>  frac < nb or frac > 1 - nb (s strictly inside (0, 1))
+      const bool n0 = s0 > 0.f && s0 < 1.f && fabsf(f0 - 0.5f) > 0.5f - nb;
+      const bool n1 = s1 > 0.f && s1 < 1.f && fabsf(f1 - 0.5f) > 0.5f - nb;
+      near |= (n0 && (VEC || i0 < nv)) || (n1 && (VEC || i0 + 1 < nv));
       const uint32_t c0 = ok ? (__float_as_uint(m0) & 0xFu) : 0u;
       const uint32_t c1 = ok ? (__float_as_uint(m1) & 0xFu) : 0u;
       if (VEC) {
@@ -820,21 +817,21 @@ __device__ __forceinline__ void emit_greedy(const Params& p, const float4* ys4, 
     }
     if (VEC && rvalid) *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = (uint16_t)w;
   }
-  if (!fast) need = ok ? ((nv >= 64) ? ~0ull : ((1ull << nv) - 1ull)) : 0ull;
-  if (!rvalid) need = 0ull;
-  if (__any_sync(FULL, need != 0ull)) {   // rare: float64 codec (uniform.py:77-79)
-    if (need) {
+  if (!fast) near = ok;
+  if (!rvalid) near = false;
+  if (__any_sync(FULL, near)) {   // rare: float64 codec (uniform.py:77-79) for the whole slice
+    if (near) {
       const CodeParams cp = make_code_params(lo, hi);
-      for (int i = 0; i < E; ++i) {
-        if (!((need >> i) & 1ull)) continue;
-        const unsigned cc = code_exact(xr[VEC ? 4 * (q + LPR * (i >> 2)) + (i & 3) : q + LPR * i], cp);
-        if (VEC) {
-          const int byte = 2 * (q + LPR * (i >> 2)) + ((i & 3) >> 1);
-          const int sh = (i & 1) * 4;
-          orow[byte] = (uint8_t)((orow[byte] & ~(0xF << sh)) | (cc << sh));
-        } else {
-          crow[q + LPR * i] = (uint8_t)cc;
+      for (int c = 0; c < E / 4; ++c) {
+        uint32_t w = 0;
+        for (int k = 0; k < 4; ++k) {
+          const int i = 4 * c + k;
+          if (!VEC && i >= nv) continue;
+          const unsigned cc = code_exact(xr[VEC ? 4 * (q + LPR * c) + k : q + LPR * i], cp);
+          if (VEC) w |= cc << (4 * k);
+          else crow[q + LPR * i] = (uint8_t)cc;
         }
+        if (VEC) *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = (uint16_t)w;
       }
     }
   }
@@ -907,6 +904,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
   const int gw = lane / LPR, q = lane % LPR;
   unsigned char* ws = smem + warp * S::bytes(p.stride);
   float4* ys4 = reinterpret_cast<float4*>(ws + S::ys_off());
+  const float4* ysl = ys4 + lane;   // this lane's column of the [E/4][32] slice
   RowShared* rs = reinterpret_cast<RowShared*>(ws + S::rs_off());
   double* e2 = reinterpret_cast<double*>(ws + S::e2_off());
   double* leaf_sum = reinterpret_cast<double*>(ws + S::leaf_off());
@@ -1012,7 +1010,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       const float Wf = (float)p.b;                                                   // :174
       float a0;
       if constexpr (VEC)
-        a0 = eval_one_x2<E>(ys4, 0.f, -Wf, rcp_approx(Wf * ALPHA), hh);
+        a0 = eval_one_x2<E>(ysl, 0.f, -Wf, rcp_approx(Wf * ALPHA), hh);
       else
         a0 = eval_one<E, true>(ys4, nv, 0.f, -Wf, rcp_approx(Wf * ALPHA), hh);
       Lbest = group_sum<LPR>(a0);
@@ -1034,9 +1032,9 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         float aL, aR;
         if constexpr (VEC) {
           if (Wf >= 17.f)   // codes move by at most one under the 15-shift
-            eval_pair_x2_shift<E>(ys4, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+            eval_pair_x2_shift<E>(ysl, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
           else
-            eval_pair_x2<E>(ys4, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+            eval_pair_x2<E>(ysl, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
         } else {
           eval_pair<E, true>(ys4, nv, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
         }
@@ -1087,7 +1085,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         const float Wf = (float)W;
         float aL, aR;
         if constexpr (VEC)
-          eval_pair_x2<E>(ys4, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+          eval_pair_x2<E>(ysl, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
         else
           eval_pair<E, true>(ys4, nv, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
         group_sum_pair<LPR>(aL, aR, SL, SR);
@@ -1125,7 +1123,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
     const int blk_rows = (int)min((int64_t)RPW, p.rows - row0);
     const size_t gofs = (size_t)row0 * p.stride;
     uint8_t* out_tile = out_base + (((uintptr_t)p.packed + gofs) & 15);
-    emit_greedy<LPR, E, VEC>(p, ys4, nv, q, lo, hi, bi, bj, mn != mx,
+    emit_greedy<LPR, E, VEC>(p, ysl, nv, q, lo, hi, bi, bj, mn != mx,
                              rvalid && !bad && !(flags & F_ERR), rvalid, xr,
                              out_tile + gw * p.stride, codes_w + gw * D);
     if (rvalid && q == 0) {
