@@ -305,7 +305,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--rows", type=int, default=ROWS)
-    ap.add_argument("--cpu-rows", type=int, default=200_000)
+    ap.add_argument("--cpu-rows", type=int, default=2_000_000)   # ~2 s x all host threads
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
