@@ -48,6 +48,8 @@ extern "C" {
 
 #define EQ4_STATUS_NONFINITE 1 /* a row holds NaN/Inf */
 #define EQ4_STATUS_RANGE 2     /* a GREEDY candidate had xmin > xmax (ClipRange ValueError) */
+#define EQ4_STATUS_QUERY 4     /* pooled lookup: negative length / lengths do not sum to nidx */
+#define EQ4_STATUS_INDEX 8     /* pooled lookup: a query index is out of range */
 
 /* Version string of the library build. */
 const char *eq4_version(void);
@@ -111,6 +113,26 @@ int eq4_unpack(const uint8_t *packed, int64_t rows, int64_t dim, int aux, uint8_
  * out[i] = quant_mse(x[i, :dim], ClipRange(xmin[i], xmax[i]), 4).  Device. */
 int eq4_quant_mse(const float *x, int64_t rows, int64_t dim, int64_t ld, const double *xmin,
                   const double *xmax, double *out, void *stream);
+
+/*
+ * packed.py:167-177 sparse_lengths_sum_4bit: pooled lookup over packed rows.
+ *   out[s, :] = sum over segment s's rows (lengths[s] consecutive entries of
+ *   indices), strictly in query order from 0.0f, of the dequantized row
+ *   float32(scale) * float32(code) + float32(bias) (two rounded float32 ops,
+ *   packed.py:174-176; fp16 aux widened exactly), i.e. the bit-exact contract
+ *   of sparse_lengths_sum_ref (packed.py:202-221).
+ *   packed  [rows x eq4_packed_row_stride(dim, aux)] bytes, device
+ *   indices [nidx] int64, lengths [batch] int64, out [batch x dim] fp32, device
+ * Validation on the device (PooledQuery, packed.py:131-140; _check_indices,
+ * packed.py:147-152): a negative length or sum(lengths) != nidx sets
+ * EQ4_STATUS_QUERY and zeroes out; an out-of-range index sets
+ * EQ4_STATUS_INDEX, is skipped, and the first such position is written to
+ * *bad_pos (optional device int64; INT64-large when none).  Stream-ordered.
+ */
+int eq4_sparse_lengths_sum4(const uint8_t *packed, int64_t rows, int64_t dim, int aux,
+                            const int64_t *indices, int64_t nidx, const int64_t *lengths,
+                            int64_t batch, float *out, int32_t *status, int64_t *bad_pos,
+                            void *stream);
 
 /* Diagnostics: internal arithmetic self-test on the current device (mismatch
  * count, -1 on CUDA error).  which 0/1: the divide-free float64 w/15 used for

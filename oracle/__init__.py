@@ -39,6 +39,9 @@ ERRORS = {
     6: "nbits must be 4 or 8",
     7: "allocation failed",
     8: "unknown method",
+    9: "lengths must be non-negative",
+    10: "lengths do not sum to the number of indices",
+    11: "query index out of range",
 }
 
 
@@ -79,6 +82,7 @@ def lib():
         L.eqo_quantize_pack_table.argtypes = [vp, i64, i64, i64, i32, i32, dbl, i32, vp, vp, vp,
                                               vp, vp, vp, i32]
         L.eqo_max_threads.restype = i32
+        L.eqo_sls4.argtypes = [vp, i64, i64, i32, vp, i64, vp, i64, vp, vp]
         _lib = L
     return _lib
 
@@ -240,3 +244,19 @@ def quantize_pack_table(x, method: str, b: int = 200, r: float = 0.16, aux: str 
     if rc:
         raise OracleError(rc)
     return TableResult(packed, lo, hi, i0, i1, nv)
+
+
+def sparse_lengths_sum4(packed, rows: int, d: int, aux: str, indices, lengths):
+    """packed.py:202-221 sparse_lengths_sum_ref over a PackedTable4 buffer.
+
+    Returns (out float32 [batch x d], error code, bad position): error 0 = ok,
+    9/10 = PooledQuery validation (packed.py:131-140), 11 = index out of range
+    at `bad position` (packed.py:147-152)."""
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    idx = np.ascontiguousarray(indices, dtype=np.int64).ravel()
+    ln = np.ascontiguousarray(lengths, dtype=np.int64).ravel()
+    out = np.zeros((ln.size, d), np.float32)
+    bad = np.full(1, -1, np.int64)
+    rc = lib().eqo_sls4(_p(packed), rows, d, AUX[aux], _p(idx), idx.size, _p(ln), ln.size,
+                        _p(out), _p(bad))
+    return out, int(rc), int(bad[0])

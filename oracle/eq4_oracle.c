@@ -447,3 +447,67 @@ int eqo_max_threads(void) {
     return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------------ */
+/* packed.py:202-221 sparse_lengths_sum_ref for a PackedTable4 source: for each
+ * segment s (lengths[s] consecutive entries of indices), out[s, j] accumulates
+ * float32(float32(scale) * float32(code) + float32(bias)) in query order,
+ * starting from 0.0f (packed.py:185-201 _ref_row_value, nibble decoded from
+ * the byte buffer; fp16 aux widened exactly).  PooledQuery validation
+ * (packed.py:131-140) and _check_indices (packed.py:147-152) first:
+ *   EQO_ELEN   a negative length
+ *   EQO_ESUM   lengths do not sum to nidx (*bad_pos = the sum)
+ *   EQO_EINDEX first out-of-range index at position *bad_pos
+ * out [batch x d] float32.  Float arithmetic is float32 (no contraction). */
+#define EQO_ELEN 9
+#define EQO_ESUM 10
+#define EQO_EINDEX 11
+
+static float aux_to_f32(const uint8_t *p, int aux) {
+    if (aux == 1) {
+        _Float16 h;
+        memcpy(&h, p, 2);
+        return (float)h;
+    }
+    float f;
+    memcpy(&f, p, 4);
+    return f;
+}
+
+int eqo_sls4(const uint8_t *packed, long rows, long d, int aux, const int64_t *indices, long nidx,
+             const int64_t *lengths, long batch, float *out, int64_t *bad_pos) {
+    int64_t total = 0;
+    for (long s = 0; s < batch; s++) {
+        if (lengths[s] < 0) return EQO_ELEN;
+        total += lengths[s];
+    }
+    if (total != nidx) {
+        if (bad_pos) *bad_pos = total;
+        return EQO_ESUM;
+    }
+    for (long p = 0; p < nidx; p++)
+        if (indices[p] < 0 || indices[p] >= rows) {
+            if (bad_pos) *bad_pos = p;
+            return EQO_EINDEX;
+        }
+    const long stride = eqo_packed_row_stride(d, aux), half = (d + 1) / 2;
+    const int ab = aux == 1 ? 2 : 4;
+    long pos = 0;
+    for (long s = 0; s < batch; s++) {
+        float *o = out + s * d;
+        for (long j = 0; j < d; j++) o[j] = 0.0f;
+        for (int64_t t = 0; t < lengths[s]; t++, pos++) {
+            const uint8_t *row = packed + indices[pos] * stride;
+            const float scale = aux_to_f32(row + half, aux);
+            const float bias = aux_to_f32(row + half + ab, aux);
+            for (long j = 0; j < d; j++) {
+                const uint8_t byte = row[j / 2];
+                const float code = (float)((j % 2 == 0) ? (byte & 0x0F) : (byte >> 4));
+                const float prod = scale * code;          /* rounded to float32 */
+                const float v = prod + bias;              /* rounded to float32 */
+                o[j] = o[j] + v;
+            }
+        }
+    }
+    return EQO_OK;
+}

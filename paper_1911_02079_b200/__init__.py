@@ -32,5 +32,6 @@ from .api import (  # noqa: F401
     quantize_table,
     row_clip_range,
 )
+from .pooled import PooledQuery, bytes_per_pooled_row, sparse_lengths_sum_4bit  # noqa: F401
 
 __version__ = "0.1.0"

@@ -25,6 +25,8 @@ METHOD = {"asym": 0, "greedy": 1, "hist-brute": 2}
 AUX = {"fp32": 0, "fp16": 1}
 STATUS_NONFINITE = 1
 STATUS_RANGE = 2
+STATUS_QUERY = 4
+STATUS_INDEX = 8
 
 # every symbol include/eq4.h declares (tests check the .so exports them all)
 EXPORTS = (
@@ -36,6 +38,7 @@ EXPORTS = (
     "eq4_pack",
     "eq4_unpack",
     "eq4_quant_mse",
+    "eq4_sparse_lengths_sum4",
     "eq4_selftest",
 )
 
@@ -77,6 +80,8 @@ def load() -> ctypes.CDLL:
         L.eq4_unpack.restype = i32
         L.eq4_quant_mse.argtypes = [vp, i64, i64, i64, vp, vp, vp, vp]
         L.eq4_quant_mse.restype = i32
+        L.eq4_sparse_lengths_sum4.argtypes = [vp, i64, i64, i32, vp, i64, vp, i64, vp, vp, vp, vp]
+        L.eq4_sparse_lengths_sum4.restype = i32
         L.eq4_selftest.argtypes = [i32, i64, ctypes.c_uint64]
         L.eq4_selftest.restype = ctypes.c_longlong
         _lib = L

@@ -1537,6 +1537,21 @@ const char* eq4_version(void) { return "eq4 0.1.0 (sm_100a)"; }
 
 const char* eq4_last_error(void) { return g_err.c_str(); }
 
+int eq4_sparse_lengths_sum4(const uint8_t* packed, int64_t rows, int64_t dim, int aux,
+                            const int64_t* indices, int64_t nidx, const int64_t* lengths,
+                            int64_t batch, float* out, int32_t* status, int64_t* bad_pos,
+                            void* stream) {
+  if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "packed table must be at least 1x1");
+  if (batch < 0 || nidx < 0) return fail(EQ4_EINVAL, "batch and nidx must be non-negative");
+  if (aux != EQ4_AUX_FP16 && aux != EQ4_AUX_FP32) return fail(EQ4_EINVAL, "aux must be fp32 or fp16");
+  if (!packed || (batch > 0 && (!lengths || !out)) || (nidx > 0 && !indices))
+    return fail(EQ4_EINVAL, "null buffer");
+  std::string err;
+  const int rc = eq4_sls_launch(packed, rows, dim, aux, indices, nidx, lengths, batch, out, status,
+                                bad_pos, (cudaStream_t)stream, err);
+  return rc == EQ4_OK ? rc : fail(rc, err);
+}
+
 int64_t eq4_packed_row_stride(int64_t dim, int aux) {
   return (dim + 1) / 2 + 2 * (aux == EQ4_AUX_FP16 ? 2 : 4);
 }

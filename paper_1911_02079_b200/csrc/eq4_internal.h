@@ -10,3 +10,8 @@
 int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b, int aux,
                     uint8_t* packed, double* xmin, double* xmax, int32_t* info0, int32_t* info1,
                     double* norm, int32_t* status, cudaStream_t s, std::string& err);
+
+// Pooled lookup over packed rows (eq4_sls.cu).  Returns an EQ4_* code.
+int eq4_sls_launch(const uint8_t* packed, int64_t rows, int64_t dim, int aux,
+                   const int64_t* indices, int64_t nidx, const int64_t* lengths, int64_t batch,
+                   float* out, int32_t* status, int64_t* bad_pos, cudaStream_t s, std::string& err);

@@ -215,7 +215,54 @@ def make_mse():
     print("quant_mse: done")
 
 
+def make_sls():
+    """sparse_lengths_sum_4bit over packed tables (packed.py:167-177), checked against
+    sparse_lengths_sum_ref (packed.py:202-221), plus the reference's error texts."""
+    from embquant.packed import PooledQuery, sparse_lengths_sum_4bit, sparse_lengths_sum_ref
+    from embquant.uniform import UniformQuantTable
+
+    rng = np.random.default_rng(11)
+    bufs, outs, idxs, lens, meta = [], [], [], [], []
+    for case in range(400):
+        rows = int(rng.integers(1, 7)) if case % 4 else int(rng.integers(7, 60))
+        d = int(rng.integers(1, 41)) if case % 10 else int(rng.choice([64, 96, 128, 256, 2048]))
+        aux = "fp32" if case % 3 else "fp16"
+        codes = rng.integers(0, 16, size=(rows, d)).astype(np.uint8)
+        scales = 0.01 + rng.integers(0, 1000, size=rows) / 250.0 * 10.0 ** rng.uniform(-3, 2)
+        biases = -2.0 + rng.integers(0, 1000, size=rows) / 250.0 * 10.0 ** rng.uniform(-3, 2)
+        q = UniformQuantTable(codes, scales, biases, 4, aux)
+        packed = eq.pack_table4(q)
+        batch = int(rng.integers(1, 6))
+        ln = rng.integers(0, 5, size=batch)
+        if case % 17 == 0:
+            ln[:] = 0
+        idx = rng.integers(0, rows, size=int(ln.sum()))
+        query = PooledQuery(idx, ln)
+        got = sparse_lengths_sum_4bit(packed, query)
+        want = sparse_lengths_sum_ref(packed, query)
+        assert np.array_equal(got, want)
+        bufs.append(packed.buffer.copy()); outs.append(got.ravel()); idxs.append(idx); lens.append(ln)
+        meta.append((rows, d, 1 if aux == "fp16" else 0, batch, idx.size))
+    errs = {}
+    packed = eq.pack_table4(UniformQuantTable(np.zeros((4, 6), np.uint8), np.ones(4), np.zeros(4), 4, "fp16"))
+    for name, (i, l) in {"oob": ([0, 1, 9], [3]), "neg": ([0, 1], [-1, 2])}.items():
+        try:
+            sparse_lengths_sum_4bit(packed, PooledQuery(i, l))
+        except (IndexError, ValueError) as e:
+            errs[name] = f"{type(e).__name__}: {e}"
+    try:
+        PooledQuery([1, 2], [1])
+    except ValueError as e:
+        errs["sum"] = f"ValueError: {e}"
+    out = {"packed": np.concatenate(bufs), "out": np.concatenate(outs), "indices": np.concatenate(idxs),
+           "lengths": np.concatenate(lens), "meta": np.array(meta, np.int64),
+           "errors": np.array(json.dumps(errs))}
+    np.savez_compressed(os.path.join(HERE, "sls.npz"), **out)
+    print("sls: done", errs)
+
+
 if __name__ == "__main__":
-    which = sys.argv[2:] or ["mse", "edge", "hist", "config1"]
+    which = sys.argv[2:] or ["mse", "edge", "hist", "config1", "sls"]
     for w in which:
-        {"mse": make_mse, "edge": make_edge, "hist": make_hist, "config1": make_config1}[w]()
+        {"mse": make_mse, "edge": make_edge, "hist": make_hist, "config1": make_config1,
+         "sls": make_sls}[w]()

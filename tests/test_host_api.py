@@ -184,3 +184,26 @@ def test_row_sharded_quantization_over_gloo():
     want = oracle.quantize_pack_table(x, "greedy", 200, 0.16, "fp16").packed
     assert got == want.tobytes()
     assert tmax == float(world)
+
+
+def test_pooled_query_validation_matches_reference(ref):
+    from embquant.packed import PooledQuery as RefQuery
+
+    for i, l in (([1, 2], [1]), ([1], [-1, 2]), ([], [0, -1])):
+        with pytest.raises(ValueError) as theirs:
+            RefQuery(i, l)
+        with pytest.raises(ValueError) as ours:
+            eq.PooledQuery(i, l)
+        assert str(ours.value) == str(theirs.value)
+    q = eq.PooledQuery([3, 1, 2], [2, 0, 1])
+    assert q.batch == 3 and q.indices.dtype == np.int64
+
+
+def test_bytes_per_pooled_row_kats():
+    # test_packed.py:159-181
+    assert eq.bytes_per_pooled_row("fp32", 128) == 512
+    assert eq.bytes_per_pooled_row("int8", 128, "fp32") == 136
+    assert eq.bytes_per_pooled_row("int4", 128, "fp32") == 72
+    assert eq.bytes_per_pooled_row("int4", 128, "fp16") == 68
+    with pytest.raises(ValueError):
+        eq.bytes_per_pooled_row("int2", 8)

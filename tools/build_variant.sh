@@ -14,9 +14,11 @@ if [ -n "$REV" ]; then
   src=$tmp/paper_1911_02079_b200/csrc
 fi
 F="-O3 -lineinfo -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr"
-/usr/local/cuda/bin/nvcc $F "$@" -c -o $out/obj_$name/eq4.o $src/eq4.cu 2>/dev/null &
-/usr/local/cuda/bin/nvcc $F "$@" -c -o $out/obj_$name/eq4_hist.o $src/eq4_hist.cu 2>/dev/null &
+for f in $src/*.cu; do
+  b=$(basename $f .cu)
+  /usr/local/cuda/bin/nvcc $F "$@" -c -o $out/obj_$name/$b.o $f 2>/dev/null &
+done
 wait
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libeq4_$name.so $out/obj_$name/eq4.o $out/obj_$name/eq4_hist.o
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libeq4_$name.so $out/obj_$name/*.o
 rm -rf $out/obj_$name ${tmp:-}
 echo $out/libeq4_$name.so
