@@ -54,8 +54,11 @@ constexpr int LT = 2048;            // lengths per scan tile (256 threads x 8)
 #define SLS_L2HINT ""
 #endif
 constexpr int SLS_THREADS = SLS_NTHREADS;
+#ifndef SLS_MINB
+#define SLS_MINB 6
+#endif
 constexpr int SLS_WARPS = SLS_THREADS / 32;
-constexpr int TILE_BYTES = 24 * 1024;
+constexpr int SLS_BUF_BYTES = 20 * 1024;   // gathered rows of one tile
 constexpr int MAX_TILE_ROWS = SLS_TILE_ROWS;
 
 struct SlsParams {
@@ -79,11 +82,20 @@ struct SlsParams {
   unsigned long long* bad_pos;
   int tile_rows;
   int64_t ntiles;
+  int64_t* tile_seg;      // [ntiles] first segment intersecting each tile
 };
 
 __device__ __forceinline__ void flag_index(const SlsParams& p, int64_t pos) {
   atomicMin(p.bad_pos, (unsigned long long)pos);
   if (p.status) atomicOr(p.status, EQ4_STATUS_INDEX);
+}
+
+// Programmatic dependent launch: a kernel may start while its predecessor in
+// the stream is still running; griddep_wait() blocks until the predecessor
+// has completed and its writes are visible.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // ---- lengths -> offsets (PooledQuery validation, packed.py:131-140) ----
@@ -104,6 +116,7 @@ __device__ __forceinline__ T block_sum(T v, T* sh) {
 
 __global__ void __launch_bounds__(256) k_len_partials(const SlsParams p) {
   __shared__ int64_t sh[8];
+  griddep_launch();
   const int64_t base = (int64_t)blockIdx.x * LT;
   int64_t sum = 0;
   bool bad = false;
@@ -125,6 +138,8 @@ __global__ void __launch_bounds__(1024) k_len_scan(const SlsParams p) {
   __shared__ int64_t wsum[32];
   __shared__ int64_t carry_in;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  griddep_launch();
+  griddep_wait();   // partial sums of k_len_partials
   if (threadIdx.x == 0) carry_in = 0;
   __syncthreads();
   for (int64_t c0 = 0; c0 < p.nlt; c0 += 1024) {
@@ -171,6 +186,7 @@ __global__ void __launch_bounds__(256) k_len_offsets(const SlsParams p) {
   __shared__ int64_t wsum[8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t s0 = (int64_t)blockIdx.x * LT + 8 * threadIdx.x;
+  griddep_launch();
   int64_t l[8], tsum = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -186,6 +202,7 @@ __global__ void __launch_bounds__(256) k_len_offsets(const SlsParams p) {
   __syncthreads();
   int64_t wpre = 0;
   for (int k = 0; k < w; ++k) wpre += wsum[k];
+  griddep_wait();   // scanned partials and q_ok of k_len_scan
   int64_t run = p.partial[blockIdx.x] + wpre + x - tsum;
   const bool ok = *p.q_ok != 0;
 #pragma unroll
@@ -193,6 +210,11 @@ __global__ void __launch_bounds__(256) k_len_offsets(const SlsParams p) {
     if (s0 + k < p.batch) {
       p.offsets[s0 + k] = run;
       if (!ok || l[k] == 0) zero_row(p, s0 + k);
+      // tiles whose first position falls in this segment start with it
+      if (ok && l[k] > 0) {
+        const int64_t T = p.tile_rows;
+        for (int64_t t = (run + T - 1) / T; t * T < run + l[k]; ++t) p.tile_seg[t] = s0 + k;
+      }
     }
     run += l[k];
   }
@@ -240,42 +262,30 @@ __device__ __forceinline__ float aux_at(const uint8_t* a, int aux) {
                          ((uint32_t)a[3] << 24));
 }
 
-// M = packed bytes per lane per pass (row bytes b = lane + 32 m, codes 2b, 2b+1)
-template <int M>
-__global__ void __launch_bounds__(SLS_THREADS) k_sls_tiles(const SlsParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ uint32_t tile_sh;
-  __shared__ int64_t seg_first;
-  const int T = p.tile_rows;
-  int64_t* idx_s = reinterpret_cast<int64_t*>(smem);
-  uint8_t* rows_s = smem + (size_t)T * 8;
-  if (*p.q_ok == 0) return;
-  if (threadIdx.x == 0) tile_sh = atomicAdd(p.tile_counter, 1u);
-  __syncthreads();
-  const int64_t tile = tile_sh;
-  const int64_t P0 = tile * T, P1 = min(p.nidx, P0 + T);
-  const int n = (int)(P1 - P0);
-  // stage indices (packed.py:147-152 range check)
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Stage tile `tile`'s indices in shared memory (one coalesced pass; out-of-range
+// indices, packed.py:147-152, are reported and become -1), then issue the copies
+// of its rows into `buf` (row-major, the packed stride).  An out-of-range row is
+// staged as zeros (scale 0, bias 0), which adds nothing to a sum.
+__device__ __forceinline__ void gather_tile(const SlsParams& p, int64_t tile, uint8_t* buf,
+                                            int64_t* idx_s, bool words) {
+  const int T = p.tile_rows, stride = p.stride;
+  const int64_t P0 = tile * T;
+  const int n = (int)(min(p.nidx, P0 + T) - P0);
   for (int r = threadIdx.x; r < n; r += SLS_THREADS) {
-    int64_t i = p.indices[P0 + r];
+    int64_t i = __ldg(p.indices + P0 + r);
     if (i < 0 || i >= p.rows) {
       flag_index(p, P0 + r);
       i = -1;
     }
     idx_s[r] = i;
   }
-  if (threadIdx.x == 0) {   // first segment intersecting the tile: last s with offsets[s] <= P0
-    int64_t lo = 0, hi = p.batch;
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (p.offsets[mid] <= P0) lo = mid; else hi = mid;
-    }
-    seg_first = lo;
-  }
   __syncthreads();
-  // gather the tile's rows (an out-of-range row is staged as zeros: scale 0, bias 0)
-  const int stride = p.stride;
-  const bool words = (stride & 3) == 0 && (p.half & 3) == 0 && (((uintptr_t)p.packed) & 3) == 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (words) {
     const int wpr = stride >> 2;
@@ -284,7 +294,7 @@ __global__ void __launch_bounds__(SLS_THREADS) k_sls_tiles(const SlsParams p) {
       if (rr < rpw) {
         for (int r = warp * rpw + rr; r < n; r += SLS_WARPS * rpw) {
           const int64_t i = idx_s[r];
-          uint32_t* dst = reinterpret_cast<uint32_t*>(rows_s + (size_t)r * stride) + k;
+          uint32_t* dst = reinterpret_cast<uint32_t*>(buf + (size_t)r * stride) + k;
           if (i >= 0) cp_async4(dst, p.packed + i * stride + 4 * k);
           else *dst = 0u;
         }
@@ -292,27 +302,35 @@ __global__ void __launch_bounds__(SLS_THREADS) k_sls_tiles(const SlsParams p) {
     } else {           // wide rows: one warp per row
       for (int r = warp; r < n; r += SLS_WARPS) {
         const int64_t i = idx_s[r];
-        uint32_t* dst = reinterpret_cast<uint32_t*>(rows_s + (size_t)r * stride);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(buf + (size_t)r * stride);
         for (int k = lane; k < wpr; k += 32) {
           if (i >= 0) cp_async4(dst + k, p.packed + i * stride + 4 * k);
           else dst[k] = 0u;
         }
       }
     }
-    cp_async_wait_all();
-  } else {
-    const int total = n * stride;
-    for (int b = threadIdx.x; b < total; b += SLS_THREADS) {
-      const int r = b / stride, k = b - r * stride;
+  } else {             // unaligned rows: plain byte copies
+    for (int r = warp; r < n; r += SLS_WARPS) {
       const int64_t i = idx_s[r];
-      rows_s[b] = i >= 0 ? p.packed[i * stride + k] : (uint8_t)0;
+      for (int k = lane; k < stride; k += 32)
+        buf[(size_t)r * stride + k] = i >= 0 ? p.packed[i * stride + k] : (uint8_t)0;
     }
   }
-  __syncthreads();
-  // ordered sums, one warp per segment
+  cp_async_commit();
+}
+
+// Ordered sums of the segments intersecting tile `tile` (staged in buf): segment
+// k of the tile goes to warp k mod 8, lanes over the row bytes (M per lane).
+template <int M>
+__device__ __forceinline__ void accumulate_tile(const SlsParams& p, int64_t tile, const uint8_t* buf,
+                                                bool words) {
+  const int T = p.tile_rows, stride = p.stride;
+  const int64_t P0 = tile * T, P1 = min(p.nidx, P0 + T);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int half = p.half, d = p.dim;
   const int ab = p.aux == EQ4_AUX_FP16 ? 2 : 4;
   const sls::f2 magic2 = sls::pk(-8388608.f, -8388608.f);
+  const int64_t seg_first = p.tile_seg[tile];
   for (int64_t s = seg_first + warp; s < p.batch; s += SLS_WARPS) {
     const int64_t off = p.offsets[s];
     if (off >= P1) break;
@@ -321,8 +339,7 @@ __global__ void __launch_bounds__(SLS_THREADS) k_sls_tiles(const SlsParams p) {
     const bool before = off < P0, after = end > P1;
     const int r0 = (int)(max(off, P0) - P0), r1 = (int)(min(end, P1) - P0);
     if (before) {              // the previous tile's carry for this segment
-      while (ld_acquire(p.carry_flag + tile - 1) == 0) {
-      }
+      while (ld_acquire(p.carry_flag + tile - 1) == 0) __nanosleep(64);
     }
     for (int b0 = 0; b0 < half; b0 += 32 * M) {
       sls::f2 acc[M];
@@ -334,7 +351,7 @@ __global__ void __launch_bounds__(SLS_THREADS) k_sls_tiles(const SlsParams p) {
       }
 #pragma unroll 8
       for (int r = r0; r < r1; ++r) {   // unrolled: the shared-memory loads of 8 rows in flight
-        const uint8_t* row = rows_s + (size_t)r * stride;
+        const uint8_t* row = buf + (size_t)r * stride;
         float sc, bi;
         if (words) {
           const uint32_t* aw = reinterpret_cast<const uint32_t*>(row + half);
@@ -387,6 +404,45 @@ __global__ void __launch_bounds__(SLS_THREADS) k_sls_tiles(const SlsParams p) {
   }
 }
 
+// One tile per CTA (tile ids from an atomic counter, so they are handed out in
+// scheduling order and a CTA waiting for the previous tile's carry always waits
+// on a resident or finished CTA).
+template <int M>
+__global__ void __launch_bounds__(SLS_THREADS, M <= 1 ? SLS_MINB : (M <= 4 ? 4 : 2)) k_sls_tiles(const SlsParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t claim_sh;
+  const bool words = (p.stride & 3) == 0 && (p.half & 3) == 0 && (((uintptr_t)p.packed) & 3) == 0;
+  if (threadIdx.x == 0) claim_sh = atomicAdd(p.tile_counter, 1u);
+  __syncthreads();
+  const int64_t tile = claim_sh;
+  int64_t* idx_s = reinterpret_cast<int64_t*>(smem);
+  uint8_t* rows_s = smem + (size_t)p.tile_rows * 8;
+  gather_tile(p, tile, rows_s, idx_s, words);
+  // the gather only needs the indices; segment offsets and the query check
+  // come from the scan kernels that may still be finishing
+  griddep_wait();
+  cp_async_wait_group<0>();
+  __syncthreads();
+  if (*p.q_ok == 0) return;
+  accumulate_tile<M>(p, tile, rows_s, words);
+}
+
+template <typename Kern>
+static cudaError_t launch_pdl(Kern k, unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                              const SlsParams& p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, p);
+}
+
 }  // namespace eq4
 
 using namespace eq4;
@@ -401,16 +457,17 @@ int eq4_sls_launch(const uint8_t* packed, int64_t rows, int64_t dim, int aux,
   p.stride = p.half + 2 * (aux == EQ4_AUX_FP16 ? 2 : 4);
   p.indices = indices; p.nidx = nidx; p.lengths = lengths; p.batch = batch; p.out = out;
   p.status = status;
-  int T = TILE_BYTES / p.stride;
+  int T = SLS_BUF_BYTES / p.stride;
   if (T > MAX_TILE_ROWS) T = MAX_TILE_ROWS;
   if (T < 1) T = 1;
   p.tile_rows = T;
   p.ntiles = (nidx + T - 1) / T;
   p.nlt = (batch + LT - 1) / LT;
-  // scratch: offsets | partial | carry | carry_flag | q_ok, neg, tile_counter, pad | bad_pos
+  // scratch: offsets | partial | tile_seg | carry | carry_flag | q_ok, neg, tile_counter, pad | bad_pos
   const size_t off_b = 0;
   const size_t part_b = off_b + (size_t)batch * 8;
-  const size_t carry_b = part_b + (size_t)p.nlt * 8;
+  const size_t tseg_b = part_b + (size_t)p.nlt * 8;
+  const size_t carry_b = tseg_b + (size_t)p.ntiles * 8;
   const size_t flag_b = carry_b + (((size_t)p.ntiles * dim * 4 + 15) & ~(size_t)15);
   const size_t misc_b = flag_b + (((size_t)p.ntiles * 4 + 15) & ~(size_t)15);
   const size_t bad_b = misc_b + 16;
@@ -420,6 +477,7 @@ int eq4_sls_launch(const uint8_t* packed, int64_t rows, int64_t dim, int aux,
   if (e != cudaSuccess) { err = std::string("cudaMallocAsync: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
   p.offsets = reinterpret_cast<int64_t*>(scratch + off_b);
   p.partial = reinterpret_cast<int64_t*>(scratch + part_b);
+  p.tile_seg = reinterpret_cast<int64_t*>(scratch + tseg_b);
   p.carry = reinterpret_cast<float*>(scratch + carry_b);
   p.carry_flag = reinterpret_cast<int32_t*>(scratch + flag_b);
   p.q_ok = reinterpret_cast<int32_t*>(scratch + misc_b);
@@ -431,21 +489,22 @@ int eq4_sls_launch(const uint8_t* packed, int64_t rows, int64_t dim, int aux,
   if (e == cudaSuccess) e = cudaMemsetAsync(p.bad_pos, 0x7f, 8, s);   // 0x7f7f... = none
   if (e == cudaSuccess) {
     if (p.nlt > 0) k_len_partials<<<(unsigned)p.nlt, 256, 0, s>>>(p);
-    k_len_scan<<<1, 1024, 0, s>>>(p);   // batch == 0: valid iff nidx == 0
-    if (p.nlt > 0) k_len_offsets<<<(unsigned)p.nlt, 256, 0, s>>>(p);
     e = cudaGetLastError();
+    // the rest chain with programmatic dependent launch (each waits in-kernel)
+    if (e == cudaSuccess) e = launch_pdl(k_len_scan, 1, 1024, 0, s, p);   // batch 0: ok iff nidx 0
+    if (e == cudaSuccess && p.nlt > 0) e = launch_pdl(k_len_offsets, (unsigned)p.nlt, 256, 0, s, p);
   }
   if (e == cudaSuccess && p.ntiles > 0) {
-    const size_t sm = (size_t)T * 8 + (size_t)T * p.stride;
+    const size_t sm = (size_t)T * 8 + (((size_t)T * p.stride + 15) & ~(size_t)15);
     const int M = p.half <= 32 ? 1 : p.half <= 64 ? 2 : p.half <= 128 ? 4 : p.half <= 256 ? 8 : 16;
+    const unsigned g = (unsigned)p.ntiles;
     switch (M) {
-      case 1: k_sls_tiles<1><<<(unsigned)p.ntiles, SLS_THREADS, sm, s>>>(p); break;
-      case 2: k_sls_tiles<2><<<(unsigned)p.ntiles, SLS_THREADS, sm, s>>>(p); break;
-      case 4: k_sls_tiles<4><<<(unsigned)p.ntiles, SLS_THREADS, sm, s>>>(p); break;
-      case 8: k_sls_tiles<8><<<(unsigned)p.ntiles, SLS_THREADS, sm, s>>>(p); break;
-      default: k_sls_tiles<16><<<(unsigned)p.ntiles, SLS_THREADS, sm, s>>>(p); break;
+      case 1: e = launch_pdl(k_sls_tiles<1>, g, SLS_THREADS, sm, s, p); break;
+      case 2: e = launch_pdl(k_sls_tiles<2>, g, SLS_THREADS, sm, s, p); break;
+      case 4: e = launch_pdl(k_sls_tiles<4>, g, SLS_THREADS, sm, s, p); break;
+      case 8: e = launch_pdl(k_sls_tiles<8>, g, SLS_THREADS, sm, s, p); break;
+      default: e = launch_pdl(k_sls_tiles<16>, g, SLS_THREADS, sm, s, p); break;
     }
-    e = cudaGetLastError();
   }
   cudaFreeAsync(scratch, s);
   if (e != cudaSuccess) {
