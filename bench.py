@@ -266,6 +266,7 @@ def run_ours(args, rank: int, world: int):
     }
     if args.secondary:
         line["secondary"] = secondary(eq, workloads, torch, dev, peaks)
+        line["secondary"]["sls_20Mx64_greedy_packed"] = sls_secondary(eq, torch, dev, peaks, out, rows)
     print(json.dumps(line), flush=True)
 
 
@@ -296,6 +297,54 @@ def secondary(eq, workloads, torch, dev, peaks):
         res[name] = r
         del x, out
     return res
+
+
+def sls_secondary(eq, torch, dev, peaks, packed_buf, rows, batch=16384, pool=64):
+    """§8f.1 pooled lookup (sparse_lengths_sum_4bit) over the step's own GREEDY-packed
+    20M x 64 fp16 table: batch x pool uniform random rows, timed as a CUDA graph of 20
+    calls (no host gaps).  Algorithmic bytes = packed row + int64 index per pooled row
+    + the fp32 output (bench.py:31-42 bytes model of the reference, plus index/output)."""
+    p = eq.PackedTable4(rows, DIM, AUX, device_buffer=packed_buf)
+    g = torch.Generator(device=dev).manual_seed(1911)
+    idx = torch.randint(0, rows, (batch * pool,), device=dev, generator=g)
+    ln = torch.full((batch,), pool, dtype=torch.int64, device=dev)
+    q = eq.PooledQuery(idx, ln)
+    o = torch.empty(batch, DIM, device=dev)
+    eq.sparse_lengths_sum_4bit(p, q, out=o)   # validated once (raises on bad input)
+    f = lambda: eq.sparse_lengths_sum_4bit(p, q, out=o, check=False)
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        for _ in range(3):
+            f()
+    torch.cuda.current_stream(dev).wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    n = 20
+    with torch.cuda.graph(graph):
+        for _ in range(n):
+            f()
+    graph.replay()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    graph.replay()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / n
+    nrows = batch * pool
+    alg = nrows * (eq.bytes_per_pooled_row("int4", DIM, AUX) + 8) + batch * DIM * 4
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get("sls_20Mx64", {}).get("dram_bytes_per_launch")
+    return {"us": ms * 1e3, "batch": batch, "pooling": pool, "pooled_rows_per_s": nrows / ms * 1e3,
+            "giga_sums_per_s": nrows * DIM / ms / 1e6, "alg_GBps": alg / ms / 1e6,
+            "roofline": {"bound": "hbm", "achieved": alg / ms / 1e6,
+                         "peak": float(peaks.get("hbm_gbs", 6546.9)), "unit": "GB/s",
+                         "frac": alg / ms / 1e6 / float(peaks.get("hbm_gbs", 6546.9)),
+                         "traffic": traffic,
+                         "note": "random 36-byte row gathers: DRAM moves ~160 B per row"}}
 
 
 def main():

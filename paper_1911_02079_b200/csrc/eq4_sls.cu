@@ -234,6 +234,11 @@ __device__ __forceinline__ int ld_acquire(const int32_t* f) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int32_t* f) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release(int32_t* f, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(f), "r"(v) : "memory");
 }
@@ -339,7 +344,10 @@ __device__ __forceinline__ void accumulate_tile(const SlsParams& p, int64_t tile
     const bool before = off < P0, after = end > P1;
     const int r0 = (int)(max(off, P0) - P0), r1 = (int)(min(end, P1) - P0);
     if (before) {              // the previous tile's carry for this segment
-      while (ld_acquire(p.carry_flag + tile - 1) == 0) __nanosleep(64);
+      // poll with relaxed loads (an acquire load invalidates L1 on every poll), then
+      // one acquire to order the carry reads after the flag
+      while (ld_relaxed(p.carry_flag + tile - 1) == 0) __nanosleep(32);
+      (void)ld_acquire(p.carry_flag + tile - 1);
     }
     for (int b0 = 0; b0 < half; b0 += 32 * M) {
       sls::f2 acc[M];
