@@ -134,6 +134,25 @@ int eq4_sparse_lengths_sum4(const uint8_t *packed, int64_t rows, int64_t dim, in
                             int64_t batch, float *out, int32_t *status, int64_t *bad_pos,
                             void *stream);
 
+/*
+ * EMBT file -> EMBQ uniform4 file (fileio.py:40-70 read_embt, methods.py:63-89,
+ * packed.py:68-83, fileio.py:87-101 write_embq), streamed: chunks of the EMBT
+ * payload are read into pinned memory, quantized on the GPU and written as the
+ * reference's EMBQ header + PackedTable4 bytes while the next chunk is read.
+ * Synchronous.  EQ4_EDATA for a malformed input or non-finite values
+ * (read_embt's DataError), EQ4_ERANGE with *bad_row / bad_lohi for a GREEDY
+ * candidate with xmin > xmax; on failure no output file is left behind.
+ * chunk_rows = 0 picks ~64 MiB of input per chunk.
+ */
+int eq4_quantize_file(const char *in_path, const char *out_path, int method, int b, double r,
+                      int aux, int64_t chunk_rows, int64_t *bad_row, double *bad_lohi);
+
+/* fileio.py:87-101 write_embq of a PackedTable4: the EMBQ uniform4 header then
+ * the packed rows verbatim.  on_device != 0: `packed` is a device pointer and
+ * is streamed out through pinned buffers (no host repack).  Synchronous. */
+int eq4_write_embq(const char *path, const uint8_t *packed, int64_t rows, int64_t dim, int aux,
+                   int on_device);
+
 /* Diagnostics: internal arithmetic self-test on the current device (mismatch
  * count, -1 on CUDA error).  which 0/1: the divide-free float64 w/15 used for
  * scales against the IEEE divide, on float differences / full-range doubles. */

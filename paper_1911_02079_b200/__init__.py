@@ -33,5 +33,7 @@ from .api import (  # noqa: F401
     row_clip_range,
 )
 from .pooled import PooledQuery, bytes_per_pooled_row, sparse_lengths_sum_4bit  # noqa: F401
+from .fileio import (DataError, quantize_file, read_embq, read_embt, write_embq,  # noqa: F401
+                     write_embt)
 
 __version__ = "0.1.0"

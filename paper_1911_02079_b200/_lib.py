@@ -39,6 +39,8 @@ EXPORTS = (
     "eq4_unpack",
     "eq4_quant_mse",
     "eq4_sparse_lengths_sum4",
+    "eq4_quantize_file",
+    "eq4_write_embq",
     "eq4_selftest",
 )
 
@@ -82,6 +84,11 @@ def load() -> ctypes.CDLL:
         L.eq4_quant_mse.restype = i32
         L.eq4_sparse_lengths_sum4.argtypes = [vp, i64, i64, i32, vp, i64, vp, i64, vp, vp, vp, vp]
         L.eq4_sparse_lengths_sum4.restype = i32
+        cp = ctypes.c_char_p
+        L.eq4_quantize_file.argtypes = [cp, cp, i32, i32, dbl, i32, i64, vp, vp]
+        L.eq4_quantize_file.restype = i32
+        L.eq4_write_embq.argtypes = [cp, vp, i64, i64, i32, i32]
+        L.eq4_write_embq.restype = i32
         L.eq4_selftest.argtypes = [i32, i64, ctypes.c_uint64]
         L.eq4_selftest.restype = ctypes.c_longlong
         _lib = L

@@ -1537,6 +1537,28 @@ const char* eq4_version(void) { return "eq4 0.1.0 (sm_100a)"; }
 
 const char* eq4_last_error(void) { return g_err.c_str(); }
 
+int eq4_quantize_file(const char* in_path, const char* out_path, int method, int b, double r,
+                      int aux, int64_t chunk_rows, int64_t* bad_row, double* bad_lohi) {
+  if (!in_path || !out_path) return fail(EQ4_EINVAL, "null path");
+  if (aux != EQ4_AUX_FP16 && aux != EQ4_AUX_FP32) return fail(EQ4_EINVAL, "aux must be fp32 or fp16");
+  if (method != EQ4_METHOD_ASYM && method != EQ4_METHOD_GREEDY && method != EQ4_METHOD_HIST_BRUTE)
+    return fail(EQ4_EINVAL, "unknown method " + std::to_string(method));
+  std::string err;
+  const int rc = eq4_io_quantize_file(in_path, out_path, method, b, r, aux, chunk_rows, bad_row,
+                                      bad_lohi, err);
+  return rc == EQ4_OK ? rc : fail(rc, err);
+}
+
+int eq4_write_embq(const char* path, const uint8_t* packed, int64_t rows, int64_t dim, int aux,
+                   int on_device) {
+  if (!path || !packed) return fail(EQ4_EINVAL, "null buffer");
+  if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "packed table must be at least 1x1");
+  if (aux != EQ4_AUX_FP16 && aux != EQ4_AUX_FP32) return fail(EQ4_EINVAL, "aux must be fp32 or fp16");
+  std::string err;
+  const int rc = eq4_io_write_embq(path, packed, rows, dim, aux, on_device, err);
+  return rc == EQ4_OK ? rc : fail(rc, err);
+}
+
 int eq4_sparse_lengths_sum4(const uint8_t* packed, int64_t rows, int64_t dim, int aux,
                             const int64_t* indices, int64_t nidx, const int64_t* lengths,
                             int64_t batch, float* out, int32_t* status, int64_t* bad_pos,

@@ -15,3 +15,10 @@ int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b
 int eq4_sls_launch(const uint8_t* packed, int64_t rows, int64_t dim, int aux,
                    const int64_t* indices, int64_t nidx, const int64_t* lengths, int64_t batch,
                    float* out, int32_t* status, int64_t* bad_pos, cudaStream_t s, std::string& err);
+
+// EMBT -> EMBQ uniform4 streaming pipeline and the EMBQ writer (eq4_io.cu).
+int eq4_io_quantize_file(const char* in_path, const char* out_path, int method, int b, double r,
+                         int aux, int64_t chunk_rows, int64_t* bad_row, double* bad_lohi,
+                         std::string& err);
+int eq4_io_write_embq(const char* path, const uint8_t* packed, int64_t rows, int64_t dim, int aux,
+                      int on_device, std::string& err);

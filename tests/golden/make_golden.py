@@ -261,8 +261,72 @@ def make_sls():
     print("sls: done", errs)
 
 
+def make_files():
+    """EMBT / EMBQ container bytes and DataError texts (fileio.py) from the reference."""
+    import tempfile
+
+    from embquant import fileio
+
+    out = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        def path(name):
+            return os.path.join(tmp, name)
+
+        x = gaussian_rows(4242, 37, 9)
+        t = eq.EmbeddingTable(x)
+        fileio.write_embt(path("t.embt"), t)
+        out["embt"] = np.frombuffer(open(path("t.embt"), "rb").read(), np.uint8)
+        for name, method, aux in (("greedy_fp16", "greedy", "fp16"), ("asym_fp32", "asym", "fp32"),
+                                  ("hist_fp16", "hist-brute", "fp16")):
+            q = eq.quantize_table(t, method, 4, aux)
+            fileio.write_embq(path(name), q)
+            out["embq_" + name] = np.frombuffer(open(path(name), "rb").read(), np.uint8)
+        good = bytes(out["embt"])
+        cases = {
+            "embt_short": good[:20],
+            "embt_magic": b"EMBX" + good[4:],
+            "embt_version": good[:4] + (2).to_bytes(4, "little") + good[8:],
+            "embt_dtype": good[:24] + b"\x01" + good[25:],
+            "embt_shape": good[:8] + (0).to_bytes(8, "little") + good[16:],
+            "embt_payload": good[:-4],
+            "embt_nonfinite": good[:25] + np.array([np.nan], "<f4").tobytes() + good[29:],
+        }
+        msgs = {}
+        for k, blob in cases.items():
+            with open(path(k), "wb") as fh:
+                fh.write(blob)
+            try:
+                fileio.read_embt(path(k))
+            except fileio.DataError as e:
+                msgs[k] = str(e).replace(tmp, "<dir>")
+            out["bad_" + k] = np.frombuffer(blob, np.uint8)
+        gq = bytes(out["embq_greedy_fp16"])
+        qcases = {
+            "embq_short": gq[:10],
+            "embq_magic": b"EMBT" + gq[4:],
+            "embq_version": gq[:4] + (9).to_bytes(4, "little") + gq[8:],
+            "embq_scheme": gq[:8] + b"\x07" + gq[9:],
+            "embq_aux": gq[:9] + b"\x05" + gq[10:],
+            "embq_shape": gq[:18] + (0).to_bytes(8, "little") + gq[26:],
+            "embq_truncated": gq[:-1],
+            "embq_mismatch": gq + b"\x00",
+        }
+        for k, blob in qcases.items():
+            with open(path(k), "wb") as fh:
+                fh.write(blob)
+            try:
+                fileio.read_embq(path(k))
+            except fileio.DataError as e:
+                msgs[k] = str(e).replace(tmp, "<dir>")
+            out["bad_" + k] = np.frombuffer(blob, np.uint8)
+    out["table"] = x
+    out["messages"] = np.array(json.dumps(msgs))
+    np.savez_compressed(os.path.join(HERE, "files.npz"), **out)
+    print("files: done", len(msgs), "messages")
+
+
 if __name__ == "__main__":
-    which = sys.argv[2:] or ["mse", "edge", "hist", "config1", "sls"]
+    which = sys.argv[2:] or ["mse", "edge", "hist", "config1", "sls", "files"]
     for w in which:
         {"mse": make_mse, "edge": make_edge, "hist": make_hist, "config1": make_config1,
-         "sls": make_sls}[w]()
+         "sls": make_sls, "files": make_files}[w]()
