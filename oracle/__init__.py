@@ -27,7 +27,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "build", "libeq4_oracle.so")
 _lib = None
 
-METHODS = {"asym": 0, "greedy": 1, "hist-brute": 2}
+METHODS = {"asym": 0, "greedy": 1, "hist-brute": 2, "sym": 3, "aciq": 4, "gss": 5, "table": 6}
 AUX = {"fp32": 0, "fp16": 1}
 
 ERRORS = {
@@ -82,6 +82,9 @@ def lib():
         L.eqo_quantize_pack_table.argtypes = [vp, i64, i64, i64, i32, i32, dbl, i32, vp, vp, vp,
                                               vp, vp, vp, i32]
         L.eqo_max_threads.restype = i32
+        L.eqo_clip_range_sym.argtypes = [vp, i64, vp, vp]
+        L.eqo_clip_range_aciq.argtypes = [vp, i64, vp, vp, vp]
+        L.eqo_clip_range_gss.argtypes = [vp, i64, i32, vp, vp, vp, vp]
         L.eqo_sls4.argtypes = [vp, i64, i64, i32, vp, i64, vp, i64, vp, vp]
         _lib = L
     return _lib
@@ -223,7 +226,7 @@ class TableResult:
     packed: np.ndarray     # rows * stride bytes (packed.py layout)
     xmin: np.ndarray       # f64 per row
     xmax: np.ndarray
-    info0: np.ndarray      # greedy: iterations (-1 constant); hist-brute: start_bin
+    info0: np.ndarray      # greedy: iterations (-1 constant); hist-brute: start_bin; gss: evals
     info1: np.ndarray      # greedy: best_i; hist-brute: nbins_selected
     norm: np.ndarray       # hist-brute window norm
 
@@ -260,3 +263,23 @@ def sparse_lengths_sum4(packed, rows: int, d: int, aux: str, indices, lengths):
     rc = lib().eqo_sls4(_p(packed), rows, d, AUX[aux], _p(idx), idx.size, _p(ln), ln.size,
                         _p(out), _p(bad))
     return out, int(rc), int(bad[0])
+
+
+def clip_range_rowwise(x, method: str):
+    """clipping.py sym / aciq (laplacian) / gss (tol 1e-4) for one row -> (lo, hi, evals)."""
+    x = _f32(x)
+    lo, hi = np.zeros(1), np.zeros(1)
+    ev = np.zeros(1, np.int32)
+    scratch = np.empty(max(16, x.size), np.float64)
+    L = lib()
+    if method == "sym":
+        rc = L.eqo_clip_range_sym(_p(x), x.size, _p(lo), _p(hi))
+    elif method == "aciq":
+        rc = L.eqo_clip_range_aciq(_p(x), x.size, _p(scratch), _p(lo), _p(hi))
+    elif method == "gss":
+        rc = L.eqo_clip_range_gss(_p(x), x.size, 4, _p(scratch), _p(lo), _p(hi), _p(ev))
+    else:
+        raise ValueError(method)
+    if rc:
+        raise OracleError(rc)
+    return float(lo[0]), float(hi[0]), int(ev[0])

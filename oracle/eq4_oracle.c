@@ -48,6 +48,10 @@
 #define METHOD_ASYM 0
 #define METHOD_GREEDY 1
 #define METHOD_HIST_BRUTE 2
+#define METHOD_SYM 3
+#define METHOD_ACIQ 4
+#define METHOD_GSS 5
+#define METHOD_TABLE 6
 
 #define DST_NBINS 16 /* histclip.py:31 */
 
@@ -132,6 +136,83 @@ static void row_minmax(const float *x, long d, double *lo, double *hi) {
 int eqo_clip_range_asym(const float *x, long d, double *lo, double *hi) {
     if (d <= 0) return EQO_EEMPTY;
     row_minmax(x, d, lo, hi);
+    return EQO_OK;
+}
+
+/* clipping.py:51-55 clip_range_sym: xmax = max|x| (float64), range (-xmax, xmax). */
+int eqo_clip_range_sym(const float *x, long d, double *lo, double *hi) {
+    if (d <= 0) return EQO_EEMPTY;
+    double m = fabs((double)x[0]);
+    for (long i = 1; i < d; i++) {
+        double a = fabs((double)x[i]);
+        if (a > m) m = a;
+    }
+    *lo = -m;
+    *hi = m;
+    return EQO_OK;
+}
+
+/* clipping.py:115-139 clip_range_aciq, laplacian branch (the one row_clip_range uses):
+ * mean = np.mean(x) (pairwise sum / n), alpha = 5.03 * np.mean(|x - mean|);
+ * alpha == 0 -> the data range.  scratch: d doubles. */
+int eqo_clip_range_aciq(const float *x, long d, double *scratch, double *lo, double *hi) {
+    if (d <= 0) return EQO_EEMPTY;
+    for (long i = 0; i < d; i++) scratch[i] = (double)x[i];
+    const double mean = eqo_np_sum(scratch, d) / (double)d;
+    for (long i = 0; i < d; i++) scratch[i] = fabs((double)x[i] - mean);
+    const double alpha = 5.03 * (eqo_np_sum(scratch, d) / (double)d);
+    if (alpha == 0.0) return eqo_clip_range_asym(x, d, lo, hi);
+    *lo = mean - alpha;
+    *hi = mean + alpha;
+    return EQO_OK;
+}
+
+/* clipping.py:70-112 clip_range_gss (tol = 1e-4): golden-section search over
+ * t in (0, max|x|] of quant_mse(x, (-t, t)), keeping the best point evaluated
+ * (strict <, the unclipped endpoint first).  scratch: d doubles. */
+int eqo_clip_range_gss(const float *x, long d, int nbits, double *scratch, double *lo, double *hi,
+                       int *evals) {
+    if (d <= 0) return EQO_EEMPTY;
+    const double invphi = (sqrt(5.0) - 1.0) / 2.0;          /* clipping.py:27 */
+    const double tol = 1e-4;
+    double tmax = 0.0;
+    eqo_clip_range_sym(x, d, lo, &tmax);
+    int n = 0;
+    if (tmax == 0.0) {
+        *lo = 0.0;
+        *hi = 0.0;
+        if (evals) *evals = 0;
+        return EQO_OK;
+    }
+#define GSS_F(t, out) do { n++; int rc_ = eqo_quant_mse(x, d, -(t), (t), nbits, scratch, &(out)); \
+                           if (rc_) return rc_; } while (0)
+    double best_t = tmax, best_f;
+    GSS_F(tmax, best_f);
+    double a = 0.0, b = tmax;
+    double c = b - invphi * (b - a);
+    double e = a + invphi * (b - a);
+    double fc, fe;
+    GSS_F(c, fc);
+    GSS_F(e, fe);
+    if (fc < best_f) { best_t = c; best_f = fc; }
+    if (fe < best_f) { best_t = e; best_f = fe; }
+    while (b - a > tol * tmax) {
+        if (fc < fe) {
+            b = e; e = c; fe = fc;
+            c = b - invphi * (b - a);
+            GSS_F(c, fc);
+            if (fc < best_f) { best_t = c; best_f = fc; }
+        } else {
+            a = c; c = e; fc = fe;
+            e = a + invphi * (b - a);
+            GSS_F(e, fe);
+            if (fe < best_f) { best_t = e; best_f = fe; }
+        }
+    }
+#undef GSS_F
+    *lo = -best_t;
+    *hi = best_t;
+    if (evals) *evals = n;
     return EQO_OK;
 }
 
@@ -374,7 +455,7 @@ int eqo_quantize_pack_table(const float *x, long rows, long d, long ld, int meth
                             double r, int aux, uint8_t *packed, double *lo_out, double *hi_out,
                             int32_t *info0, int32_t *info1, double *norm_out, int nthreads) {
     if (rows < 1 || d < 1) return EQO_EEMPTY;
-    if (method < 0 || method > 2) return EQO_EMETHOD;
+    if (method < 0 || method > 6) return EQO_EMETHOD;
     if (method == METHOD_GREEDY) {
         if (b < 1) return EQO_EB;
         if (!(0.0 < r && r <= 1.0)) return EQO_ER;
@@ -384,6 +465,18 @@ int eqo_quantize_pack_table(const float *x, long rows, long d, long ld, int meth
         if (check_finite(x + i * ld, d)) return EQO_EFINITE;      /* table.py:28-29 */
     long stride = eqo_packed_row_stride(d, aux);
     int err = 0;
+    double tlo = 0.0, thi = 0.0;                                  /* clipping.py:64-67 table range */
+    if (method == METHOD_TABLE) {
+        float a = x[0], bb = x[0];
+        for (long i = 0; i < rows; i++)
+            for (long k = 0; k < d; k++) {
+                const float v = x[i * ld + k];
+                if (v < a) a = v;
+                if (v > bb) bb = v;
+            }
+        tlo = (double)a;
+        thi = (double)bb;
+    }
     long scratch_n = d > 5 * (long)b ? d : 5 * (long)b;
     if (scratch_n < 16) scratch_n = 16;
 #ifdef _OPENMP
@@ -412,9 +505,18 @@ int eqo_quantize_pack_table(const float *x, long rows, long d, long ld, int meth
                     int bi, bj;
                     rc = eqo_clip_range_greedy(row, d, 4, b, r, &lo, &hi, &a0, &bi, &bj, scratch);
                     a1 = bi;
-                } else {
+                } else if (method == METHOD_HIST_BRUTE) {
                     long ce = 0, bv = 0;
                     rc = eqo_hist_brute(row, d, b, &lo, &hi, &a0, &a1, &nv, &ce, &bv, scratch);
+                } else if (method == METHOD_SYM) {
+                    rc = eqo_clip_range_sym(row, d, &lo, &hi);
+                } else if (method == METHOD_ACIQ) {
+                    rc = eqo_clip_range_aciq(row, d, scratch, &lo, &hi);
+                } else if (method == METHOD_GSS) {
+                    rc = eqo_clip_range_gss(row, d, 4, scratch, &lo, &hi, &a0);
+                } else {
+                    lo = tlo;
+                    hi = thi;
                 }
                 if (!rc) {
                     uint8_t sb[4], bb[4];

@@ -325,8 +325,52 @@ def make_files():
     print("files: done", len(msgs), "messages")
 
 
+def make_methods():
+    """SYM / ACIQ / GSS / TABLE (clipping.py:51-139) end to end: packed bytes, per-row ranges
+    and GSS loss_evals from the reference, on varied tables incl. edge rows."""
+    rng = np.random.default_rng(23)
+    tables = {
+        "gauss64": gaussian_rows(501, 200, 64),
+        "lap64": laplacian_rows(502, 100, 64, 0.3),
+        "mixed17": mixed_table(150, 17, 503),
+        "mixed128": mixed_table(60, 128, 504),
+    }
+    e = rng.standard_normal((12, 9)).astype(np.float32)
+    e[0] = 0.0
+    e[1] = 3.25
+    e[2] = -np.abs(e[2])
+    e[3] *= 1e-30
+    e[4] *= 1e30
+    e[5, :] = [0, 0, 0, 0, 0, 0, 0, 0, 1e-3]
+    e[6] = -0.0
+    tables["edge9"] = e
+    tables["d1"] = rng.standard_normal((7, 1)).astype(np.float32)
+    tables["d2"] = rng.standard_normal((7, 2)).astype(np.float32)
+    out = {}
+    for tname, x in tables.items():
+        out[f"x_{tname}"] = x
+        t = eq.EmbeddingTable(x)
+        for method in ("sym", "aciq", "gss", "table"):
+            for aux in ("fp16", "fp32"):
+                q = eq.quantize_table(t, method, 4, aux)
+                out[f"packed_{tname}_{method}_{aux}"] = eq.pack_table4(q).buffer.copy()
+            if method == "table":
+                cr = eq.clip_range_table(t)
+                out[f"range_{tname}_table"] = np.array([cr.xmin, cr.xmax])
+                continue
+            lo, hi, ev = [], [], []
+            for i in range(t.rows):
+                c = eq.WorkCounters()
+                cr = eq.row_clip_range(method, t.row(i), 4, counters=c)
+                lo.append(cr.xmin); hi.append(cr.xmax); ev.append(c.loss_evals)
+            out[f"range_{tname}_{method}"] = np.array([lo, hi])
+            out[f"evals_{tname}_{method}"] = np.array(ev, np.int64)
+    np.savez_compressed(os.path.join(HERE, "methods.npz"), **out)
+    print("methods: done", len(tables), "tables")
+
+
 if __name__ == "__main__":
-    which = sys.argv[2:] or ["mse", "edge", "hist", "config1", "sls", "files"]
+    which = sys.argv[2:] or ["mse", "edge", "hist", "config1", "sls", "files", "methods"]
     for w in which:
         {"mse": make_mse, "edge": make_edge, "hist": make_hist, "config1": make_config1,
-         "sls": make_sls, "files": make_files}[w]()
+         "sls": make_sls, "files": make_files, "methods": make_methods}[w]()
