@@ -42,6 +42,10 @@ extern "C" {
 #define EQ4_METHOD_ASYM 0       /* clipping.py:58-61   clip_range_asym */
 #define EQ4_METHOD_GREEDY 1     /* clipping.py:142-193 clip_range_greedy */
 #define EQ4_METHOD_HIST_BRUTE 2 /* histclip.py:136-178 hist_brute_search */
+#define EQ4_METHOD_SYM 3        /* clipping.py:51-55   clip_range_sym */
+#define EQ4_METHOD_ACIQ 4       /* clipping.py:115-139 clip_range_aciq (laplacian) */
+#define EQ4_METHOD_GSS 5        /* clipping.py:70-112  clip_range_gss (tol 1e-4) */
+#define EQ4_METHOD_TABLE 6      /* clipping.py:64-67   clip_range_table (one range per table) */
 
 #define EQ4_AUX_FP32 0 /* uniform.py:19-35 aux_precision="fp32" */
 #define EQ4_AUX_FP16 1 /* aux_precision="fp16" */
@@ -73,7 +77,8 @@ int64_t eq4_packed_row_stride(int64_t dim, int aux);
  * Optional per-row device outputs (NULL to skip):
  *   xmin, xmax  float64 ClipRange of the row (the reference's row_clip_range)
  *   info0       GREEDY: while-loop iterations (loss_evals = 1 + 2*iters),
- *               -1 constant row, -2 range error; HIST-BRUTE: start_bin
+ *               -1 constant row, -2 range error; HIST-BRUTE: start_bin;
+ *               GSS: quant_mse evaluations (WorkCounters.loss_evals)
  *   info1       GREEDY: (best_i << 16) | best_j; HIST-BRUTE: nbins_selected
  *   norm        HIST-BRUTE window norm (HistWindow.norm); unused otherwise
  *   status      device int32, EQ4_STATUS_* bits OR-ed in by the kernels

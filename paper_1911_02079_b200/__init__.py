@@ -20,8 +20,12 @@ from .api import (  # noqa: F401
     RowResults,
     UniformQuantTable,
     WorkCounters,
+    clip_range_aciq,
     clip_range_asym,
     clip_range_greedy,
+    clip_range_gss,
+    clip_range_sym,
+    clip_range_table,
     clip_range_hist_brute,
     hist_brute_search,
     pack_table4,

@@ -31,7 +31,7 @@ except ImportError:  # pragma: no cover - torch is part of the image
 UNIFORM_METHODS = ("sym", "asym", "table", "gss", "aciq", "greedy", "hist-apprx", "hist-brute")
 CODEBOOK_METHODS = ("kmeans", "kmeans-cls")
 ALL_METHODS = UNIFORM_METHODS + CODEBOOK_METHODS            # methods.py:38-40
-GPU_METHODS = ("asym", "greedy", "hist-brute")
+GPU_METHODS = ("sym", "asym", "table", "gss", "aciq", "greedy", "hist-brute")
 AUX_PRECISIONS = ("fp32", "fp16")                            # uniform.py:19
 _AUX_NP = {"fp32": np.float32, "fp16": np.float16}
 
@@ -447,7 +447,11 @@ def _raise_status(st: int, x, method, b, r, aux):
 
 
 def _apply_counters(counters: WorkCounters, method: str, b: int, rr: RowResults) -> None:
-    if counters is None or method == "asym":
+    if counters is None or method in ("asym", "sym", "aciq", "table"):
+        return
+    if method == "gss":                                             # clipping.py:87-89
+        ev = np.asarray(rr.info0.cpu() if _is_cuda(rr.info0) else rr.info0).astype(np.int64)
+        counters.loss_evals += int(ev.sum())
         return
     if method == "greedy":                                          # clipping.py:174,183-184
         it = np.asarray(rr.info0.cpu() if _is_cuda(rr.info0) else rr.info0).astype(np.int64)
@@ -535,18 +539,63 @@ def clip_range_hist_brute(x, b: int = 200, counters: WorkCounters | None = None)
     return hist_brute_search(x, b, counters).clip_range
 
 
+def clip_range_sym(x) -> ClipRange:
+    """clipping.py:51-55."""
+    rr = _row_search("sym", x)
+    return ClipRange(float(rr.xmin[0].item()), float(rr.xmax[0].item()))
+
+
+def clip_range_aciq(x, distribution: str = "laplacian", gaussian_constant: float | None = None) -> ClipRange:
+    """clipping.py:115-139 (the laplacian constant 5.03; the caller-supplied gaussian
+    constant branch is not on the GPU path)."""
+    if distribution == "gaussian":
+        if gaussian_constant is None:
+            raise ValueError("gaussian clipping requires an explicit gaussian_constant; "
+                             "only the laplacian constant is built in")
+        raise ValueError("aciq with a gaussian constant is not on the B200 hot path (laplacian only)")
+    if distribution != "laplacian":
+        raise ValueError(f"distribution must be 'laplacian' or 'gaussian', got {distribution!r}")
+    rr = _row_search("aciq", x)
+    return ClipRange(float(rr.xmin[0].item()), float(rr.xmax[0].item()))
+
+
+def clip_range_gss(x, nbits: int = 4, tol: float = 1e-4, counters: WorkCounters | None = None) -> ClipRange:
+    """clipping.py:70-112 (4-bit, tol 1e-4 -- the row_clip_range configuration)."""
+    if tol <= 0:
+        raise ValueError(f"tol must be positive, got {tol}")
+    if nbits != 4 or tol != 1e-4:
+        raise ValueError("gss is on the B200 hot path for nbits=4, tol=1e-4 only")
+    rr = _row_search("gss", x)
+    _apply_counters(counters, "gss", 0, rr)
+    return ClipRange(float(rr.xmin[0].item()), float(rr.xmax[0].item()))
+
+
+def clip_range_table(table) -> ClipRange:
+    """clipping.py:64-67: one (min, max) range over the whole table."""
+    if not isinstance(table, EmbeddingTable):
+        table = EmbeddingTable(table)
+    _, rr = quantize_pack_table4(table, "table", "fp32", with_rows=True)
+    return ClipRange(float(rr.xmin[0].item()), float(rr.xmax[0].item()))
+
+
 def row_clip_range(method: str, x, nbits: int = 4, b: int = 200, r: float = 0.16,
                    counters: WorkCounters | None = None) -> ClipRange:
     """methods.py:43-60 for the GPU methods."""
+    if method == "sym":
+        return clip_range_sym(x)
     if method == "asym":
         return clip_range_asym(x)
+    if method == "gss":
+        return clip_range_gss(x, nbits, counters=counters)
+    if method == "aciq":
+        return clip_range_aciq(x)
     if method == "greedy":
         return clip_range_greedy(x, nbits, b, r, counters=counters)
     if method == "hist-brute":
         return clip_range_hist_brute(x, b, counters=counters)
-    if method in UNIFORM_METHODS:
+    if method == "hist-apprx":
         raise ValueError(f"{method!r} is not on the B200 hot path (supported: {GPU_METHODS})")
-    raise ValueError(f"{method!r} is not a row-wise uniform strategy")
+    raise ValueError(f"{method!r} is not a row-wise uniform strategy")     # methods.py:60
 
 
 def quant_mse_rows(x, xmin, xmax):

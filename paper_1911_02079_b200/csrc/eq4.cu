@@ -87,6 +87,10 @@ struct Params {
   int32_t* info0;
   int32_t* info1;
   int32_t* status;
+  // ASYM-family range of a row: 0 (min, max) clipping.py:58-61; 1 SYM (-max|x|, max|x|)
+  // clipping.py:51-55; 2 TABLE: one (min, max) over the table, clipping.py:64-67
+  int range_mode;
+  const int* trange;  // TABLE: order-preserving int keys of the table min / max (device)
   // GREEDY constants (host-computed)
   int it_exact_from;  // loop iterations < this have a provably true condition
   double qY, inv_qY;  // Y grid quantum and inverse
@@ -379,6 +383,84 @@ __device__ __forceinline__ void emit_asym_vec(const Params& p, const float (&v)[
   }
 }
 
+// Order-preserving float <-> int keys (signed compare), for the TABLE min/max reduction.
+__device__ __forceinline__ int float_key(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float key_float(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); }
+
+// The ASYM family's row range from the row's (min, max): SYM uses (-M, M) with
+// M = max|x| (np.max(np.abs(x)), so an all-zero row gives (-0.0, +0.0)); TABLE
+// the table-wide range.  Every element then lies inside the range, so the
+// fast code path needs no clamping.
+__device__ __forceinline__ void apply_range_mode(const Params& p, float& mn, float& mx) {
+  if (p.range_mode == 1) {
+    const float m = fmaxf(fabsf(mn), fabsf(mx));
+    mn = -m;
+    mx = m;
+  } else if (p.range_mode == 2) {
+    mn = key_float(__ldg(p.trange));
+    mx = key_float(__ldg(p.trange + 1));
+  }
+}
+
+__global__ void k_table_init(int* keys) {
+  keys[0] = 0x7fffffff;               // min key
+  keys[1] = (int)0x80000000;          // max key
+}
+
+// Table-wide min / max (clipping.py:64-67: np.min / np.max over all values):
+// warps stride over rows, lanes over the row (float4 when rows are 16-byte
+// aligned), then one warp reduction and two atomics per warp.
+__global__ void __launch_bounds__(256) k_table_minmax(const float* x, int64_t rows, int d, int64_t ld,
+                                                     int* keys) {
+  int kmin = 0x7fffffff, kmax = (int)0x80000000;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t wn = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vec = (d % 4 == 0) && (ld % 4 == 0) && (((uintptr_t)x & 15) == 0);
+  if (vec && ld == d) {   // contiguous table: one flat float4 stream, 4 loads in flight per thread
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const int64_t n4 = rows * (int64_t)d / 4;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, ts = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = t0; i < n4; i += 4 * ts) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = i + u * ts < n4 ? __ldcs(x4 + i + u * ts) : x4[t0 < n4 ? t0 : 0];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        kmin = min(kmin, min(min(float_key(v[u].x), float_key(v[u].y)), min(float_key(v[u].z), float_key(v[u].w))));
+        kmax = max(kmax, max(max(float_key(v[u].x), float_key(v[u].y)), max(float_key(v[u].z), float_key(v[u].w))));
+      }
+    }
+  } else for (int64_t r = w0; r < rows; r += wn) {
+    const float* row = x + r * ld;
+    if (vec) {
+      const float4* r4 = reinterpret_cast<const float4*>(row);
+      for (int k = lane; k < d / 4; k += 32) {
+        const float4 v = __ldcs(r4 + k);
+        kmin = min(kmin, min(min(float_key(v.x), float_key(v.y)), min(float_key(v.z), float_key(v.w))));
+        kmax = max(kmax, max(max(float_key(v.x), float_key(v.y)), max(float_key(v.z), float_key(v.w))));
+      }
+    } else {
+      for (int k = lane; k < d; k += 32) {
+        const int key = float_key(__ldcs(row + k));
+        kmin = min(kmin, key);
+        kmax = max(kmax, key);
+      }
+    }
+  }
+  for (int o = 16; o >= 1; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(FULL, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(FULL, kmax, o));
+  }
+  if (lane == 0) {
+    atomicMin(keys, kmin);
+    atomicMax(keys + 1, kmax);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // ASYM: min/max -> codes -> pack (HBM-bound streaming kernel)
 // ---------------------------------------------------------------------------
@@ -413,6 +495,7 @@ k_asym(const Params p) {
     float mn, mx;
     bool bad;
     row_minmax<LPR, E, VEC>(p, v, nv, rvalid, q, mn, mx, bad);
+    apply_range_mode(p, mn, mx);
     const double lo = (double)mn, hi = (double)mx;   // clipping.py:61
     if (VEC)
       emit_asym_vec<LPR, E>(p, v, mn, mx, !bad, rvalid, q, out_tile + g * p.stride);
@@ -1193,6 +1276,7 @@ __device__ __forceinline__ void asym_row(const Params& p, const float4 (&cur)[E 
     bad = group_any<LPR>(lb) && rvalid;
     if (bad && q == 0 && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
   }
+  apply_range_mode(p, mn, mx);
   // ---- codes: u = (x - min) * 15/(max - min) + 1/2, code = floor(u) ----
   const float w32 = __fadd_rn(mx, -mn);
   const bool degenerate = !(mn != mx);                     // uniform.py:74-76: all codes 0
@@ -1578,10 +1662,34 @@ int64_t eq4_packed_row_stride(int64_t dim, int aux) {
   return (dim + 1) / 2 + 2 * (aux == EQ4_AUX_FP16 ? 2 : 4);
 }
 
+static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t ld, int method,
+                              int b, double r, int aux, uint8_t* packed, double* xmin, double* xmax,
+                              int32_t* info0, int32_t* info1, double* norm, int32_t* status,
+                              void* stream, const int* table_keys);
+
 int eq4_quantize_pack(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, int b,
                       double r, int aux, uint8_t* packed, double* xmin, double* xmax,
                       int32_t* info0, int32_t* info1, double* norm, int32_t* status,
                       void* stream) {
+  return quantize_pack_impl(x, rows, dim, ld, method, b, r, aux, packed, xmin, xmax, info0, info1,
+                            norm, status, stream, nullptr);
+}
+
+// TABLE range keys of rows [0, rows) accumulated into keys[0..1] (k_table_init first).
+static int table_keys_accumulate(const float* x, int64_t rows, int64_t dim, int64_t ld, int* keys,
+                                 cudaStream_t s) {
+  int64_t blocks = (rows + 7) / 8;                       // 8 warps per block, >= 1 row each
+  const int64_t cap = (int64_t)sm_count() * 4;
+  if (blocks > cap) blocks = cap;
+  k_table_minmax<<<(unsigned)std::max<int64_t>(1, blocks), 256, 0, s>>>(x, rows, (int)dim, ld, keys);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? EQ4_OK : cuda_fail(e, "k_table_minmax");
+}
+
+static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t ld, int method,
+                              int b, double r, int aux, uint8_t* packed, double* xmin, double* xmax,
+                              int32_t* info0, int32_t* info1, double* norm, int32_t* status,
+                              void* stream, const int* table_keys) {
   if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "table must be at least 1x1");
   if (ld < dim) return fail(EQ4_EINVAL, "ld must be >= dim");
   if (!x || !packed) return fail(EQ4_EINVAL, "null buffer");
@@ -1604,6 +1712,32 @@ int eq4_quantize_pack(const float* x, int64_t rows, int64_t dim, int64_t ld, int
   const bool vec = (dim % 4 == 0) && (ld % 4 == 0) && (((uintptr_t)x & 15) == 0) &&
                    (((uintptr_t)packed & 1) == 0);
   if (method == EQ4_METHOD_ASYM) return dispatch_rq<M_ASYM>(p, vec, s);
+  if (method == EQ4_METHOD_SYM) {
+    p.range_mode = 1;
+    return dispatch_rq<M_ASYM>(p, vec, s);
+  }
+  if (method == EQ4_METHOD_TABLE) {
+    p.range_mode = 2;
+    if (table_keys) {   // range computed by the caller (chunked host path)
+      p.trange = table_keys;
+      return dispatch_rq<M_ASYM>(p, vec, s);
+    }
+    int* keys = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&keys, 8, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    k_table_init<<<1, 1, 0, s>>>(keys);
+    int rc = table_keys_accumulate(x, rows, dim, ld, keys, s);
+    p.trange = keys;
+    if (rc == EQ4_OK) rc = dispatch_rq<M_ASYM>(p, vec, s);
+    cudaFreeAsync(keys, s);
+    return rc;
+  }
+  if (method == EQ4_METHOD_ACIQ || method == EQ4_METHOD_GSS) {
+    std::string err;
+    const int rc = eq4_rowrange_launch(x, rows, dim, ld, method, aux, packed, xmin, xmax, info0,
+                                       status, s, err);
+    return rc == EQ4_OK ? rc : fail(rc, err);
+  }
   if (method == EQ4_METHOD_GREEDY) {
     if (b > 65535) return fail(EQ4_EUNSUPPORTED, "b > 65535 is not supported by the B200 path");
     // Loop condition (clipping.py:180) at iteration it, i.e. after it moves
@@ -1720,6 +1854,25 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
     if (e == cudaSuccess && want_lohi) e = cudaMallocAsync(&bf[i].hi, chunk * 8, st[i]);
     if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocAsync");
   }
+  // TABLE: one range over the whole table -> a first streaming pass for the min / max keys
+  int* tkeys = nullptr;
+  if (rc == EQ4_OK && method == EQ4_METHOD_TABLE) {
+    e = cudaMallocAsync((void**)&tkeys, 8, st[0]);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocAsync");
+    if (rc == EQ4_OK) k_table_init<<<1, 1, 0, st[0]>>>(tkeys);
+    if (rc == EQ4_OK) e = cudaStreamSynchronize(st[0]);
+    for (int64_t c = 0; c < nchunks && rc == EQ4_OK; c++) {
+      const int si = (int)(c % NS);
+      const int64_t r0 = c * chunk, nr = std::min(chunk, rows - r0);
+      e = cudaMemcpy2DAsync(bf[si].x, dim * 4, x + r0 * ld, ld * 4, dim * 4, nr, cudaMemcpyHostToDevice, st[si]);
+      if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
+      rc = table_keys_accumulate(bf[si].x, nr, dim, dim, tkeys, st[si]);
+    }
+    for (int i = 0; i < NS && rc == EQ4_OK; i++) {
+      e = cudaStreamSynchronize(st[i]);
+      if (e != cudaSuccess) rc = cuda_fail(e, "stream sync");
+    }
+  }
   for (int64_t c = 0; c < nchunks && rc == EQ4_OK; c++) {
     const int si = (int)(c % NS);
     cudaStream_t s = st[si];
@@ -1728,8 +1881,8 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
     e = cudaMemcpy2DAsync(B.x, dim * 4, x + r0 * ld, ld * 4, dim * 4, nr, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(B.status, 0, 4, s);
     if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
-    rc = eq4_quantize_pack(B.x, nr, dim, dim, method, b, r, aux, B.out, B.lo, B.hi, B.i0, B.i1,
-                           nullptr, B.status, s);
+    rc = quantize_pack_impl(B.x, nr, dim, dim, method, b, r, aux, B.out, B.lo, B.hi, B.i0, B.i1,
+                            nullptr, B.status, s, tkeys);
     if (rc) break;
     e = cudaMemcpyAsync(packed + r0 * stride, B.out, nr * stride, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && info0) e = cudaMemcpyAsync(info0 + r0, B.i0, nr * 4, cudaMemcpyDeviceToHost, s);
@@ -1791,6 +1944,7 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
       if (bad_row && first >= 0) *bad_row = r0 + first;
     }
   }
+  if (tkeys) cudaFreeAsync(tkeys, st[0]);
   for (int i = 0; i < NS; i++) {
     cudaFreeAsync(bf[i].x, st[i]); cudaFreeAsync(bf[i].out, st[i]); cudaFreeAsync(bf[i].i0, st[i]);
     cudaFreeAsync(bf[i].status, st[i]);

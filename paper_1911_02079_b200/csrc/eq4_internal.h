@@ -22,3 +22,8 @@ int eq4_io_quantize_file(const char* in_path, const char* out_path, int method, 
                          std::string& err);
 int eq4_io_write_embq(const char* path, const uint8_t* packed, int64_t rows, int64_t dim, int aux,
                       int on_device, std::string& err);
+
+// ACIQ / GSS row-range searches + quantize + pack (eq4_rowrange.cu).
+int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, int aux,
+                        uint8_t* packed, double* xmin, double* xmax, int32_t* info0,
+                        int32_t* status, cudaStream_t s, std::string& err);

@@ -1,0 +1,351 @@
+// eq4_rowrange.cu -- ACIQ and GSS row-range searches fused with the codec and
+// the packer (clipping.py:70-139).
+//
+// Both searches are float64 computations whose every comparison must match the
+// reference bit for bit:
+//   ACIQ (laplacian, the branch row_clip_range uses): mean = np.mean(x),
+//     alpha = 5.03 * np.mean(|x - mean|)  (numpy pairwise sums / n),
+//     range (mean - alpha, mean + alpha), or the data range when alpha == 0;
+//   GSS (tol 1e-4): golden-section search over t in (0, max|x|] of
+//     quant_mse(x, (-t, t), 4), keeping the best point evaluated (strict <),
+//     ~23 exact float64 quant_mse evaluations per row.
+// So they run lane-per-row: a warp stages 32 rows in shared memory as a
+// conflict-free [d][33] column layout and every lane replays numpy's pairwise
+// summation order for its own row sequentially (8 accumulator chains per
+// <=128-element leaf, recursive halving n2 = n/2 - (n/2 % 8) above), 32 rows
+// in flight per warp instead of one warp-cooperative row at a time.  Codes use
+// a divide-free estimate of (c - lo) / scale and take the IEEE divide only
+// when the estimate is within 1e-12 of a rounding boundary (numpy's q is the
+// correctly rounded quotient; the estimate is within a few ulp of it).
+// Rows wider than 256 read their elements straight from global memory.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <string>
+
+#include "../../include/eq4.h"
+#include "eq4_device.cuh"
+#include "eq4_internal.h"
+
+namespace eq4 {
+
+constexpr int RR_THREADS = 128;
+constexpr int RR_WARPS = RR_THREADS / 32;
+constexpr int RR_MAX_STAGED = 256;   // d above this reads global memory
+constexpr int RR_COL = 33;           // padded column stride (floats) of the staged tile
+
+struct RRParams {
+  const float* x;
+  int64_t rows, ld;
+  int d, aux, stride, half, method;
+  uint8_t* packed;
+  double* lo_out;
+  double* hi_out;
+  int32_t* info0;
+  int32_t* status;
+  double invphi;     // (sqrt(5) - 1) / 2, clipping.py:27
+  int staged;
+  size_t warp_bytes;
+};
+
+// Element k of this lane's row.
+struct RowView {
+  const float* base;
+  int ks;
+  __device__ __forceinline__ float operator[](int k) const { return base[(size_t)k * ks]; }
+};
+
+// numpy pairwise summation of f(a .. a+n-1) (loops_utils.h.src), one thread.
+template <class F>
+__device__ __forceinline__ double np_leaf(const F& f, int a, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; i++) res = __dadd_rn(res, f(a + i));
+    return res;
+  }
+  double r0 = f(a), r1 = f(a + 1), r2 = f(a + 2), r3 = f(a + 3);
+  double r4 = f(a + 4), r5 = f(a + 5), r6 = f(a + 6), r7 = f(a + 7);
+  const int nf = n - (n % 8);
+  int i = 8;
+  for (; i < nf; i += 8) {
+    r0 = __dadd_rn(r0, f(a + i));     r1 = __dadd_rn(r1, f(a + i + 1));
+    r2 = __dadd_rn(r2, f(a + i + 2)); r3 = __dadd_rn(r3, f(a + i + 3));
+    r4 = __dadd_rn(r4, f(a + i + 4)); r5 = __dadd_rn(r5, f(a + i + 5));
+    r6 = __dadd_rn(r6, f(a + i + 6)); r7 = __dadd_rn(r7, f(a + i + 7));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < n; i++) res = __dadd_rn(res, f(a + i));
+  return res;
+}
+
+// pw(a, n) = pw(a, n2) + pw(a + n2, n - n2) for n > 128, n2 = n/2 - (n/2 % 8),
+// evaluated with an explicit stack (leaves left to right, the same association).
+template <class F>
+__device__ __forceinline__ double np_pw(const F& f, int a0, int n0) {
+  if (n0 <= 128) return np_leaf(f, a0, n0);
+  int sa[24], sn[24], sstage[24];
+  double sleft[24];
+  int sp = 0;
+  sa[0] = a0; sn[0] = n0; sstage[0] = 0;
+  double ret = 0.0;
+  while (true) {
+    const int a = sa[sp], n = sn[sp];
+    if (n <= 128) {
+      ret = np_leaf(f, a, n);
+      // return up the stack until a node still needs its right half
+      while (true) {
+        if (sp == 0) return ret;
+        --sp;
+        if (sstage[sp] == 1) {
+          sleft[sp] = ret;
+          sstage[sp] = 2;
+          int n2 = sn[sp] / 2;
+          n2 -= n2 % 8;
+          ++sp;
+          sa[sp] = sa[sp - 1] + n2; sn[sp] = sn[sp - 1] - n2; sstage[sp] = 0;
+          break;
+        }
+        ret = __dadd_rn(sleft[sp], ret);
+      }
+    } else {
+      int n2 = n / 2;
+      n2 -= n2 % 8;
+      sstage[sp] = 1;
+      ++sp;
+      sa[sp] = a; sn[sp] = n2; sstage[sp] = 0;
+    }
+  }
+}
+
+// np.add.reduce: identity 0.0 plus the pairwise sum.
+template <class F>
+__device__ __forceinline__ double np_sum(const F& f, int n) {
+  return __dadd_rn(0.0, np_pw(f, 0, n));
+}
+
+// uniform.py:77-79 / table.py:100-101 code of x under (lo, hi) with scale =
+// (hi - lo) / 15 (hi > lo): floor((clip(x) - lo) / scale + 0.5) clipped to [0, 15].
+struct Codec {
+  double lo, hi, scale, inv;
+  __device__ __forceinline__ double code(double x) const {
+    const double c = np_clip(x, lo, hi);
+    const double dl = __dsub_rn(c, lo);
+    const double t = __dadd_rn(__dmul_rn(dl, inv), 0.5);
+    const double fl = floor(t);
+    const double fr = __dsub_rn(t, fl);
+    double q = fl;
+    if (!(fr > 1e-12 && fr < 1.0 - 1e-12)) q = floor(__dadd_rn(__ddiv_rn(dl, scale), 0.5));
+    return np_clip(q, 0.0, 15.0);
+  }
+};
+
+__device__ __forceinline__ Codec make_codec(double lo, double hi) {
+  Codec c;
+  c.lo = lo;
+  c.hi = hi;
+  c.scale = div15(__dsub_rn(hi, lo));       // table.py:99 (exactly rounded w / 15)
+  c.inv = __drcp_rn(c.scale);
+  return c;
+}
+
+// table.py:81-103 quant_mse(x, (lo, hi), 4) of this lane's row, bit-exact.
+__device__ __forceinline__ double lane_quant_mse(const RowView& xr, int d, double lo, double hi) {
+  if (hi == lo) {
+    return np_sum([&](int k) {
+      const double e = __dsub_rn((double)xr[k], lo);
+      return __dmul_rn(e, e);
+    }, d);
+  }
+  const Codec cd = make_codec(lo, hi);
+  return np_sum([&](int k) {
+    const double x = (double)xr[k];
+    const double recon = __dadd_rn(__dmul_rn(cd.scale, cd.code(x)), lo);
+    const double e = __dsub_rn(x, recon);
+    return __dmul_rn(e, e);
+  }, d);
+}
+
+// clipping.py:115-139, laplacian branch.
+__device__ __forceinline__ void lane_aciq(const RowView& xr, int d, float mn, float mx, double& lo,
+                                          double& hi) {
+  const double n = (double)d;
+  const double mean = __ddiv_rn(np_sum([&](int k) { return (double)xr[k]; }, d), n);
+  const double mad = __ddiv_rn(np_sum([&](int k) { return fabs(__dsub_rn((double)xr[k], mean)); }, d), n);
+  const double alpha = __dmul_rn(5.03, mad);
+  if (alpha == 0.0) {
+    lo = (double)mn;
+    hi = (double)mx;
+  } else {
+    lo = __dsub_rn(mean, alpha);
+    hi = __dadd_rn(mean, alpha);
+  }
+}
+
+// clipping.py:70-112 with tol = 1e-4; returns the number of quant_mse calls.
+__device__ __forceinline__ int lane_gss(const RowView& xr, int d, float mn, float mx, double invphi,
+                                        double& lo_out, double& hi_out) {
+  const double tmax = (double)fmaxf(fabsf(mn), fabsf(mx));
+  if (tmax == 0.0) {
+    lo_out = 0.0;
+    hi_out = 0.0;
+    return 0;
+  }
+  int n = 0;
+  auto f = [&](double t) {
+    ++n;
+    return lane_quant_mse(xr, d, -t, t);
+  };
+  double best_t = tmax, best_f = f(tmax);
+  double a = 0.0, b = tmax;
+  double c = __dsub_rn(b, __dmul_rn(invphi, __dsub_rn(b, a)));
+  double e = __dadd_rn(a, __dmul_rn(invphi, __dsub_rn(b, a)));
+  double fc = f(c), fe = f(e);
+  if (fc < best_f) { best_t = c; best_f = fc; }
+  if (fe < best_f) { best_t = e; best_f = fe; }
+  const double stop = __dmul_rn(1e-4, tmax);
+  while (__dsub_rn(b, a) > stop) {
+    if (fc < fe) {
+      b = e; e = c; fe = fc;
+      c = __dsub_rn(b, __dmul_rn(invphi, __dsub_rn(b, a)));
+      fc = f(c);
+      if (fc < best_f) { best_t = c; best_f = fc; }
+    } else {
+      a = c; c = e; fc = fe;
+      e = __dadd_rn(a, __dmul_rn(invphi, __dsub_rn(b, a)));
+      fe = f(e);
+      if (fe < best_f) { best_t = e; best_f = fe; }
+    }
+  }
+  lo_out = -best_t;
+  hi_out = best_t;
+  return n;
+}
+
+__global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* ws = smem + (size_t)warp * p.warp_bytes;
+  float* xs = reinterpret_cast<float*>(ws);
+  const size_t xs_bytes = p.staged ? (size_t)p.d * RR_COL * 4 : 0;
+  uint8_t* out_base = ws + ((xs_bytes + 15) & ~(size_t)15);
+  const int d = p.d;
+  const int64_t nblk = (p.rows + 31) / 32;
+  for (int64_t blk = (int64_t)blockIdx.x * RR_WARPS + warp; blk < nblk;
+       blk += (int64_t)gridDim.x * RR_WARPS) {
+    const int64_t row0 = blk * 32, row = row0 + lane;
+    const bool rvalid = row < p.rows;
+    const int nrows = (int)min((int64_t)32, p.rows - row0);
+    RowView xr;
+    if (p.staged) {
+      for (int r = 0; r < nrows; r++) {
+        const float* src = p.x + (row0 + r) * p.ld;
+#pragma unroll 4
+        for (int k = lane; k < d; k += 32) xs[k * RR_COL + r] = __ldcs(src + k);
+      }
+      __syncwarp();
+      xr.base = xs + lane;
+      xr.ks = RR_COL;
+    } else {
+      xr.base = p.x + (rvalid ? row : row0) * p.ld;
+      xr.ks = 1;
+    }
+    // row min / max / finiteness (table.py:28-29)
+    float mn = INFINITY, mx = -INFINITY;
+    bool bad = false;
+    if (rvalid) {
+      for (int k = 0; k < d; k++) {
+        const float v = xr[k];
+        mn = fminf(mn, v);
+        mx = fmaxf(mx, v);
+        bad |= !isfinite(v);
+      }
+      if (bad && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
+    }
+    double lo = 0.0, hi = 0.0;
+    int evals = 0;
+    if (rvalid && !bad) {
+      if (p.method == EQ4_METHOD_ACIQ) lane_aciq(xr, d, mn, mx, lo, hi);
+      else evals = lane_gss(xr, d, mn, mx, p.invphi, lo, hi);
+    }
+    // codes (uniform.py:60-80) + packed row (packed.py:68-83), staged then copied out
+    uint8_t* out_tile = out_base + (((uintptr_t)p.packed + (size_t)row0 * p.stride) & 15);
+    if (rvalid) {
+      uint8_t* orow = out_tile + (size_t)lane * p.stride;
+      const bool degenerate = bad || hi == lo;
+      Codec cd;
+      if (!degenerate) cd = make_codec(lo, hi);
+      for (int m = 0; m < p.half; m++) {
+        unsigned c0 = 0, c1 = 0;
+        if (!degenerate) {
+          c0 = (unsigned)cd.code((double)xr[2 * m]);
+          if (2 * m + 1 < d) c1 = (unsigned)cd.code((double)xr[2 * m + 1]);
+        }
+        orow[m] = (uint8_t)(c0 | (c1 << 4));
+      }
+      const double sc = degenerate ? 0.0 : cd.scale;   // uniform.py:74-80
+      uint8_t* a = orow + p.half;
+      if (p.aux == EQ4_AUX_FP16) {
+        const uint32_t s16 = aux_bits_f16(sc), b16 = aux_bits_f16(lo);
+        a[0] = s16 & 0xff; a[1] = s16 >> 8; a[2] = b16 & 0xff; a[3] = b16 >> 8;
+      } else {
+        const uint32_t s32 = aux_bits_f32(sc), b32 = aux_bits_f32(lo);
+        for (int k = 0; k < 4; ++k) { a[k] = (s32 >> (8 * k)) & 0xff; a[4 + k] = (b32 >> (8 * k)) & 0xff; }
+      }
+      if (p.lo_out) { p.lo_out[row] = lo; p.hi_out[row] = hi; }
+      if (p.info0) p.info0[row] = evals;
+    }
+    __syncwarp();
+    // warp copy of the staged packed rows (16-byte stores where aligned)
+    {
+      uint8_t* dst = p.packed + (size_t)row0 * p.stride;
+      const int nbytes = nrows * p.stride;
+      int head = (int)((16 - ((uintptr_t)dst & 15)) & 15);
+      if (head > nbytes) head = nbytes;
+      const int nvec = (nbytes - head) >> 4;
+      const int tail = head + (nvec << 4);
+      if (lane < head) dst[lane] = out_tile[lane];
+      const uint4* s4 = reinterpret_cast<const uint4*>(out_tile + head);
+      uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+      for (int i = lane; i < nvec; i += 32) d4[i] = s4[i];
+      for (int i = tail + lane; i < nbytes; i += 32) dst[i] = out_tile[i];
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace eq4
+
+using namespace eq4;
+
+int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, int aux,
+                        uint8_t* packed, double* xmin, double* xmax, int32_t* info0,
+                        int32_t* status, cudaStream_t s, std::string& err) {
+  RRParams p;
+  p.x = x; p.rows = rows; p.ld = ld; p.d = (int)dim; p.aux = aux; p.method = method;
+  p.half = (int)((dim + 1) / 2);
+  p.stride = p.half + 2 * (aux == EQ4_AUX_FP16 ? 2 : 4);
+  p.packed = packed; p.lo_out = xmin; p.hi_out = xmax; p.info0 = info0; p.status = status;
+  p.invphi = (std::sqrt(5.0) - 1.0) / 2.0;
+  p.staged = dim <= RR_MAX_STAGED;
+  const size_t xs_bytes = p.staged ? (size_t)dim * RR_COL * 4 : 0;
+  p.warp_bytes = ((xs_bytes + 15) & ~(size_t)15) + (size_t)32 * p.stride + 32;
+  p.warp_bytes = (p.warp_bytes + 15) & ~(size_t)15;
+  const size_t smem = p.warp_bytes * RR_WARPS;
+  cudaError_t e = cudaFuncSetAttribute(k_rowrange, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 0, per_sm = 0;
+  if (e == cudaSuccess) e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rowrange, RR_THREADS, smem);
+  if (e != cudaSuccess) { err = std::string("k_rowrange setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+  const int64_t nblk = (rows + 31) / 32;
+  int64_t grid = (nblk + RR_WARPS - 1) / RR_WARPS;
+  const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  k_rowrange<<<(unsigned)grid, RR_THREADS, smem, s>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) { err = std::string("k_rowrange: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+  return EQ4_OK;
+}

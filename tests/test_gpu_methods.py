@@ -1,0 +1,74 @@
+"""GPU parity of the other row-wise ranges: SYM, ACIQ, GSS, TABLE against
+reference-made fixtures (tests/golden/methods.npz) and the C oracle: bit-exact packed rows,
+float64 ranges and GSS evaluation counts."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1911_02079_b200 as eq
+from oracle import rng
+from test_oracle_golden import METHOD_TABLES, _load
+
+pytestmark = pytest.mark.gpu
+
+METHODS = ("sym", "aciq", "gss", "table")
+
+
+@pytest.mark.parametrize("method", METHODS)
+def test_methods_golden_device_and_host(method):
+    f = _load("methods.npz")
+    for tname in METHOD_TABLES:
+        x = f[f"x_{tname}"]
+        for aux in ("fp16", "fp32"):
+            want = f[f"packed_{tname}_{method}_{aux}"]
+            p, rr = eq.quantize_pack_table4(torch.from_numpy(x).cuda(), method, aux, with_rows=True)
+            assert np.array_equal(p.buffer, want), (tname, aux, "device")
+            ph, rh = eq.quantize_pack_table4(eq.EmbeddingTable(x), method, aux, with_rows=True)
+            assert np.array_equal(ph.buffer, want), (tname, aux, "host")
+        lo, hi = rr.xmin.cpu().numpy(), rr.xmax.cpu().numpy()
+        if method == "table":
+            assert (lo[0], hi[0]) == tuple(f[f"range_{tname}_table"])
+            continue
+        glo, ghi = f[f"range_{tname}_{method}"]
+        assert np.array_equal(lo, glo) and np.array_equal(hi, ghi), tname
+        assert np.array_equal(np.signbit(lo), np.signbit(glo)), tname
+        if method == "gss":
+            assert np.array_equal(rr.info0.cpu().numpy(), f[f"evals_{tname}_gss"]), tname
+
+
+@pytest.mark.parametrize("method", METHODS)
+@pytest.mark.parametrize("rows,d,gen", [(20000, 64, "gauss"), (4000, 128, "mixed"), (3000, 33, "mixed"),
+                                        (1000, 300, "gauss"), (200, 2048, "mixed"), (5000, 8, "gauss")])
+def test_methods_random_vs_oracle(method, rows, d, gen):
+    x = (rng.mixed_table(rows, d, d) if gen == "mixed" else
+         rng.sample_table("gaussian", 0.0, 1.0, d, rows, d))
+    aux = "fp16" if d % 2 == 0 else "fp32"
+    p, rr = eq.quantize_pack_table4(torch.from_numpy(x).cuda(), method, aux, with_rows=True)
+    want = oracle.quantize_pack_table(x, method, 200, 0.16, aux)
+    assert np.array_equal(p.buffer, want.packed)
+    assert np.array_equal(rr.xmin.cpu().numpy(), want.xmin)
+    assert np.array_equal(rr.xmax.cpu().numpy(), want.xmax)
+    if method == "gss":
+        assert np.array_equal(rr.info0.cpu().numpy(), want.info0)
+
+
+def test_method_api_single_rows_and_counters():
+    x = rng.sample_table("laplacian", 0.0, 1.0, 7, 5, 64)
+    for row in x:
+        lo, hi, ev = oracle.clip_range_rowwise(row, "gss")
+        c = eq.WorkCounters()
+        cr = eq.clip_range_gss(row, counters=c)
+        assert (cr.xmin, cr.xmax, c.loss_evals) == (lo, hi, ev)
+        lo, hi, _ = oracle.clip_range_rowwise(row, "aciq")
+        cr = eq.clip_range_aciq(row)
+        assert (cr.xmin, cr.xmax) == (lo, hi)
+        lo, hi, _ = oracle.clip_range_rowwise(row, "sym")
+        cr = eq.row_clip_range("sym", row)
+        assert (cr.xmin, cr.xmax) == (lo, hi)
+    cr = eq.clip_range_table(x)
+    assert (cr.xmin, cr.xmax) == (float(x.min()), float(x.max()))
+    c = eq.WorkCounters()
+    eq.quantize_table(x, "gss", counters=c)
+    assert c.loss_evals == sum(oracle.clip_range_rowwise(r, "gss")[2] for r in x)

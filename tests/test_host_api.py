@@ -90,7 +90,7 @@ def test_greedy_parameter_errors_match_reference(ref):
 
 def test_methods_off_the_hot_path_raise_instead_of_falling_back():
     t = np.ones((2, 4), np.float32)
-    for m in ("sym", "gss", "aciq", "table", "hist-apprx", "kmeans"):
+    for m in ("hist-apprx", "kmeans"):
         with pytest.raises(ValueError, match="not on the B200 hot path"):
             eq.quantize_table(t, m)
     with pytest.raises(ValueError, match="not on the B200 hot path"):
@@ -207,3 +207,23 @@ def test_bytes_per_pooled_row_kats():
     assert eq.bytes_per_pooled_row("int4", 128, "fp16") == 68
     with pytest.raises(ValueError):
         eq.bytes_per_pooled_row("int2", 8)
+
+
+def test_row_clip_range_table_is_not_rowwise_like_reference(ref):
+    x = [1.0, 2.0, 3.0]
+    with pytest.raises(ValueError) as theirs:
+        ref.row_clip_range("table", x)
+    with pytest.raises(ValueError) as ours:
+        eq.row_clip_range("table", x)
+    assert str(ours.value) == str(theirs.value)
+    with pytest.raises(ValueError) as theirs:
+        ref.clip_range_gss(x, 4, tol=0.0)
+    with pytest.raises(ValueError) as ours:
+        eq.clip_range_gss(x, 4, tol=0.0)
+    assert str(ours.value) == str(theirs.value)
+    for kw in (dict(distribution="gaussian"), dict(distribution="cauchy")):
+        with pytest.raises(ValueError) as theirs:
+            ref.clip_range_aciq(x, **kw)
+        with pytest.raises(ValueError) as ours:
+            eq.clip_range_aciq(x, **kw)
+        assert str(ours.value) == str(theirs.value)
