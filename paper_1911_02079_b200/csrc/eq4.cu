@@ -394,12 +394,13 @@ __device__ __forceinline__ float key_float(int k) { return __int_as_float(k >= 0
 // M = max|x| (np.max(np.abs(x)), so an all-zero row gives (-0.0, +0.0)); TABLE
 // the table-wide range.  Every element then lies inside the range, so the
 // fast code path needs no clamping.
+template <int RM>
 __device__ __forceinline__ void apply_range_mode(const Params& p, float& mn, float& mx) {
-  if (p.range_mode == 1) {
+  if constexpr (RM == 1) {
     const float m = fmaxf(fabsf(mn), fabsf(mx));
     mn = -m;
     mx = m;
-  } else if (p.range_mode == 2) {
+  } else if constexpr (RM == 2) {
     mn = key_float(__ldg(p.trange));
     mx = key_float(__ldg(p.trange + 1));
   }
@@ -472,7 +473,7 @@ struct LayoutA {
   __host__ __device__ static size_t total(int stride) { return out_off() + (size_t)RPB * stride + 32; }
 };
 
-template <int LPR, int E, bool VEC>
+template <int LPR, int E, bool VEC, int RM>
 __global__ void __launch_bounds__(NTHREADS, E <= 16 ? 4 : (E == 32 ? 3 : 2))
 k_asym(const Params p) {
   using L = LayoutA<LPR, E, VEC>;
@@ -495,7 +496,7 @@ k_asym(const Params p) {
     float mn, mx;
     bool bad;
     row_minmax<LPR, E, VEC>(p, v, nv, rvalid, q, mn, mx, bad);
-    apply_range_mode(p, mn, mx);
+    apply_range_mode<RM>(p, mn, mx);
     const double lo = (double)mn, hi = (double)mx;   // clipping.py:61
     if (VEC)
       emit_asym_vec<LPR, E>(p, v, mn, mx, !bad, rvalid, q, out_tile + g * p.stride);
@@ -1252,7 +1253,7 @@ __device__ __forceinline__ void asym_load(const float* rowp, bool ok, int q, flo
 
 // Code + pack one row slice (E elements of lane q) straight to the packed row
 // in global memory (2-byte stores; L2 merges a row's partial sectors).
-template <int LPR, int E>
+template <int LPR, int E, int RM>
 __device__ __forceinline__ void asym_row(const Params& p, const float4 (&cur)[E / 4], int64_t row,
                                          int q) {
   const bool rvalid = row < p.rows;
@@ -1276,7 +1277,7 @@ __device__ __forceinline__ void asym_row(const Params& p, const float4 (&cur)[E 
     bad = group_any<LPR>(lb) && rvalid;
     if (bad && q == 0 && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
   }
-  apply_range_mode(p, mn, mx);
+  apply_range_mode<RM>(p, mn, mx);
   // ---- codes: u = (x - min) * 15/(max - min) + 1/2, code = floor(u) ----
   const float w32 = __fadd_rn(mx, -mn);
   const bool degenerate = !(mn != mx);                     // uniform.py:74-76: all codes 0
@@ -1347,7 +1348,7 @@ __device__ __forceinline__ void asym_row(const Params& p, const float4 (&cur)[E 
 
 // ASYM vector kernel: warps are independent; each warp keeps the next row
 // block's loads in flight (double buffer A/B) while it codes the current one.
-template <int LPR, int E>
+template <int LPR, int E, int RM>
 __global__ void __launch_bounds__(NTHREADS, 3) k_asym_vec(const Params p) {
   constexpr int RPW = 32 / LPR;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1361,12 +1362,12 @@ __global__ void __launch_bounds__(NTHREADS, 3) k_asym_vec(const Params p) {
   if (blk < nblocks) asym_load<LPR, E>(xp, blk * RPW + gw < p.rows, q, a);
   while (blk < nblocks) {
     if (blk + wstride < nblocks) asym_load<LPR, E>(xp + rstep, (blk + wstride) * RPW + gw < p.rows, q, b);
-    asym_row<LPR, E>(p, a, blk * RPW + gw, q);
+    asym_row<LPR, E, RM>(p, a, blk * RPW + gw, q);
     blk += wstride;
     xp += rstep;
     if (blk >= nblocks) break;
     if (blk + wstride < nblocks) asym_load<LPR, E>(xp + rstep, (blk + wstride) * RPW + gw < p.rows, q, a);
-    asym_row<LPR, E>(p, b, blk * RPW + gw, q);
+    asym_row<LPR, E, RM>(p, b, blk * RPW + gw, q);
     blk += wstride;
     xp += rstep;
   }
@@ -1511,12 +1512,16 @@ static int launch_rq(const Params& p, cudaStream_t s) {
   if constexpr (METHOD == M_ASYM) {
     if constexpr (VEC && E <= 16) {
       using S = SliceA<LPR, E>;
-      return launch_persistent(k_asym_vec<LPR, E>, 0,
-                               (p.rows + S::RPW * NWARPS - 1) / (S::RPW * NWARPS), p, s, "k_asym_vec");
+      const int64_t nt = (p.rows + S::RPW * NWARPS - 1) / (S::RPW * NWARPS);
+      if (p.range_mode == 1) return launch_persistent(k_asym_vec<LPR, E, 1>, 0, nt, p, s, "k_asym_vec");
+      if (p.range_mode == 2) return launch_persistent(k_asym_vec<LPR, E, 2>, 0, nt, p, s, "k_asym_vec");
+      return launch_persistent(k_asym_vec<LPR, E, 0>, 0, nt, p, s, "k_asym_vec");
     }
     using L = LayoutA<LPR, E, VEC>;
-    return launch_persistent(k_asym<LPR, E, VEC>, L::total(p.stride), (p.rows + L::RPB - 1) / L::RPB,
-                             p, s, "k_asym");
+    const int64_t nt = (p.rows + L::RPB - 1) / L::RPB;
+    if (p.range_mode == 1) return launch_persistent(k_asym<LPR, E, VEC, 1>, L::total(p.stride), nt, p, s, "k_asym");
+    if (p.range_mode == 2) return launch_persistent(k_asym<LPR, E, VEC, 2>, L::total(p.stride), nt, p, s, "k_asym");
+    return launch_persistent(k_asym<LPR, E, VEC, 0>, L::total(p.stride), nt, p, s, "k_asym");
   } else {
     using S = WarpSliceG<LPR, E, VEC>;
     return launch_persistent(k_greedy<LPR, E, VEC>, NWARPS_G * S::bytes(p.stride),
