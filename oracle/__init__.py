@@ -27,7 +27,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "build", "libeq4_oracle.so")
 _lib = None
 
-METHODS = {"asym": 0, "greedy": 1, "hist-brute": 2, "sym": 3, "aciq": 4, "gss": 5, "table": 6}
+METHODS = {"asym": 0, "greedy": 1, "hist-brute": 2, "sym": 3, "aciq": 4, "gss": 5, "table": 6,
+           "hist-apprx": 7}
 AUX = {"fp32": 0, "fp16": 1}
 
 ERRORS = {
@@ -74,6 +75,8 @@ def lib():
         L.eqo_bin_l2_norm.restype = dbl
         L.eqo_offset_unit_norms.argtypes = [vp, i64, dbl, dbl, vp]
         L.eqo_hist_brute.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.eqo_kmeans_table.argtypes = [vp, i64, i64, i64, i32, vp, vp, vp, i32]
+        L.eqo_hist_apprx.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp]
         L.eqo_hist_window_norm.argtypes = [vp, i64, i32, i32, i32, vp, vp]
         L.eqo_quantize_uniform.argtypes = [vp, i64, dbl, dbl, i32, i32, vp, vp, vp]
         L.eqo_pack_table4.argtypes = [vp, i64, i64, i32, vp, vp, vp]
@@ -174,6 +177,21 @@ def hist_brute_search(x, b: int = 200) -> HistResult:
     ce, bv = np.zeros(1, np.int64), np.zeros(1, np.int64)
     scratch = np.empty(max(16, 5 * b), np.float64)
     rc = lib().eqo_hist_brute(_p(x), x.size, b, _p(lo), _p(hi), _p(st), _p(ns), _p(norm), _p(ce),
+                              _p(bv), _p(scratch))
+    if rc:
+        raise OracleError(rc)
+    return HistResult(float(lo[0]), float(hi[0]), int(st[0]), int(ns[0]), float(norm[0]),
+                      int(ce[0]), int(bv[0]))
+
+
+def hist_apprx_search(x, b: int = 200) -> HistResult:
+    """histclip.py:181-217."""
+    x = _f32(x)
+    lo, hi, norm = np.zeros(1), np.zeros(1), np.zeros(1)
+    st, ns = np.zeros(1, np.int32), np.zeros(1, np.int32)
+    ce, bv = np.zeros(1, np.int64), np.zeros(1, np.int64)
+    scratch = np.empty(max(16, 5 * b), np.float64)
+    rc = lib().eqo_hist_apprx(_p(x), x.size, b, _p(lo), _p(hi), _p(st), _p(ns), _p(norm), _p(ce),
                               _p(bv), _p(scratch))
     if rc:
         raise OracleError(rc)
@@ -283,3 +301,18 @@ def clip_range_rowwise(x, method: str):
     if rc:
         raise OracleError(rc)
     return float(lo[0]), float(hi[0]), int(ev[0])
+
+
+def kmeans_table(x, aux: str = "fp32", nthreads: int = 0):
+    """codebook.py:164-172 quantize_table_kmeans -> (codebooks (N,16) aux dtype, indices (N,d) u8,
+    Lloyd rounds per row; -1 = the <= 16 distinct values shortcut)."""
+    x = _f32(x)
+    rows, d = x.shape
+    dt = np.float16 if aux == "fp16" else np.float32
+    books = np.zeros((rows, 16), dt)
+    idx = np.zeros((rows, d), np.uint8)
+    it = np.zeros(rows, np.int32)
+    rc = lib().eqo_kmeans_table(_p(x), rows, d, d, AUX[aux], _p(books), _p(idx), _p(it), int(nthreads))
+    if rc:
+        raise OracleError(rc)
+    return books, idx, it

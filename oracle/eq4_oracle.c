@@ -52,6 +52,7 @@
 #define METHOD_ACIQ 4
 #define METHOD_GSS 5
 #define METHOD_TABLE 6
+#define METHOD_HIST_APPRX 7
 
 #define DST_NBINS 16 /* histclip.py:31 */
 
@@ -313,6 +314,66 @@ void eqo_offset_unit_norms(const double *k, long n, double bin_width, double dst
     }
 }
 
+/* histclip.py:110-121 window_norm: np.sum(density * _offset_unit_norms(arange(b) - s, w, dst_w)).
+ * density/k/contrib scratch: 3b doubles. */
+static double window_norm(const double *density, int b, double w, int s, int n, double *kbuf,
+                          double *contrib, double *prod) {
+    if (w == 0.0) return 0.0;
+    double dst_w = w * (double)n / (double)(DST_NBINS - 1);
+    for (int j = 0; j < b; j++) kbuf[j] = (double)j - (double)s;
+    eqo_offset_unit_norms(kbuf, b, w, dst_w, contrib);
+    for (int j = 0; j < b; j++) prod[j] = density[j] * contrib[j];
+    return eqo_np_sum(prod, b);
+}
+
+/* histclip.py:181-217 hist_apprx_search: from the full window, repeatedly drop
+ * NOTE: window norms use libm pow(x, 3); the reference's numpy `**3` dispatches
+ * to SIMD (SVML) power on AVX-512 hosts, which differs from libm in the last
+ * bit for a few % of inputs, so its norms are host-dependent in the last ulp
+ * (window selection agrees except at such near-ties).
+ * one bin from the end whose removal scores lower (ties drop from the right),
+ * keeping the best window seen.  scratch: >= 4*b doubles. */
+int eqo_hist_apprx(const float *x, long d, int b, double *lo, double *hi, int *start, int *nsel,
+                   double *norm, long *cand_evals, long *bin_visits, double *scratch) {
+    if (b < 1) return EQO_EB;
+    if (d <= 0) return EQO_EEMPTY;
+    int64_t *counts = (int64_t *)malloc(sizeof(int64_t) * (size_t)b);
+    if (!counts) return EQO_EALLOC;
+    double hlo, hhi;
+    eqo_build_histogram(x, d, b, &hlo, &hhi, counts);
+    if (hlo == hhi) {                                          /* :193-197 */
+        *cand_evals += 1;
+        *bin_visits += b;
+        *lo = hlo; *hi = hhi; *start = 0; *nsel = 1; *norm = 0.0;
+        free(counts);
+        return EQO_OK;
+    }
+    double w = (hhi - hlo) / (double)b;
+    double *density = scratch, *kbuf = scratch + b, *contrib = scratch + 2 * (long)b,
+           *prod = scratch + 3 * (long)b;
+    for (int j = 0; j < b; j++) density[j] = (double)counts[j] / w;
+    int st = 0, en = b;
+    double best = window_norm(density, b, w, st, en - st, kbuf, contrib, prod);
+    long evals = 1;
+    int bs = st, be = en;
+    while (en - st > 1) {                                      /* :201-213 */
+        double nl = window_norm(density, b, w, st + 1, en - st - 1, kbuf, contrib, prod);
+        double nr = window_norm(density, b, w, st, en - st - 1, kbuf, contrib, prod);
+        evals += 2;
+        double cur;
+        if (nl < nr) { st += 1; cur = nl; } else { en -= 1; cur = nr; }
+        if (cur < best) { best = cur; bs = st; be = en; }
+    }
+    *cand_evals += evals;
+    *bin_visits += evals * b;
+    *lo = hlo + w * (double)bs;                                /* :214-219 */
+    *hi = hlo + w * (double)be;
+    *start = bs; *nsel = be - bs; *norm = best;
+    free(counts);
+    if (!(isfinite(*lo) && isfinite(*hi)) || *lo > *hi) return EQO_ERANGE;
+    return EQO_OK;
+}
+
 /* histclip.py:136-174 hist_brute_search.  scratch: >= 5*b doubles.
  * Work counters follow histclip.py:148-150,162-164. */
 int eqo_hist_brute(const float *x, long d, int b, double *lo, double *hi, int *start, int *nsel,
@@ -455,12 +516,12 @@ int eqo_quantize_pack_table(const float *x, long rows, long d, long ld, int meth
                             double r, int aux, uint8_t *packed, double *lo_out, double *hi_out,
                             int32_t *info0, int32_t *info1, double *norm_out, int nthreads) {
     if (rows < 1 || d < 1) return EQO_EEMPTY;
-    if (method < 0 || method > 6) return EQO_EMETHOD;
+    if (method < 0 || method > 7) return EQO_EMETHOD;
     if (method == METHOD_GREEDY) {
         if (b < 1) return EQO_EB;
         if (!(0.0 < r && r <= 1.0)) return EQO_ER;
     }
-    if (method == METHOD_HIST_BRUTE && b < 1) return EQO_EB;
+    if ((method == METHOD_HIST_BRUTE || method == METHOD_HIST_APPRX) && b < 1) return EQO_EB;
     for (long i = 0; i < rows; i++)
         if (check_finite(x + i * ld, d)) return EQO_EFINITE;      /* table.py:28-29 */
     long stride = eqo_packed_row_stride(d, aux);
@@ -508,6 +569,9 @@ int eqo_quantize_pack_table(const float *x, long rows, long d, long ld, int meth
                 } else if (method == METHOD_HIST_BRUTE) {
                     long ce = 0, bv = 0;
                     rc = eqo_hist_brute(row, d, b, &lo, &hi, &a0, &a1, &nv, &ce, &bv, scratch);
+                } else if (method == METHOD_HIST_APPRX) {
+                    long ce = 0, bv = 0;
+                    rc = eqo_hist_apprx(row, d, b, &lo, &hi, &a0, &a1, &nv, &ce, &bv, scratch);
                 } else if (method == METHOD_SYM) {
                     rc = eqo_clip_range_sym(row, d, &lo, &hi);
                 } else if (method == METHOD_ACIQ) {
@@ -538,6 +602,170 @@ int eqo_quantize_pack_table(const float *x, long rows, long d, long ld, int meth
         }
         free(scratch);
         free(codes);
+    }
+    return err;
+}
+
+/* ------------------------------------------------------------------------ */
+/* codebook.py:35-137 row-wise KMEANS: kmeans_1d(x, 16, _uniform_grid(x), 100, 1e-7)
+ * then _sorted_codebook.  Bit-exact float64 restatement:
+ *  - <= 16 distinct values: centers = sorted distinct values padded with the
+ *    largest, assignments = searchsorted (codebook.py:55-61);
+ *  - Lloyd: argmin |v - c| (ties -> lower index), sse = np.sum((v - c[a])**2)
+ *    (pairwise), members.mean() (pairwise sum of the members in index order / m),
+ *    empty clusters keep their center, stop when max|new - old| < tol * spread,
+ *    keep the best-scoring assignment (strict <), score the final update;
+ *  - codebook sorted by a stable argsort, cast to the aux dtype; indices = rank.
+ * codebook_out: 16 values at the aux width; idx_out: d bytes; *iters_out =
+ * Lloyd rounds run (-1 for the distinct-value shortcut). scratch: 4*d doubles. */
+#define KM_K 16
+
+static int km_assign(const double *v, long d, const double *c, uint8_t *a) {
+    for (long i = 0; i < d; i++) {
+        double best = fabs(v[i] - c[0]);
+        int bj = 0;
+        for (int j = 1; j < KM_K; j++) {
+            double t = fabs(v[i] - c[j]);
+            if (t < best) { best = t; bj = j; }
+        }
+        a[i] = (uint8_t)bj;
+    }
+    return 0;
+}
+
+static double km_sse(const double *v, long d, const double *c, const uint8_t *a, double *tmp) {
+    for (long i = 0; i < d; i++) {
+        double e = v[i] - c[a[i]];
+        tmp[i] = e * e;
+    }
+    return eqo_np_sum(tmp, d);
+}
+
+int eqo_kmeans_row(const float *x, long d, int aux, void *codebook_out, uint8_t *idx_out,
+                   int *iters_out, double *scratch) {
+    if (d <= 0) return EQO_EEMPTY;
+    double *v = scratch, *tmp = scratch + d, *mem = scratch + 2 * d;
+    for (long i = 0; i < d; i++) v[i] = (double)x[i];
+    double centers[KM_K];
+    uint8_t *assign = (uint8_t *)malloc((size_t)d * 2);
+    if (!assign) return EQO_EALLOC;
+    uint8_t *best_a = assign + d;
+    /* distinct values (np.unique) */
+    double uniq[KM_K + 1];
+    int nu = 0;
+    for (long i = 0; i < d && nu <= KM_K; i++) {
+        int pos = 0;
+        while (pos < nu && uniq[pos] < v[i]) pos++;
+        if (pos < nu && uniq[pos] == v[i]) continue;
+        if (nu < KM_K + 1) {
+            for (int q = nu; q > pos; q--) uniq[q] = uniq[q - 1];
+            uniq[pos] = v[i];
+            nu++;
+        }
+    }
+    int iters = -1;
+    if (nu <= KM_K) {
+        for (int j = 0; j < KM_K; j++) centers[j] = j < nu ? uniq[j] : uniq[nu - 1];
+        for (long i = 0; i < d; i++) {
+            int pos = 0;
+            while (uniq[pos] < v[i]) pos++;            /* searchsorted, side='left' */
+            best_a[i] = (uint8_t)pos;
+        }
+    } else {
+        double lo = v[0], hi = v[0];
+        for (long i = 1; i < d; i++) { if (v[i] < lo) lo = v[i]; if (v[i] > hi) hi = v[i]; }
+        const double scale = (hi - lo) / (double)(KM_K - 1);   /* _uniform_grid */
+        for (int j = 0; j < KM_K; j++) centers[j] = lo + scale * (double)j;
+        const double spread = hi - lo;                          /* uniq[-1] - uniq[0] */
+        double best_sse = INFINITY, best_c[KM_K];
+        int it = 0;
+        for (it = 0; it < 100; it++) {
+            km_assign(v, d, centers, assign);
+            double sse = km_sse(v, d, centers, assign, tmp);
+            if (sse < best_sse) {
+                best_sse = sse;
+                memcpy(best_c, centers, sizeof centers);
+                memcpy(best_a, assign, (size_t)d);
+            }
+            double nc[KM_K];
+            memcpy(nc, centers, sizeof centers);
+            for (int j = 0; j < KM_K; j++) {
+                long m = 0;
+                for (long i = 0; i < d; i++)
+                    if (assign[i] == j) mem[m++] = v[i];
+                if (m) nc[j] = eqo_np_sum(mem, m) / (double)m;
+            }
+            double movement = 0.0;
+            for (int j = 0; j < KM_K; j++) {
+                double t = fabs(nc[j] - centers[j]);
+                if (t > movement) movement = t;
+            }
+            memcpy(centers, nc, sizeof centers);
+            if (movement < 1e-7 * spread) break;
+        }
+        iters = it < 100 ? it + 1 : 100;
+        km_assign(v, d, centers, assign);                       /* score the final update */
+        double sse = km_sse(v, d, centers, assign, tmp);
+        if (sse < best_sse) {
+            memcpy(best_a, assign, (size_t)d);
+        } else {
+            memcpy(centers, best_c, sizeof centers);
+        }
+    }
+    /* _sorted_codebook: stable argsort of the centers */
+    int order[KM_K], rank[KM_K];
+    for (int j = 0; j < KM_K; j++) order[j] = j;
+    for (int j = 1; j < KM_K; j++) {                            /* stable insertion sort */
+        int t = order[j], q = j - 1;
+        while (q >= 0 && centers[order[q]] > centers[t]) { order[q + 1] = order[q]; q--; }
+        order[q + 1] = t;
+    }
+    for (int j = 0; j < KM_K; j++) rank[order[j]] = j;
+    for (int j = 0; j < KM_K; j++) {
+        const double c = centers[order[j]];
+        if (aux == 1) {
+            _Float16 h = (_Float16)c;
+            memcpy((uint8_t *)codebook_out + 2 * j, &h, 2);
+        } else {
+            float f = (float)c;
+            memcpy((uint8_t *)codebook_out + 4 * j, &f, 4);
+        }
+    }
+    for (long i = 0; i < d; i++) idx_out[i] = (uint8_t)rank[best_a[i]];
+    if (iters_out) *iters_out = iters;
+    free(assign);
+    return EQO_OK;
+}
+
+int eqo_kmeans_table(const float *x, long rows, long d, long ld, int aux, void *codebooks,
+                     uint8_t *indices, int32_t *iters, int nthreads) {
+    if (rows < 1 || d < 1) return EQO_EEMPTY;
+    for (long i = 0; i < rows; i++)
+        if (check_finite(x + i * ld, d)) return EQO_EFINITE;
+    int err = 0;
+    const int ab = aux == 1 ? 2 : 4;
+#ifdef _OPENMP
+    if (nthreads < 1) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+#endif
+    {
+        double *scratch = (double *)malloc(sizeof(double) * (size_t)(4 * d + 16));
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 16)
+#endif
+        for (long i = 0; i < rows; i++) {
+            int it = 0;
+            int rc = scratch ? eqo_kmeans_row(x + i * ld, d, aux, (uint8_t *)codebooks + i * KM_K * ab,
+                                              indices + i * d, &it, scratch) : EQO_EALLOC;
+            if (iters) iters[i] = it;
+            if (rc) {
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+                { if (!err) err = rc; }
+            }
+        }
+        free(scratch);
     }
     return err;
 }

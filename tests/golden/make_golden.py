@@ -369,8 +369,45 @@ def make_methods():
     print("methods: done", len(tables), "tables")
 
 
+def make_kmeans():
+    """Row-wise KMEANS codebooks (codebook.py:35-172) and its EMBQ container from the reference."""
+    import tempfile
+
+    from embquant import fileio
+
+    rng = np.random.default_rng(31)
+    tables = {
+        "gauss64": gaussian_rows(601, 120, 64),
+        "lap64": laplacian_rows(602, 60, 64, 0.5),
+        "mixed17": mixed_table(80, 17, 603),
+        "mixed200": mixed_table(20, 200, 604),
+    }
+    e = rng.standard_normal((10, 20)).astype(np.float32)
+    e[0] = 0.0
+    e[1] = np.arange(20) % 5
+    e[2] = np.arange(20) % 16
+    e[3] = np.arange(20) % 17
+    e[4] *= 1e-25
+    e[5, :10] = 1.0
+    tables["edge20"] = e
+    tables["d1"] = rng.standard_normal((5, 1)).astype(np.float32)
+    out = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for tname, x in tables.items():
+            out[f"x_{tname}"] = x
+            for aux in ("fp16", "fp32"):
+                q = eq.quantize_table(eq.EmbeddingTable(x), "kmeans", 4, aux)
+                out[f"books_{tname}_{aux}"] = np.ascontiguousarray(q.codebooks)
+                out[f"idx_{tname}_{aux}"] = np.ascontiguousarray(q.indices)
+                path = os.path.join(tmp, "k.embq")
+                fileio.write_embq(path, q)
+                out[f"embq_{tname}_{aux}"] = np.frombuffer(open(path, "rb").read(), np.uint8)
+    np.savez_compressed(os.path.join(HERE, "kmeans.npz"), **out)
+    print("kmeans: done", len(tables), "tables")
+
+
 if __name__ == "__main__":
-    which = sys.argv[2:] or ["mse", "edge", "hist", "config1", "sls", "files", "methods"]
+    which = sys.argv[2:] or ["mse", "edge", "hist", "config1", "sls", "files", "methods", "kmeans"]
     for w in which:
         {"mse": make_mse, "edge": make_edge, "hist": make_hist, "config1": make_config1,
-         "sls": make_sls, "files": make_files, "methods": make_methods}[w]()
+         "sls": make_sls, "files": make_files, "methods": make_methods, "kmeans": make_kmeans}[w]()
