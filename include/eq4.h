@@ -158,6 +158,22 @@ int eq4_quantize_file(const char *in_path, const char *out_path, int method, int
 int eq4_write_embq(const char *path, const uint8_t *packed, int64_t rows, int64_t dim, int aux,
                    int on_device);
 
+/* fileio.py:105-110 kmeans_row payload stride: 16 codebook values at the aux
+ * width, then ceil(d/2) nibble bytes. */
+int64_t eq4_kmeans_row_stride(int64_t dim, int aux);
+
+/*
+ * codebook.py:164-172 quantize_table_kmeans (row-wise 16-value codebooks,
+ * k-means seeded at the row's uniform grid, codebook.py:35-137), bit-exact
+ * float64.  out [rows x eq4_kmeans_row_stride(dim, aux)] receives each row's
+ * sorted codebook (aux width) followed by its packed indices -- the EMBQ
+ * kmeans_row payload (fileio.py:105-110).  iters (optional): Lloyd rounds
+ * per row, -1 for the <= 16 distinct values shortcut.  dim <= 256.  Device
+ * pointers, stream-ordered; non-finite rows set EQ4_STATUS_NONFINITE.
+ */
+int eq4_kmeans_rows(const float *x, int64_t rows, int64_t dim, int64_t ld, int aux, uint8_t *out,
+                    int32_t *iters, int32_t *status, void *stream);
+
 /* Diagnostics: internal arithmetic self-test on the current device (mismatch
  * count, -1 on CUDA error).  which 0/1: the divide-free float64 w/15 used for
  * scales against the IEEE divide, on float differences / full-range doubles. */

@@ -36,6 +36,8 @@ from .api import (  # noqa: F401
     quantize_table,
     row_clip_range,
 )
+from .codebook import (CodebookQuantTable, CodebookRowQuant, quantize_row_kmeans,  # noqa: F401
+                       quantize_table_kmeans)
 from .pooled import PooledQuery, bytes_per_pooled_row, sparse_lengths_sum_4bit  # noqa: F401
 from .fileio import (DataError, quantize_file, read_embq, read_embt, write_embq,  # noqa: F401
                      write_embt)

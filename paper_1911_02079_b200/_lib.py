@@ -39,6 +39,8 @@ EXPORTS = (
     "eq4_unpack",
     "eq4_quant_mse",
     "eq4_sparse_lengths_sum4",
+    "eq4_kmeans_row_stride",
+    "eq4_kmeans_rows",
     "eq4_quantize_file",
     "eq4_write_embq",
     "eq4_selftest",
@@ -84,6 +86,10 @@ def load() -> ctypes.CDLL:
         L.eq4_quant_mse.restype = i32
         L.eq4_sparse_lengths_sum4.argtypes = [vp, i64, i64, i32, vp, i64, vp, i64, vp, vp, vp, vp]
         L.eq4_sparse_lengths_sum4.restype = i32
+        L.eq4_kmeans_row_stride.argtypes = [i64, i32]
+        L.eq4_kmeans_row_stride.restype = i64
+        L.eq4_kmeans_rows.argtypes = [vp, i64, i64, i64, i32, vp, vp, vp, vp]
+        L.eq4_kmeans_rows.restype = i32
         cp = ctypes.c_char_p
         L.eq4_quantize_file.argtypes = [cp, cp, i32, i32, dbl, i32, i64, vp, vp]
         L.eq4_quantize_file.restype = i32

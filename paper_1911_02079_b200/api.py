@@ -476,9 +476,13 @@ def quantize_table(table, method: str, nbits: int = 4, aux_precision: str = "fp3
         raise ValueError(f"{method} is 4-bit only, got nbits={nbits}")
     if k is not None and method != "kmeans-cls":
         raise ValueError(f"k applies only to kmeans-cls, not {method}")
+    if method == "kmeans":                                          # methods.py:76-77
+        from .codebook import quantize_table_kmeans
+
+        return quantize_table_kmeans(table, aux_precision)
     if method not in GPU_METHODS or nbits != 4:
         raise ValueError(f"{method!r} with nbits={nbits} is not on the B200 hot path "
-                         f"(supported: {GPU_METHODS} at nbits=4)")
+                         f"(supported: {GPU_METHODS + ('kmeans',)} at nbits=4)")
     _check_aux(aux_precision)
     if not isinstance(table, EmbeddingTable):
         table = EmbeddingTable(table)

@@ -1626,6 +1626,21 @@ const char* eq4_version(void) { return "eq4 0.1.0 (sm_100a)"; }
 
 const char* eq4_last_error(void) { return g_err.c_str(); }
 
+int64_t eq4_kmeans_row_stride(int64_t dim, int aux) {
+  return 16 * (aux == EQ4_AUX_FP16 ? 2 : 4) + (dim + 1) / 2;
+}
+
+int eq4_kmeans_rows(const float* x, int64_t rows, int64_t dim, int64_t ld, int aux, uint8_t* out,
+                    int32_t* iters, int32_t* status, void* stream) {
+  if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "table must be at least 1x1");
+  if (ld < dim) return fail(EQ4_EINVAL, "ld must be >= dim");
+  if (!x || !out) return fail(EQ4_EINVAL, "null buffer");
+  if (aux != EQ4_AUX_FP16 && aux != EQ4_AUX_FP32) return fail(EQ4_EINVAL, "aux must be fp32 or fp16");
+  std::string err;
+  const int rc = eq4_kmeans_launch(x, rows, dim, ld, aux, out, iters, status, (cudaStream_t)stream, err);
+  return rc == EQ4_OK ? rc : fail(rc, err);
+}
+
 int eq4_quantize_file(const char* in_path, const char* out_path, int method, int b, double r,
                       int aux, int64_t chunk_rows, int64_t* bad_row, double* bad_lohi) {
   if (!in_path || !out_path) return fail(EQ4_EINVAL, "null path");

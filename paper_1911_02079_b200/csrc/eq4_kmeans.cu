@@ -1,0 +1,350 @@
+// eq4_kmeans.cu -- row-wise KMEANS codebooks (
+// codebook.py:35-172): per row, scalar Lloyd iterations seeded at the 16
+// points of the row's uniform grid, float64, then a stable sort of the
+// codebook.  Output is the EMBQ kmeans_row payload (fileio.py:105-110): per
+// row 16 codebook values at the aux width, then the ceil(d/2) nibble bytes of
+// the indices (element 2k in the low nibble).
+//
+// Lane-per-row: every comparison and every float64 sum of the reference must
+// be replayed in order (argmin |v - c| with ties to the lower index, numpy
+// pairwise sums for the SSE and for each cluster mean, strict improvements of
+// the best SSE, movement < 1e-7 * spread), so each lane runs its own row's
+// Lloyd loop while the warp stages 32 rows as a [d][33] column tile.  The 16
+// centers live in registers (fully unrolled cluster loops); assignments are a
+// per-lane byte column in shared memory.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <string>
+
+#include "../../include/eq4.h"
+#include "eq4_device.cuh"
+#include "eq4_internal.h"
+
+namespace eq4 {
+
+constexpr int KM_THREADS = 128;
+constexpr int KM_WARPS = KM_THREADS / 32;
+constexpr int KM_K = 16;
+constexpr int KM_COL = 33;
+constexpr int KM_MAX_D = 256;
+
+struct KMParams {
+  const float* x;
+  int64_t rows, ld;
+  int d, aux, stride, half;
+  uint8_t* out;
+  int32_t* iters;
+  int32_t* status;
+  size_t warp_bytes;
+};
+
+struct KMLane {
+  const float* xs;   // this lane's column: element k at xs[k * KM_COL]
+  uint8_t* a;        // assignments, element k at a[k * 32]
+  uint8_t* ba;       // best assignments
+  __device__ __forceinline__ double v(int k) const { return (double)xs[k * KM_COL]; }
+};
+
+// numpy leaf (loops_utils.h.src) over the members [ms, me) of cluster j, in element order
+__device__ __forceinline__ double km_member_leaf(const KMLane& L, int d, int j, int ms, int me) {
+  const int n = me - ms;
+  if (n < 8) {
+    double res = 0.0;
+    int mi = 0;
+    for (int k = 0; k < d && mi < me; k++) {
+      if (L.a[k * 32] != j) continue;
+      if (mi >= ms) res = __dadd_rn(res, L.v(k));
+      mi++;
+    }
+    return res;
+  }
+  const int nfull = n - (n % 8);
+  double r[8];
+  double tail[8];
+  int nt = 0;
+  int mi = 0;
+  for (int k = 0; k < d && mi < me; k++) {
+    if (L.a[k * 32] != j) continue;
+    if (mi >= ms) {
+      const int t = mi - ms;
+      const double x = L.v(k);
+      if (t < 8) r[t] = x;
+      else if (t < nfull) r[t & 7] = __dadd_rn(r[t & 7], x);
+      else tail[nt++] = x;
+    }
+    mi++;
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (int i = 0; i < nt; i++) res = __dadd_rn(res, tail[i]);
+  return res;
+}
+
+// members.mean(): 0.0 + pairwise sum (<= 256 members: at most two leaves) / m
+__device__ __forceinline__ double km_member_mean(const KMLane& L, int d, int j, int m) {
+  double s;
+  if (m <= 128) {
+    s = km_member_leaf(L, d, j, 0, m);
+  } else {
+    int n2 = m / 2;
+    n2 -= n2 % 8;
+    s = __dadd_rn(km_member_leaf(L, d, j, 0, n2), km_member_leaf(L, d, j, n2, m));
+  }
+  return __ddiv_rn(__dadd_rn(0.0, s), (double)m);
+}
+
+// np.sum((v - c[a])**2): pairwise over the d squared errors (d <= 256: two leaves max)
+__device__ __forceinline__ double km_sse_leaf(const KMLane& L, const double* cl, int a0, int n) {
+  auto f = [&](int k) {
+    const double e = __dsub_rn(L.v(k), cl[L.a[k * 32]]);
+    return __dmul_rn(e, e);
+  };
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; i++) res = __dadd_rn(res, f(a0 + i));
+    return res;
+  }
+  double r0 = f(a0), r1 = f(a0 + 1), r2 = f(a0 + 2), r3 = f(a0 + 3);
+  double r4 = f(a0 + 4), r5 = f(a0 + 5), r6 = f(a0 + 6), r7 = f(a0 + 7);
+  const int nf = n - (n % 8);
+  int i = 8;
+  for (; i < nf; i += 8) {
+    r0 = __dadd_rn(r0, f(a0 + i));     r1 = __dadd_rn(r1, f(a0 + i + 1));
+    r2 = __dadd_rn(r2, f(a0 + i + 2)); r3 = __dadd_rn(r3, f(a0 + i + 3));
+    r4 = __dadd_rn(r4, f(a0 + i + 4)); r5 = __dadd_rn(r5, f(a0 + i + 5));
+    r6 = __dadd_rn(r6, f(a0 + i + 6)); r7 = __dadd_rn(r7, f(a0 + i + 7));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < n; i++) res = __dadd_rn(res, f(a0 + i));
+  return res;
+}
+
+__device__ __forceinline__ double km_sse(const KMLane& L, const double* cl, int d) {
+  if (d <= 128) return __dadd_rn(0.0, km_sse_leaf(L, cl, 0, d));
+  int n2 = d / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(0.0, __dadd_rn(km_sse_leaf(L, cl, 0, n2), km_sse_leaf(L, cl, n2, d - n2)));
+}
+
+// argmin_j |v - c_j| (first minimum), assignments to L.a, per-cluster counts
+__device__ __forceinline__ void km_assign(const KMLane& L, const double (&c)[KM_K], int d,
+                                          int (&cnt)[KM_K]) {
+#pragma unroll
+  for (int j = 0; j < KM_K; j++) cnt[j] = 0;
+  for (int k = 0; k < d; k++) {
+    const double x = L.v(k);
+    double best = fabs(__dsub_rn(x, c[0]));
+    int bj = 0;
+#pragma unroll
+    for (int j = 1; j < KM_K; j++) {
+      const double t = fabs(__dsub_rn(x, c[j]));
+      if (t < best) { best = t; bj = j; }
+    }
+    L.a[k * 32] = (uint8_t)bj;
+#pragma unroll
+    for (int j = 0; j < KM_K; j++) cnt[j] += (bj == j);
+  }
+}
+
+__global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* ws = smem + (size_t)warp * p.warp_bytes;
+  const int d = p.d;
+  float* xs = reinterpret_cast<float*>(ws);
+  uint8_t* abuf = ws + (((size_t)d * KM_COL * 4 + 15) & ~(size_t)15);
+  uint8_t* bbuf = abuf + (size_t)d * 32;
+  uint8_t* out_base = bbuf + (((size_t)d * 32 + 15) & ~(size_t)15);
+  const int ab = p.aux == EQ4_AUX_FP16 ? 2 : 4;
+  const int64_t nblk = (p.rows + 31) / 32;
+  for (int64_t blk = (int64_t)blockIdx.x * KM_WARPS + warp; blk < nblk;
+       blk += (int64_t)gridDim.x * KM_WARPS) {
+    const int64_t row0 = blk * 32, row = row0 + lane;
+    const bool rvalid = row < p.rows;
+    const int nrows = (int)min((int64_t)32, p.rows - row0);
+    for (int r = 0; r < nrows; r++) {
+      const float* src = p.x + (row0 + r) * p.ld;
+      for (int k = lane; k < d; k += 32) xs[k * KM_COL + r] = __ldcs(src + k);
+    }
+    __syncwarp();
+    KMLane L;
+    L.xs = xs + lane;
+    L.a = abuf + lane;
+    L.ba = bbuf + lane;
+    double c[KM_K];
+    int iters = -1;
+    bool bad = false;
+    if (rvalid) {
+      double lo = L.v(0), hi = lo;
+      for (int k = 0; k < d; k++) {
+        const float f = L.xs[k * KM_COL];
+        bad |= !isfinite(f);
+        const double x = (double)f;
+        lo = x < lo ? x : lo;
+        hi = x > hi ? x : hi;
+      }
+      if (bad && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
+      // np.unique(values).size <= 16: exact codebook (codebook.py:55-61)
+      double uq[KM_K + 1];
+      int nu = 0;
+      for (int k = 0; k < d && nu <= KM_K && !bad; k++) {
+        const double x = L.v(k);
+        int pos = 0;
+        while (pos < nu && uq[pos] < x) pos++;
+        if (pos < nu && uq[pos] == x) continue;
+        for (int q = nu; q > pos; q--) uq[q] = uq[q - 1];
+        uq[pos] = x;
+        nu++;
+      }
+      if (bad) {
+#pragma unroll
+        for (int j = 0; j < KM_K; j++) c[j] = 0.0;
+        for (int k = 0; k < d; k++) L.ba[k * 32] = 0;
+      } else if (nu <= KM_K) {
+#pragma unroll
+        for (int j = 0; j < KM_K; j++) c[j] = j < nu ? uq[j] : uq[nu - 1];
+        for (int k = 0; k < d; k++) {
+          const double x = L.v(k);
+          int pos = 0;
+          while (uq[pos] < x) pos++;   // searchsorted(side='left')
+          L.ba[k * 32] = (uint8_t)pos;
+        }
+      } else {
+        const double scale = __ddiv_rn(__dsub_rn(hi, lo), 15.0);   // _uniform_grid
+#pragma unroll
+        for (int j = 0; j < KM_K; j++) c[j] = __dadd_rn(lo, __dmul_rn(scale, (double)j));
+        const double stop = __dmul_rn(1e-7, __dsub_rn(hi, lo));   // tol * spread
+        double best_sse = INFINITY, bc[KM_K];
+        double cl[KM_K];   // dynamically indexed copy of the centers (sse)
+        int cnt[KM_K];
+        int it = 0;
+        for (it = 0; it < 100; it++) {
+          km_assign(L, c, d, cnt);
+#pragma unroll
+          for (int j = 0; j < KM_K; j++) cl[j] = c[j];
+          const double sse = km_sse(L, cl, d);
+          if (sse < best_sse) {
+            best_sse = sse;
+#pragma unroll
+            for (int j = 0; j < KM_K; j++) bc[j] = c[j];
+            for (int k = 0; k < d; k++) L.ba[k * 32] = L.a[k * 32];
+          }
+          double movement = 0.0;
+#pragma unroll
+          for (int j = 0; j < KM_K; j++) {
+            if (cnt[j]) {
+              const double nc = km_member_mean(L, d, j, cnt[j]);
+              const double t = fabs(__dsub_rn(nc, c[j]));
+              movement = t > movement ? t : movement;
+              c[j] = nc;
+            }
+          }
+          if (movement < stop) break;
+        }
+        iters = it < 100 ? it + 1 : 100;
+        km_assign(L, c, d, cnt);   // score the final center update
+#pragma unroll
+        for (int j = 0; j < KM_K; j++) cl[j] = c[j];
+        const double sse = km_sse(L, cl, d);
+        if (sse < best_sse) {
+          for (int k = 0; k < d; k++) L.ba[k * 32] = L.a[k * 32];
+        } else {
+#pragma unroll
+          for (int j = 0; j < KM_K; j++) c[j] = bc[j];
+        }
+      }
+    }
+    // _sorted_codebook: stable argsort of the 16 centers, rank of each center
+    uint8_t* out_tile = out_base + (((uintptr_t)p.out + (size_t)row0 * p.stride) & 15);
+    if (rvalid) {
+      int rank[KM_K];
+#pragma unroll
+      for (int j = 0; j < KM_K; j++) {
+        int rj = 0;
+#pragma unroll
+        for (int i = 0; i < KM_K; i++) rj += (c[i] < c[j]) || (c[i] == c[j] && i < j);
+        rank[j] = rj;
+      }
+      uint8_t* orow = out_tile + (size_t)lane * p.stride;
+#pragma unroll
+      for (int j = 0; j < KM_K; j++) {
+        // position rank[j] holds center j, cast once from float64 (astype)
+        if (ab == 2) {
+          const uint32_t h = aux_bits_f16(c[j]);
+          orow[2 * rank[j]] = h & 0xff;
+          orow[2 * rank[j] + 1] = h >> 8;
+        } else {
+          const uint32_t f = aux_bits_f32(c[j]);
+          for (int b = 0; b < 4; b++) orow[4 * rank[j] + b] = (f >> (8 * b)) & 0xff;
+        }
+      }
+      uint8_t* nib = orow + KM_K * ab;
+      for (int m = 0; m < p.half; m++) {
+        const int a0 = L.ba[(2 * m) * 32];
+        const int a1 = 2 * m + 1 < d ? L.ba[(2 * m + 1) * 32] : -1;
+        unsigned c0 = 0, c1 = 0;
+#pragma unroll
+        for (int j = 0; j < KM_K; j++) {
+          c0 = a0 == j ? (unsigned)rank[j] : c0;
+          c1 = a1 == j ? (unsigned)rank[j] : c1;
+        }
+        nib[m] = (uint8_t)(c0 | (c1 << 4));
+      }
+      if (p.iters) p.iters[row] = iters;
+    }
+    __syncwarp();
+    {
+      uint8_t* dst = p.out + (size_t)row0 * p.stride;
+      const int nbytes = nrows * p.stride;
+      int head = (int)((16 - ((uintptr_t)dst & 15)) & 15);
+      if (head > nbytes) head = nbytes;
+      const int nvec = (nbytes - head) >> 4;
+      const int tail = head + (nvec << 4);
+      if (lane < head) dst[lane] = out_tile[lane];
+      const uint4* s4 = reinterpret_cast<const uint4*>(out_tile + head);
+      uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+      for (int i = lane; i < nvec; i += 32) d4[i] = s4[i];
+      for (int i = tail + lane; i < nbytes; i += 32) dst[i] = out_tile[i];
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace eq4
+
+using namespace eq4;
+
+int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int aux, uint8_t* out,
+                      int32_t* iters, int32_t* status, cudaStream_t s, std::string& err) {
+  if (dim > KM_MAX_D) {
+    err = "kmeans with dim > 256 is not supported by the B200 path";
+    return EQ4_EUNSUPPORTED;
+  }
+  KMParams p;
+  p.x = x; p.rows = rows; p.ld = ld; p.d = (int)dim; p.aux = aux;
+  p.half = (int)((dim + 1) / 2);
+  p.stride = KM_K * (aux == EQ4_AUX_FP16 ? 2 : 4) + p.half;
+  p.out = out; p.iters = iters; p.status = status;
+  size_t wb = (((size_t)dim * KM_COL * 4 + 15) & ~(size_t)15) + (((size_t)dim * 32 + 15) & ~(size_t)15) * 2 +
+              (size_t)32 * p.stride + 32;
+  p.warp_bytes = (wb + 15) & ~(size_t)15;
+  const size_t smem = p.warp_bytes * KM_WARPS;
+  cudaError_t e = cudaFuncSetAttribute(k_kmeans_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 0, per_sm = 0;
+  if (e == cudaSuccess) e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_rows, KM_THREADS, smem);
+  if (e != cudaSuccess) { err = std::string("k_kmeans_rows setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+  const int64_t nblk = (rows + 31) / 32;
+  int64_t grid = (nblk + KM_WARPS - 1) / KM_WARPS;
+  const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  k_kmeans_rows<<<(unsigned)grid, KM_THREADS, smem, s>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) { err = std::string("k_kmeans_rows: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+  return EQ4_OK;
+}

@@ -96,9 +96,19 @@ def read_embq(path) -> PackedTable4:
     if rows < 1 or dim < 1:
         raise DataError(f"{path}: invalid shape {rows}x{dim}")
     scheme = _SCHEME_NAMES[scheme_code]
-    if scheme != "uniform4":
-        raise ValueError(f"EMBQ scheme {scheme!r} is not on the B200 hot path (uniform4 only)")
     aux = _AUX_NAMES[aux_code]
+    if scheme == "kmeans_row":                                 # fileio.py:156-163
+        from .codebook import CodebookQuantTable, kmeans_row_stride
+
+        nbytes = rows * kmeans_row_stride(dim, aux)
+        if len(blob) - _EMBQ_HEADER.size < nbytes:
+            raise DataError(f"{path}: truncated payload (codebook rows)")
+        if len(blob) - _EMBQ_HEADER.size != nbytes:
+            raise DataError(f"{path}: payload size mismatch")
+        return CodebookQuantTable.from_payload(
+            np.frombuffer(blob, dtype=np.uint8, offset=_EMBQ_HEADER.size), rows, dim, aux)
+    if scheme != "uniform4":
+        raise ValueError(f"EMBQ scheme {scheme!r} is not on the B200 hot path (uniform4, kmeans_row)")
     nbytes = rows * packed_row_stride(dim, aux)
     if len(blob) - _EMBQ_HEADER.size < nbytes:
         raise DataError(f"{path}: truncated payload (packed rows)")
@@ -110,6 +120,15 @@ def read_embq(path) -> PackedTable4:
 def write_embq(path, quant) -> None:
     """fileio.py:94-101 for 4-bit uniform tables: header + PackedTable4 bytes verbatim.
     A device-resident PackedTable4 is streamed out of HBM by the native writer."""
+    from .codebook import CodebookQuantTable
+
+    if isinstance(quant, CodebookQuantTable):                  # fileio.py:105-110
+        head = _EMBQ_HEADER.pack(_EMBQ_MAGIC, _VERSION, _SCHEME_CODES["kmeans_row"],
+                                 _AUX_CODES[quant.aux_precision], quant.rows, quant.dim)
+        with open(path, "wb") as fh:
+            fh.write(head)
+            fh.write(quant.payload().tobytes())
+        return
     if isinstance(quant, UniformQuantTable):
         if quant.nbits != 4:
             raise ValueError("8-bit EMBQ (uniform8) is not on the B200 hot path")
