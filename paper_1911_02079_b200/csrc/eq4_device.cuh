@@ -58,6 +58,37 @@ __device__ __forceinline__ double np_err2(double x, double lo, double hi, double
   return __dmul_rn(e, e);
 }
 
+// np_err2 without the divide: q = (c - lo) * RN(1/scale) is within a few ulp of
+// numpy's correctly rounded quotient, so floor(q + 0.5) can only differ when
+// q + 0.5 lies within ~1e-14 of an integer; inside 1e-12 of one the IEEE
+// divide decides (bit-identical to np_err2).
+struct NpCodec {
+  double lo, hi, scale, inv;
+};
+__device__ __forceinline__ NpCodec np_codec(double lo, double hi) {
+  NpCodec c;
+  c.lo = lo;
+  c.hi = hi;
+  c.scale = (hi == lo) ? 0.0 : div15(__dsub_rn(hi, lo));   // table.py:99
+  c.inv = (hi == lo) ? 0.0 : __drcp_rn(c.scale);
+  return c;
+}
+__device__ __forceinline__ double np_err2_fast(double x, const NpCodec& c) {
+  if (c.hi == c.lo) {
+    const double e = __dsub_rn(x, c.lo);
+    return __dmul_rn(e, e);
+  }
+  const double dl = __dsub_rn(np_clip(x, c.lo, c.hi), c.lo);
+  const double t = __dadd_rn(__dmul_rn(dl, c.inv), 0.5);
+  const double fl = floor(t);
+  const double fr = __dsub_rn(t, fl);
+  double q = fl;
+  if (!(fr > 1e-12 && fr < 1.0 - 1e-12)) q = floor(__dadd_rn(__ddiv_rn(dl, c.scale), 0.5));
+  const double code = np_clip(q, 0.0, 15.0);
+  const double e = __dsub_rn(x, __dadd_rn(__dmul_rn(c.scale, code), c.lo));
+  return __dmul_rn(e, e);
+}
+
 // numpy pairwise-sum leaves: np.add.reduce splits n > 128 into
 // n2 = n/2 - (n/2 % 8) and n - n2 recursively; leaves have <= 128 elements.
 // Enumerate the leaves of [0, n) in order.  Returns the leaf count.
@@ -105,11 +136,11 @@ static __device__ __noinline__ double warp_np_loss(const float* xs, int d, doubl
                                             double* e2, double* leaf_sum, int* leaf_start,
                                             int* leaf_len, int max_leaves) {
   const int lane = threadIdx.x & 31;
-  const double scale = (hi == lo) ? 0.0 : div15(__dsub_rn(hi, lo));   // table.py:99
+  const NpCodec cd = np_codec(lo, hi);   // table.py:99
   if (d < 8) {  // numpy: res = 0.; res += a[i] sequentially
     double res = 0.0;
     if (lane == 0)
-      for (int i = 0; i < d; i++) res = __dadd_rn(res, np_err2((double)xs[i], lo, hi, scale));
+      for (int i = 0; i < d; i++) res = __dadd_rn(res, np_err2_fast((double)xs[i], cd));
     res = __shfl_sync(FULL, res, 0);
     return __dadd_rn(0.0, res);
   }
@@ -121,7 +152,7 @@ static __device__ __noinline__ double warp_np_loss(const float* xs, int d, doubl
   for (int base = 0; base < nl; base += 4) {
     const int last = min(base + 4, nl) - 1;
     const int r0 = leaf_start[base], r1 = leaf_start[last] + leaf_len[last];
-    for (int k = lane; k < r1 - r0; k += 32) e2[k] = np_err2((double)xs[r0 + k], lo, hi, scale);
+    for (int k = lane; k < r1 - r0; k += 32) e2[k] = np_err2_fast((double)xs[r0 + k], cd);
     __syncwarp();
     const int li = base + g;
     const bool ok = li < nl;
@@ -167,18 +198,19 @@ __device__ __forceinline__ void warp_np_loss3_leaf(const float* xs, int d, int n
   const double lo = k == 0 ? lo0 : (k == 1 ? lo1 : lo2);
   const double hi = k == 0 ? hi0 : (k == 1 ? hi1 : hi2);
   const bool act = k < nr;
-  const double scale = (hi == lo) ? 0.0 : div15(__dsub_rn(hi, lo));   // table.py:99
+  const NpCodec cd = np_codec(lo, hi);
   const int nfull = d - (d % 8);
+  const int nch = nfull >> 3;   // chain length <= 16
   double r = 0.0;
   if (act) {
-    r = np_err2((double)xs[m], lo, hi, scale);
-    for (int i = 8 + m; i < nfull; i += 8) r = __dadd_rn(r, np_err2((double)xs[i], lo, hi, scale));
+    r = np_err2_fast((double)xs[m], cd);
+    for (int u = 1; u < nch; u++) r = __dadd_rn(r, np_err2_fast((double)xs[m + 8 * u], cd));
   }
   r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 1));
   r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 2));
   r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 4));
   if (act && m == 0)
-    for (int i = nfull; i < d; i++) r = __dadd_rn(r, np_err2((double)xs[i], lo, hi, scale));
+    for (int i = nfull; i < d; i++) r = __dadd_rn(r, np_err2_fast((double)xs[i], cd));
   v0 = __dadd_rn(0.0, __shfl_sync(FULL, r, 0));
   v1 = __dadd_rn(0.0, __shfl_sync(FULL, r, 8));
   v2 = __dadd_rn(0.0, __shfl_sync(FULL, r, 16));
