@@ -1022,14 +1022,18 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         // two streaming passes over the row slice (the second hits L1/L2), so
         // no E-element register array is live across the float64 setup
         const float4* src = reinterpret_cast<const float4*>(xr) + q;
-        float lmn = INFINITY, lmx = -INFINITY, sm = 0.f;
+        float lmn = INFINITY, lmx = -INFINITY;
+        f2_t sm2 = pk2(0.f, 0.f);   // NaN / Inf detector: a packed running sum
 #pragma unroll
         for (int c = 0; c < E / 4; ++c) {
           const float4 t = __ldg(src + LPR * c);
           lmn = fminf(lmn, fminf(fminf(t.x, t.y), fminf(t.z, t.w)));
           lmx = fmaxf(lmx, fmaxf(fmaxf(t.x, t.y), fmaxf(t.z, t.w)));
-          sm = __fadd_rn(sm, __fadd_rn(__fadd_rn(t.x, t.y), __fadd_rn(t.z, t.w)));
+          sm2 = add2(sm2, add2(pk2(t.x, t.y), pk2(t.z, t.w)));
         }
+        float s0, s1;
+        upk2(sm2, s0, s1);
+        float sm = __fadd_rn(s0, s1);
         mn = group_min<LPR>(lmn);
         mx = group_max<LPR>(lmx);
         sm = group_sum<LPR>(sm);
