@@ -358,7 +358,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--secondary", action="store_true")
+    ap.add_argument("--secondary", action=argparse.BooleanOptionalAction, default=True,
+                    help="config 2 ASYM, config 3 GREEDY and the SLS lookup, device-timed (rank 0)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
