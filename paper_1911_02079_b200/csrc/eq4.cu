@@ -1377,6 +1377,88 @@ __global__ void __launch_bounds__(NTHREADS, 3) k_asym_vec(const Params p) {
   }
 }
 
+// ASYM-family kernel fed by the bulk-copy (TMA) engine: each warp owns a ring
+// of ASTAGES shared-memory stages; lane 0 keeps the next ASTAGES-1 row blocks
+// (RPW contiguous rows, <= 2 KB) in flight with cp.async.bulk + mbarrier
+// transaction counts, so the bytes in flight per SM no longer depend on
+// registers.  Rows must be contiguous (ld == d) and 16-byte aligned.
+#ifndef ASTAGES
+#define ASTAGES 4
+#endif
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+               "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}"
+      ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(parity) : "memory");
+}
+
+template <int LPR, int E>
+struct SliceB {
+  static constexpr int RPW = 32 / LPR;
+  static constexpr int BLK = RPW * LPR * E * 4;                      // bytes per row block
+  static constexpr int NST = (ASTAGES * 2048) / BLK;                // ~8 KB of stages per warp
+  static constexpr size_t bytes() { return (size_t)NST * BLK + 128; }   // + barriers
+};
+
+template <int LPR, int E, int RM>
+__global__ void __launch_bounds__(NTHREADS, 2) k_asym_bulk(const Params p) {
+  using S = SliceB<LPR, E>;
+  constexpr int RPW = S::RPW;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = lane / LPR, q = lane % LPR;
+  unsigned char* ws = smem + (size_t)warp * S::bytes();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ws + (size_t)S::NST * S::BLK);
+  const int64_t nblocks = (p.rows + RPW - 1) / RPW;
+  const int64_t wstride = (int64_t)gridDim.x * NWARPS;
+  const int64_t blk0 = (int64_t)blockIdx.x * NWARPS + warp;
+  const size_t row_bytes = (size_t)p.d * 4;
+  if (lane == 0) {
+    for (int st = 0; st < S::NST; st++) mbar_init(bar + st, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto issue = [&](int64_t blk, int st) {
+    const int64_t r0 = blk * RPW;
+    const unsigned nb = (unsigned)(min((int64_t)RPW, p.rows - r0) * row_bytes);
+    mbar_expect_tx(bar + st, nb);
+    bulk_g2s(ws + (size_t)st * S::BLK, p.x + r0 * p.d, nb, bar + st);
+  };
+  if (lane == 0)
+    for (int st = 0; st < S::NST - 1; st++)
+      if (blk0 + st * wstride < nblocks) issue(blk0 + st * wstride, st);
+  int64_t it = 0;
+  for (int64_t blk = blk0; blk < nblocks; blk += wstride, ++it) {
+    const int st = (int)(it % S::NST);
+    if (lane == 0) {   // keep S::NST - 1 blocks ahead in flight
+      const int64_t ahead = blk + (int64_t)(S::NST - 1) * wstride;
+      if (ahead < nblocks) issue(ahead, (int)((it + S::NST - 1) % S::NST));
+    }
+    mbar_wait(bar + st, (unsigned)((it / S::NST) & 1));
+    const float4* rs = reinterpret_cast<const float4*>(ws + (size_t)st * S::BLK + (size_t)gw * row_bytes);
+    float4 cur[E / 4];
+#pragma unroll
+    for (int c = 0; c < E / 4; ++c) cur[c] = rs[q + LPR * c];
+    __syncwarp();   // the stage is refilled only after every lane has read it
+    asym_row<LPR, E, RM>(p, cur, blk * RPW + gw, q);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // pack / unpack / quant_mse utility kernels
 // ---------------------------------------------------------------------------
@@ -1515,6 +1597,17 @@ template <int METHOD, int LPR, int E, bool VEC>
 static int launch_rq(const Params& p, cudaStream_t s) {
   if constexpr (METHOD == M_ASYM) {
     if constexpr (VEC && E <= 16) {
+      const char* bv = getenv("EQ4_ASYM_BULK");
+      // contiguous rows of >= 32 floats: bulk-copy ring (d = 16 rows make 1 KB blocks,
+      // where the register double buffer measured faster)
+      if (LPR * E >= 32 && p.ld == p.d && !(bv && bv[0] == '0')) {
+        using B = SliceB<LPR, E>;
+        const int64_t nt = (p.rows + B::RPW * NWARPS - 1) / (B::RPW * NWARPS);
+        const size_t sm = NWARPS * B::bytes();
+        if (p.range_mode == 1) return launch_persistent(k_asym_bulk<LPR, E, 1>, sm, nt, p, s, "k_asym_bulk");
+        if (p.range_mode == 2) return launch_persistent(k_asym_bulk<LPR, E, 2>, sm, nt, p, s, "k_asym_bulk");
+        return launch_persistent(k_asym_bulk<LPR, E, 0>, sm, nt, p, s, "k_asym_bulk");
+      }
       using S = SliceA<LPR, E>;
       const int64_t nt = (p.rows + S::RPW * NWARPS - 1) / (S::RPW * NWARPS);
       if (p.range_mode == 1) return launch_persistent(k_asym_vec<LPR, E, 1>, 0, nt, p, s, "k_asym_vec");
