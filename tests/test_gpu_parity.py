@@ -247,3 +247,52 @@ def test_hist_brute_api_counters(eq):
     assert w.clip_range == eq.ClipRange(h.xmin, h.xmax)
     assert (c.candidate_evals, c.bin_visits) == (h.candidate_evals, h.bin_visits)
     assert eq.clip_range_hist_brute([4.0, 4.0, 4.0], 16) == eq.ClipRange(4.0, 4.0)
+
+
+@pytest.mark.parametrize("method", ["greedy", "asym", "sym", "hist-brute", "gss"])
+def test_c_abi_strided_rows_and_unaligned_output(eq, method):
+    """eq4_quantize_pack through ctypes with ld > d (a column slice of a wider table) and a
+    packed buffer that starts at an odd byte: the generic (masked) paths, same bytes."""
+    import ctypes
+
+    import torch
+
+    from oracle import rng
+    from paper_1911_02079_b200 import _lib
+
+    rows, d, ld = 3001, 60, 67
+    full = rng.mixed_table(rows, ld, 12)
+    want = oracle.quantize_pack_table(np.ascontiguousarray(full[:, :d]), method, 200, 0.16, "fp16")
+    stride = eq.packed_row_stride(d, "fp16")
+    xd = torch.from_numpy(full).cuda()
+    buf = torch.zeros(rows * stride + 1, dtype=torch.uint8, device="cuda")
+    lo = torch.empty(rows, dtype=torch.float64, device="cuda")
+    hi = torch.empty(rows, dtype=torch.float64, device="cuda")
+    vp = ctypes.c_void_p
+    rc = eq.load().eq4_quantize_pack(vp(xd.data_ptr()), rows, d, ld, _lib.METHOD[method], 200, 0.16,
+                                     _lib.AUX["fp16"], vp(buf.data_ptr() + 1), vp(lo.data_ptr()),
+                                     vp(hi.data_ptr()), None, None, None, None, None)
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    assert np.array_equal(buf[1:].cpu().numpy(), want.packed)
+    assert np.array_equal(lo.cpu().numpy(), want.xmin) and np.array_equal(hi.cpu().numpy(), want.xmax)
+
+
+@pytest.mark.parametrize("b,r", [(50, 0.16), (200, 0.5), (400, 0.1), (1000, 0.16), (7, 1.0)])
+def test_greedy_other_b_r_vs_oracle(eq, b, r):
+    import torch
+
+    from oracle import rng
+
+    x = rng.mixed_table(4000, 64, b)
+    try:
+        want = oracle.quantize_pack_table(x, "greedy", b, r, "fp32")
+    except oracle.OracleError as e:  # a candidate with xmin > xmax: the reference's ValueError
+        assert e.code == 4
+        with pytest.raises(ValueError, match="exceeds xmax"):
+            eq.quantize_pack_table4(torch.from_numpy(x).cuda(), "greedy", "fp32", b, r)
+        return
+    p, rr = eq.quantize_pack_table4(torch.from_numpy(x).cuda(), "greedy", "fp32", b, r, with_rows=True)
+    assert np.array_equal(p.buffer, want.packed)
+    assert np.array_equal(rr.xmin.cpu().numpy(), want.xmin)
+    assert np.array_equal(rr.xmax.cpu().numpy(), want.xmax)
