@@ -46,6 +46,7 @@ extern "C" {
 #define EQ4_METHOD_ACIQ 4       /* clipping.py:115-139 clip_range_aciq (laplacian) */
 #define EQ4_METHOD_GSS 5        /* clipping.py:70-112  clip_range_gss (tol 1e-4) */
 #define EQ4_METHOD_TABLE 6      /* clipping.py:64-67   clip_range_table (one range per table) */
+#define EQ4_METHOD_HIST_APPRX 7 /* histclip.py:181-217 hist_apprx_search (b <= 256) */
 
 #define EQ4_AUX_FP32 0 /* uniform.py:19-35 aux_precision="fp32" */
 #define EQ4_AUX_FP16 1 /* aux_precision="fp16" */
@@ -78,7 +79,8 @@ int64_t eq4_packed_row_stride(int64_t dim, int aux);
  *   xmin, xmax  float64 ClipRange of the row (the reference's row_clip_range)
  *   info0       GREEDY: while-loop iterations (loss_evals = 1 + 2*iters),
  *               -1 constant row, -2 range error; HIST-BRUTE: start_bin;
- *               GSS: quant_mse evaluations (WorkCounters.loss_evals)
+ *               GSS: quant_mse evaluations (WorkCounters.loss_evals);
+ *               HIST-APPRX: start_bin (info1 nbins_selected, norm the window norm)
  *   info1       GREEDY: (best_i << 16) | best_j; HIST-BRUTE: nbins_selected
  *   norm        HIST-BRUTE window norm (HistWindow.norm); unused otherwise
  *   status      device int32, EQ4_STATUS_* bits OR-ed in by the kernels

@@ -77,6 +77,7 @@ def lib():
         L.eqo_hist_brute.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp]
         L.eqo_kmeans_table.argtypes = [vp, i64, i64, i64, i32, vp, vp, vp, i32]
         L.eqo_hist_apprx.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.eqo_hist_apprx_gap.argtypes = [vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]
         L.eqo_hist_window_norm.argtypes = [vp, i64, i32, i32, i32, vp, vp]
         L.eqo_quantize_uniform.argtypes = [vp, i64, dbl, dbl, i32, i32, vp, vp, vp]
         L.eqo_pack_table4.argtypes = [vp, i64, i64, i32, vp, vp, vp]
@@ -197,6 +198,19 @@ def hist_apprx_search(x, b: int = 200) -> HistResult:
         raise OracleError(rc)
     return HistResult(float(lo[0]), float(hi[0]), int(st[0]), int(ns[0]), float(norm[0]),
                       int(ce[0]), int(bv[0]))
+
+
+def hist_apprx_gap(x, b: int = 200):
+    """(HistResult without counters, min relative |nl - nr| gap over the walk's decisions)."""
+    x = _f32(x)
+    lo, hi, norm, gap = np.zeros(1), np.zeros(1), np.zeros(1), np.zeros(1)
+    st, ns = np.zeros(1, np.int32), np.zeros(1, np.int32)
+    scratch = np.empty(max(16, 5 * b), np.float64)
+    rc = lib().eqo_hist_apprx_gap(_p(x), x.size, b, _p(lo), _p(hi), _p(st), _p(ns), _p(norm),
+                                  _p(scratch), _p(gap))
+    if rc:
+        raise OracleError(rc)
+    return HistResult(float(lo[0]), float(hi[0]), int(st[0]), int(ns[0]), float(norm[0]), 0, 0), float(gap[0])
 
 
 def hist_window_norm(x, b: int, start: int, n: int) -> float:

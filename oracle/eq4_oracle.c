@@ -333,8 +333,27 @@ static double window_norm(const double *density, int b, double w, int s, int n, 
  * (window selection agrees except at such near-ties).
  * one bin from the end whose removal scores lower (ties drop from the right),
  * keeping the best window seen.  scratch: >= 4*b doubles. */
+static int hist_apprx_impl(const float *x, long d, int b, double *lo, double *hi, int *start,
+                           int *nsel, double *norm, long *cand_evals, long *bin_visits,
+                           double *scratch, double *min_gap);
+
 int eqo_hist_apprx(const float *x, long d, int b, double *lo, double *hi, int *start, int *nsel,
                    double *norm, long *cand_evals, long *bin_visits, double *scratch) {
+    return hist_apprx_impl(x, d, b, lo, hi, start, nsel, norm, cand_evals, bin_visits, scratch, NULL);
+}
+
+/* Same walk; *min_gap = min over its decisions of |nl - nr| / max(nl, nr) (test helper:
+ * a walk can only diverge from another float64 evaluation order at a near-tie). */
+int eqo_hist_apprx_gap(const float *x, long d, int b, double *lo, double *hi, int *start, int *nsel,
+                       double *norm, double *scratch, double *min_gap) {
+    long ce = 0, bv = 0;
+    return hist_apprx_impl(x, d, b, lo, hi, start, nsel, norm, &ce, &bv, scratch, min_gap);
+}
+
+static int hist_apprx_impl(const float *x, long d, int b, double *lo, double *hi, int *start,
+                           int *nsel, double *norm, long *cand_evals, long *bin_visits,
+                           double *scratch, double *min_gap) {
+    if (min_gap) *min_gap = INFINITY;
     if (b < 1) return EQO_EB;
     if (d <= 0) return EQO_EEMPTY;
     int64_t *counts = (int64_t *)malloc(sizeof(int64_t) * (size_t)b);
@@ -360,6 +379,11 @@ int eqo_hist_apprx(const float *x, long d, int b, double *lo, double *hi, int *s
         double nl = window_norm(density, b, w, st + 1, en - st - 1, kbuf, contrib, prod);
         double nr = window_norm(density, b, w, st, en - st - 1, kbuf, contrib, prod);
         evals += 2;
+        if (min_gap) {
+            double m = nl > nr ? nl : nr;
+            double g = m > 0 ? fabs(nl - nr) / m : 0.0;
+            if (g < *min_gap) *min_gap = g;
+        }
         double cur;
         if (nl < nr) { st += 1; cur = nl; } else { en -= 1; cur = nr; }
         if (cur < best) { best = cur; bs = st; be = en; }

@@ -24,9 +24,11 @@ from .api import (  # noqa: F401
     clip_range_asym,
     clip_range_greedy,
     clip_range_gss,
+    clip_range_hist_apprx,
     clip_range_sym,
     clip_range_table,
     clip_range_hist_brute,
+    hist_apprx_search,
     hist_brute_search,
     pack_table4,
     packed_row_stride,

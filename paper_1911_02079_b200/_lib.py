@@ -21,7 +21,8 @@ EQ4_EDATA = 3
 EQ4_ERANGE = 4
 EQ4_EUNSUPPORTED = 5
 
-METHOD = {"asym": 0, "greedy": 1, "hist-brute": 2, "sym": 3, "aciq": 4, "gss": 5, "table": 6}
+METHOD = {"asym": 0, "greedy": 1, "hist-brute": 2, "sym": 3, "aciq": 4, "gss": 5, "table": 6,
+          "hist-apprx": 7}
 AUX = {"fp32": 0, "fp16": 1}
 STATUS_NONFINITE = 1
 STATUS_RANGE = 2

@@ -31,7 +31,7 @@ except ImportError:  # pragma: no cover - torch is part of the image
 UNIFORM_METHODS = ("sym", "asym", "table", "gss", "aciq", "greedy", "hist-apprx", "hist-brute")
 CODEBOOK_METHODS = ("kmeans", "kmeans-cls")
 ALL_METHODS = UNIFORM_METHODS + CODEBOOK_METHODS            # methods.py:38-40
-GPU_METHODS = ("sym", "asym", "table", "gss", "aciq", "greedy", "hist-brute")
+GPU_METHODS = ("sym", "asym", "table", "gss", "aciq", "greedy", "hist-apprx", "hist-brute")
 AUX_PRECISIONS = ("fp32", "fp16")                            # uniform.py:19
 _AUX_NP = {"fp32": np.float32, "fp16": np.float16}
 
@@ -341,7 +341,7 @@ def _check_method_params(method: str, b: int, r: float) -> None:
             raise ValueError(f"b must be >= 1, got {b}")            # clipping.py:158-159
         if not 0.0 < r <= 1.0:
             raise ValueError(f"r must be in (0, 1], got {r}")       # clipping.py:160-161
-    elif method == "hist-brute" and b < 1:
+    elif method in ("hist-brute", "hist-apprx") and b < 1:
         raise ValueError(f"b must be >= 1, got {b}")                # histclip.py:54-55
 
 
@@ -453,6 +453,14 @@ def _apply_counters(counters: WorkCounters, method: str, b: int, rr: RowResults)
         ev = np.asarray(rr.info0.cpu() if _is_cuda(rr.info0) else rr.info0).astype(np.int64)
         counters.loss_evals += int(ev.sum())
         return
+    if method == "hist-apprx":                                      # histclip.py:113-115,193-210
+        lo = np.asarray(rr.xmin.cpu() if _is_cuda(rr.xmin) else rr.xmin)
+        hi = np.asarray(rr.xmax.cpu() if _is_cuda(rr.xmax) else rr.xmax)
+        const = int(np.sum(lo == hi))
+        full = lo.size - const
+        counters.candidate_evals += full * (2 * b - 1) + const
+        counters.bin_visits += full * (2 * b - 1) * b + const * b
+        return
     if method == "greedy":                                          # clipping.py:174,183-184
         it = np.asarray(rr.info0.cpu() if _is_cuda(rr.info0) else rr.info0).astype(np.int64)
         counters.loss_evals += int(np.sum(np.where(it >= 0, 1 + 2 * it, 0)))
@@ -538,6 +546,20 @@ def hist_brute_search(x, b: int = 200, counters: WorkCounters | None = None) -> 
                       int(rr.info0[0].item()), int(rr.info1[0].item()), float(rr.norm[0].item()))
 
 
+def hist_apprx_search(x, b: int = 200, counters: WorkCounters | None = None) -> HistWindow:
+    """histclip.py:181-217 (b <= 256 on the GPU path)."""
+    _check_method_params("hist-apprx", b, 0.16)
+    rr = _row_search("hist-apprx", x, b)
+    _apply_counters(counters, "hist-apprx", b, rr)
+    return HistWindow(ClipRange(float(rr.xmin[0].item()), float(rr.xmax[0].item())),
+                      int(rr.info0[0].item()), int(rr.info1[0].item()), float(rr.norm[0].item()))
+
+
+def clip_range_hist_apprx(x, b: int = 200, counters: WorkCounters | None = None) -> ClipRange:
+    """histclip.py:220-221."""
+    return hist_apprx_search(x, b, counters).clip_range
+
+
 def clip_range_hist_brute(x, b: int = 200, counters: WorkCounters | None = None) -> ClipRange:
     """histclip.py:177-178."""
     return hist_brute_search(x, b, counters).clip_range
@@ -598,7 +620,7 @@ def row_clip_range(method: str, x, nbits: int = 4, b: int = 200, r: float = 0.16
     if method == "hist-brute":
         return clip_range_hist_brute(x, b, counters=counters)
     if method == "hist-apprx":
-        raise ValueError(f"{method!r} is not on the B200 hot path (supported: {GPU_METHODS})")
+        return clip_range_hist_apprx(x, b, counters=counters)
     raise ValueError(f"{method!r} is not a row-wise uniform strategy")     # methods.py:60
 
 

@@ -1812,7 +1812,8 @@ static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t
   if (!x || !packed) return fail(EQ4_EINVAL, "null buffer");
   if (aux != EQ4_AUX_FP16 && aux != EQ4_AUX_FP32) return fail(EQ4_EINVAL, "aux must be fp32 or fp16");
   if ((xmin == nullptr) != (xmax == nullptr)) return fail(EQ4_EINVAL, "xmin/xmax must be given together");
-  if (method == EQ4_METHOD_GREEDY || method == EQ4_METHOD_HIST_BRUTE) {
+  if (method == EQ4_METHOD_GREEDY || method == EQ4_METHOD_HIST_BRUTE ||
+      method == EQ4_METHOD_HIST_APPRX) {
     if (b < 1) return fail(EQ4_EINVAL, "b must be >= " "1, got " + std::to_string(b));
   }
   if (method == EQ4_METHOD_GREEDY && !(0.0 < r && r <= 1.0))
@@ -1849,10 +1850,10 @@ static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t
     cudaFreeAsync(keys, s);
     return rc;
   }
-  if (method == EQ4_METHOD_ACIQ || method == EQ4_METHOD_GSS) {
+  if (method == EQ4_METHOD_ACIQ || method == EQ4_METHOD_GSS || method == EQ4_METHOD_HIST_APPRX) {
     std::string err;
     const int rc = eq4_rowrange_launch(x, rows, dim, ld, method, aux, packed, xmin, xmax, info0,
-                                       status, s, err);
+                                       status, s, err, b, info1, norm);
     return rc == EQ4_OK ? rc : fail(rc, err);
   }
   if (method == EQ4_METHOD_GREEDY) {

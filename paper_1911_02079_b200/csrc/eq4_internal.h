@@ -26,7 +26,8 @@ int eq4_io_write_embq(const char* path, const uint8_t* packed, int64_t rows, int
 // ACIQ / GSS row-range searches + quantize + pack (eq4_rowrange.cu).
 int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, int aux,
                         uint8_t* packed, double* xmin, double* xmax, int32_t* info0,
-                        int32_t* status, cudaStream_t s, std::string& err);
+                        int32_t* status, cudaStream_t s, std::string& err, int b, int32_t* info1,
+                        double* norm);
 
 // Row-wise KMEANS codebooks (eq4_kmeans.cu).
 int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int aux, uint8_t* out,

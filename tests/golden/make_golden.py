@@ -406,8 +406,33 @@ def make_kmeans():
     print("kmeans: done", len(tables), "tables")
 
 
+def make_hist_apprx():
+    """HIST-APPRX windows (histclip.py:181-217) from the reference.  Its norms go through
+    numpy's SIMD pow and are host-dependent in the last bit, so only the windows, ranges and
+    packed rows are recorded."""
+    tables = {"gauss64": gaussian_rows(701, 150, 64), "lap64": laplacian_rows(702, 100, 64, 0.4),
+              "mixed33": mixed_table(100, 33, 703)}
+    out = {}
+    for tname, x in tables.items():
+        out[f"x_{tname}"] = x
+        for b in (200, 40, 8):
+            st, ns, lo, hi = [], [], [], []
+            for row in x:
+                h = eq.hist_apprx_search(row, b)
+                st.append(h.start_bin); ns.append(h.nbins_selected)
+                lo.append(h.clip_range.xmin); hi.append(h.clip_range.xmax)
+            out[f"win_{tname}_{b}"] = np.array([st, ns])
+            out[f"range_{tname}_{b}"] = np.array([lo, hi])
+        q = eq.quantize_table(eq.EmbeddingTable(x), "hist-apprx", 4, "fp16")
+        out[f"packed_{tname}"] = eq.pack_table4(q).buffer.copy()
+    np.savez_compressed(os.path.join(HERE, "hist_apprx.npz"), **out)
+    print("hist_apprx: done")
+
+
 if __name__ == "__main__":
-    which = sys.argv[2:] or ["mse", "edge", "hist", "config1", "sls", "files", "methods", "kmeans"]
+    which = sys.argv[2:] or ["mse", "edge", "hist", "config1", "sls", "files", "methods", "kmeans",
+                             "hist_apprx"]
     for w in which:
         {"mse": make_mse, "edge": make_edge, "hist": make_hist, "config1": make_config1,
-         "sls": make_sls, "files": make_files, "methods": make_methods, "kmeans": make_kmeans}[w]()
+         "sls": make_sls, "files": make_files, "methods": make_methods, "kmeans": make_kmeans,
+         "hist_apprx": make_hist_apprx}[w]()

@@ -62,7 +62,7 @@ def test_off_path_schemes_and_methods_raise(tmp_path):
     t = tmp_path / "t.embt"
     t.write_bytes(f["embt"].tobytes())
     with pytest.raises(ValueError, match="not on the B200 hot path"):
-        eq.quantize_file(t, tmp_path / "o.embq", "hist-apprx")
+        eq.quantize_file(t, tmp_path / "o.embq", "kmeans-cls")
     with pytest.raises(ValueError, match="unknown method"):
         eq.quantize_file(t, tmp_path / "o.embq", "nope")
     with pytest.raises(ValueError, match=r"r must be in \(0, 1\]"):

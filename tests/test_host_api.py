@@ -90,7 +90,7 @@ def test_greedy_parameter_errors_match_reference(ref):
 
 def test_methods_off_the_hot_path_raise_instead_of_falling_back():
     t = np.ones((2, 4), np.float32)
-    for m in ("hist-apprx", "kmeans-cls"):
+    for m in ("kmeans-cls",):
         with pytest.raises(ValueError, match="not on the B200 hot path"):
             eq.quantize_table(t, m)
     with pytest.raises(ValueError, match="not on the B200 hot path"):
