@@ -1742,7 +1742,7 @@ int eq4_quantize_file(const char* in_path, const char* out_path, int method, int
                       int aux, int64_t chunk_rows, int64_t* bad_row, double* bad_lohi) {
   if (!in_path || !out_path) return fail(EQ4_EINVAL, "null path");
   if (aux != EQ4_AUX_FP16 && aux != EQ4_AUX_FP32) return fail(EQ4_EINVAL, "aux must be fp32 or fp16");
-  if (method != EQ4_METHOD_ASYM && method != EQ4_METHOD_GREEDY && method != EQ4_METHOD_HIST_BRUTE)
+  if (method < EQ4_METHOD_ASYM || method > EQ4_METHOD_HIST_APPRX)
     return fail(EQ4_EINVAL, "unknown method " + std::to_string(method));
   std::string err;
   const int rc = eq4_io_quantize_file(in_path, out_path, method, b, r, aux, chunk_rows, bad_row,
@@ -2091,3 +2091,23 @@ long long eq4_selftest(int which, int64_t n, uint64_t seed) {
 }
 
 }  // extern "C"
+
+// Internal entry points for the streaming file pipeline (eq4_io.cu): the TABLE
+// range must cover the whole file, so it is accumulated over a first pass.
+int eq4_internal_table_init(int* keys, cudaStream_t s) {
+  k_table_init<<<1, 1, 0, s>>>(keys);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? EQ4_OK : cuda_fail(e, "k_table_init");
+}
+int eq4_internal_table_accumulate(const float* x, int64_t rows, int64_t dim, int* keys,
+                                  cudaStream_t s) {
+  return table_keys_accumulate(x, rows, dim, dim, keys, s);
+}
+int eq4_internal_quantize_pack_keys(const float* x, int64_t rows, int64_t dim, int method, int b,
+                                    double r, int aux, uint8_t* packed, int32_t* info0,
+                                    int32_t* status, cudaStream_t s, const int* keys) {
+  return quantize_pack_impl(x, rows, dim, dim, method, b, r, aux, packed, nullptr, nullptr, info0,
+                            nullptr, nullptr, status, s, keys);
+}
+
+

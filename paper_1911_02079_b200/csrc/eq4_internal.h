@@ -32,3 +32,11 @@ int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, i
 // Row-wise KMEANS codebooks (eq4_kmeans.cu).
 int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int aux, uint8_t* out,
                       int32_t* iters, int32_t* status, cudaStream_t s, std::string& err);
+
+// TABLE-range helpers for the file pipeline (eq4.cu).
+int eq4_internal_table_init(int* keys, cudaStream_t s);
+int eq4_internal_table_accumulate(const float* x, int64_t rows, int64_t dim, int* keys,
+                                  cudaStream_t s);
+int eq4_internal_quantize_pack_keys(const float* x, int64_t rows, int64_t dim, int method, int b,
+                                    double r, int aux, uint8_t* packed, int32_t* info0,
+                                    int32_t* status, cudaStream_t s, const int* keys);

@@ -175,6 +175,27 @@ int eq4_io_quantize_file(const char* in_path, const char* out_path, int method, 
     cuda_check(cudaMalloc(&dst[i], 4), "cudaMalloc");
     cuda_check(cudaMalloc(&di0[i], chunk * 4), "cudaMalloc");
   }
+  // TABLE (clipping.py:64-67): one range over the whole file -> a first streaming pass
+  int* tkeys = nullptr;
+  if (rc == EQ4_OK && method == EQ4_METHOD_TABLE) {
+    cuda_check(cudaMalloc(&tkeys, 8), "cudaMalloc");
+    if (rc == EQ4_OK) rc = eq4_internal_table_init(tkeys, st[0]);
+    for (int64_t c = 0; c < nchunks && rc == EQ4_OK; c++) {
+      const int i = (int)(c % NS);
+      if (!cuda_check(cudaStreamSynchronize(st[i]), "stream sync")) break;   // hin[i] free again
+      const int64_t r0 = c * chunk, nr = std::min(chunk, rows - r0);
+      if (!read_parallel(in.fd, hin[i], (size_t)(nr * dim * 4), (off_t)(EMBT_HEADER + r0 * dim * 4))) {
+        err = sys_err("read", in_path);
+        rc = EQ4_EINVAL;
+        break;
+      }
+      if (!cuda_check(cudaMemcpyAsync(dx[i], hin[i], nr * dim * 4, cudaMemcpyHostToDevice, st[i]), "H2D"))
+        break;
+      if (i != 0 && !cuda_check(cudaStreamSynchronize(st[0]), "stream sync")) break;  // keys init
+      rc = eq4_internal_table_accumulate(dx[i], nr, dim, tkeys, st[i]);
+    }
+    for (int i = 0; i < NS && rc == EQ4_OK; i++) cuda_check(cudaStreamSynchronize(st[i]), "stream sync");
+  }
   // c: read + enqueue chunk c; before reusing buffer pair c % NS, drain chunk c - NS
   int64_t pending[NS] = {-1, -1};
   auto drain = [&](int i) {
@@ -201,8 +222,8 @@ int eq4_io_quantize_file(const char* in_path, const char* out_path, int method, 
     if (!cuda_check(cudaMemcpyAsync(dx[i], hin[i], nr * dim * 4, cudaMemcpyHostToDevice, st[i]), "H2D"))
       break;
     if (!cuda_check(cudaMemsetAsync(dst[i], 0, 4, st[i]), "memset")) break;
-    const int krc = eq4_quantize_pack(dx[i], nr, dim, dim, method, b, r, aux, dq[i], nullptr, nullptr,
-                                      di0[i], nullptr, nullptr, dst[i], st[i]);
+    const int krc = eq4_internal_quantize_pack_keys(dx[i], nr, dim, method, b, r, aux, dq[i], di0[i],
+                                                    dst[i], st[i], tkeys);
     if (krc != EQ4_OK) {
       err = eq4_last_error();
       rc = krc;
@@ -266,6 +287,7 @@ int eq4_io_quantize_file(const char* in_path, const char* out_path, int method, 
     if (st[i]) cudaStreamDestroy(st[i]);
   }
   if (hstatus) cudaFreeHost(hstatus);
+  if (tkeys) cudaFree(tkeys);
   if (rc != EQ4_OK) unlink(out_path);   // no partial container on failure
   return rc;
 }

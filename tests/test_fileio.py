@@ -130,3 +130,19 @@ def test_write_embq_from_device_streams_hbm(tmp_path):
     host = tmp_path / "host.embq"
     eq.write_embq(host, eq.PackedTable4(p.rows, p.dim, "fp16", buffer=p.device_buffer.cpu().numpy()))
     assert dev.read_bytes() == host.read_bytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("method", ["table", "sym", "gss", "hist-apprx"])
+def test_quantize_file_other_methods_span_chunks(tmp_path, method):
+    """TABLE's single range must cover the whole file, not each streamed chunk."""
+    from oracle import rng
+
+    x = rng.mixed_table(9000, 24, 3)
+    x[8500] *= 50.0                      # the table extremes sit in the last chunk
+    src = tmp_path / "t.embt"
+    eq.write_embt(src, x)
+    out = tmp_path / "t.embq"
+    eq.quantize_file(src, out, method, "fp32", chunk_rows=1000)
+    want = oracle.quantize_pack_table(x, method, 200, 0.16, "fp32").packed
+    assert out.read_bytes()[26:] == want.tobytes()
