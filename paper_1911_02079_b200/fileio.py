@@ -154,6 +154,11 @@ def quantize_file(in_path, out_path, method: str, aux_precision: str = "fp32", b
     non-finite payload raises read_embt's DataError and leaves no output file."""
     if method not in ALL_METHODS:
         raise ValueError(f"unknown method {method!r}; expected one of {ALL_METHODS}")
+    if method == "kmeans":                                     # codebook.py:164-172, kmeans_row
+        from .codebook import quantize_table_kmeans
+
+        write_embq(out_path, quantize_table_kmeans(read_embt(in_path), aux_precision))
+        return
     if method not in GPU_METHODS:
         raise ValueError(f"{method!r} with nbits=4 is not on the B200 hot path "
                          f"(supported: {GPU_METHODS} at nbits=4)")

@@ -146,3 +146,14 @@ def test_quantize_file_other_methods_span_chunks(tmp_path, method):
     eq.quantize_file(src, out, method, "fp32", chunk_rows=1000)
     want = oracle.quantize_pack_table(x, method, 200, 0.16, "fp32").packed
     assert out.read_bytes()[26:] == want.tobytes()
+
+
+@pytest.mark.gpu
+def test_quantize_file_kmeans_matches_reference_container(tmp_path):
+    f = np.load(os.path.join(G, "kmeans.npz"))
+    x = f["x_gauss64"]
+    src = tmp_path / "k.embt"
+    eq.write_embt(src, x)
+    out = tmp_path / "k.embq"
+    eq.quantize_file(src, out, "kmeans", "fp16")
+    assert out.read_bytes() == f["embq_gauss64_fp16"].tobytes()
