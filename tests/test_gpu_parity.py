@@ -296,3 +296,26 @@ def test_greedy_other_b_r_vs_oracle(eq, b, r):
     assert np.array_equal(p.buffer, want.packed)
     assert np.array_equal(rr.xmin.cpu().numpy(), want.xmin)
     assert np.array_equal(rr.xmax.cpu().numpy(), want.xmax)
+
+
+@pytest.mark.slow
+def test_large_table_beyond_int32_elements(eq):
+    """rows * d > 2^31 (40M x 64 = 10.2 GB): 64-bit addressing in the GREEDY and ASYM kernels;
+    a strided sample of rows (incl. the last) against the oracle."""
+    import torch
+
+    from paper_1911_02079_b200 import workloads
+
+    rows, d = 40_000_000, 64
+    x = workloads.mixed_table(rows, d, 77)
+    idx = np.unique(np.concatenate([np.arange(0, rows, 997_331), [rows - 1, rows - 2, 2 ** 31 // d]]))
+    xs = x[torch.from_numpy(idx).cuda()].cpu().numpy()
+    stride = eq.packed_row_stride(d, "fp16")
+    for method in ("greedy", "asym"):
+        p, rr = eq.quantize_pack_table4(x, method, "fp16", with_rows=True)
+        want = oracle.quantize_pack_table(xs, method, 200, 0.16, "fp16")
+        buf = p.device_buffer.view(rows, stride)[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1)
+        assert np.array_equal(buf, want.packed), method
+        assert np.array_equal(rr.xmin[torch.from_numpy(idx).cuda()].cpu().numpy(), want.xmin)
+        del p, rr
+        torch.cuda.empty_cache()
