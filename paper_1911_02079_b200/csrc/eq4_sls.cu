@@ -357,8 +357,39 @@ __device__ __forceinline__ void accumulate_tile(const SlsParams& p, int64_t tile
         acc[m] = sls::pk((before && j < d) ? p.carry[(tile - 1) * d + j] : 0.f,
                          (before && j + 1 < d) ? p.carry[(tile - 1) * d + j + 1] : 0.f);
       }
+      int rbeg = r0;
+      if (words && M == 1 && b0 + lane < half) {
+        // aligned rows, one byte (two codes) per lane: 8 rows' values are formed
+        // independently, then added to the running sum in query order
+        sls::f2 a = acc[0];
+        const int b = b0 + lane;
+        for (; rbeg + 8 <= r1; rbeg += 8) {
+          sls::f2 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint8_t* row = buf + (size_t)(rbeg + u) * stride;
+            const uint32_t* aw = reinterpret_cast<const uint32_t*>(row + half);
+            float sc, bi;
+            if (ab == 2) {
+              const uint32_t w = aw[0];
+              sc = __half2float(__ushort_as_half((unsigned short)(w & 0xffffu)));
+              bi = __half2float(__ushort_as_half((unsigned short)(w >> 16)));
+            } else {
+              sc = __uint_as_float(aw[0]);
+              bi = __uint_as_float(aw[1]);
+            }
+            const uint32_t c = row[b];
+            const float c0 = __fadd_rn(__uint_as_float((c & 0xFu) | 0x4B000000u), -8388608.f);
+            const float c1 = __fadd_rn(__uint_as_float((c >> 4) | 0x4B000000u), -8388608.f);
+            v[u] = sls::add(sls::pk(__fmul_rn(sc, c0), __fmul_rn(sc, c1)), sls::pk(bi, bi));
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) a = sls::add(a, v[u]);
+        }
+        acc[0] = a;
+      }
 #pragma unroll 8
-      for (int r = r0; r < r1; ++r) {   // unrolled: the shared-memory loads of 8 rows in flight
+      for (int r = rbeg; r < r1; ++r) {   // unrolled: the shared-memory loads of 8 rows in flight
         const uint8_t* row = buf + (size_t)r * stride;
         float sc, bi;
         if (words) {
