@@ -1597,10 +1597,9 @@ template <int METHOD, int LPR, int E, bool VEC>
 static int launch_rq(const Params& p, cudaStream_t s) {
   if constexpr (METHOD == M_ASYM) {
     if constexpr (VEC && E <= 16) {
-      const char* bv = getenv("EQ4_ASYM_BULK");
       // contiguous rows of >= 32 floats: bulk-copy ring (d = 16 rows make 1 KB blocks,
       // where the register double buffer measured faster)
-      if (LPR * E >= 32 && p.ld == p.d && !(bv && bv[0] == '0')) {
+      if (LPR * E >= 32 && p.ld == p.d) {
         using B = SliceB<LPR, E>;
         const int64_t nt = (p.rows + B::RPW * NWARPS - 1) / (B::RPW * NWARPS);
         const size_t sm = NWARPS * B::bytes();
@@ -1655,37 +1654,18 @@ static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
     if (d <= 2048) return launch_rq<METHOD, 32, 64, false>(p, s);
     return fail(EQ4_EUNSUPPORTED, "dim > 2048 is not supported by the B200 path");
   } else {
-  // GREEDY: 32 elements per lane amortise the per-iteration decision work
-  // (measured best on 20M x 64; the row slice lives in shared memory)
+  // GREEDY: 64 elements per lane amortise the per-iteration decision work best
+  // (measured on 20M x 64 and the 1 GiB d-sweep against 32 per lane; the row
+  // slice lives in shared memory)
   if (vec) {
     switch (d) {
       case 16: return launch_rq<METHOD, 1, 16, true>(p, s);
       case 32: return launch_rq<METHOD, 1, 32, true>(p, s);
-      case 64: {
-        const char* v = getenv("EQ4_G64");   // layout experiments
-        if (v && v[0] == '2') return launch_rq<METHOD, 2, 32, true>(p, s);
-        return launch_rq<METHOD, 1, 64, true>(p, s);
-      }
-      case 128: {
-        const char* v = getenv("EQ4_G128");
-        if (v && v[0] == '4') return launch_rq<METHOD, 4, 32, true>(p, s);
-        return launch_rq<METHOD, 2, 64, true>(p, s);
-      }
-      case 256: {
-        const char* v = getenv("EQ4_GW");
-        if (v && v[0] == '1') return launch_rq<METHOD, 8, 32, true>(p, s);
-        return launch_rq<METHOD, 4, 64, true>(p, s);
-      }
-      case 512: {
-        const char* v = getenv("EQ4_GW");
-        if (v && v[0] == '1') return launch_rq<METHOD, 16, 32, true>(p, s);
-        return launch_rq<METHOD, 8, 64, true>(p, s);
-      }
-      case 1024: {
-        const char* v = getenv("EQ4_GW");
-        if (v && v[0] == '1') return launch_rq<METHOD, 32, 32, true>(p, s);
-        return launch_rq<METHOD, 16, 64, true>(p, s);
-      }
+      case 64: return launch_rq<METHOD, 1, 64, true>(p, s);
+      case 128: return launch_rq<METHOD, 2, 64, true>(p, s);
+      case 256: return launch_rq<METHOD, 4, 64, true>(p, s);
+      case 512: return launch_rq<METHOD, 8, 64, true>(p, s);
+      case 1024: return launch_rq<METHOD, 16, 64, true>(p, s);
       case 2048: return launch_rq<METHOD, 32, 64, true>(p, s);
       default: break;
     }
@@ -1693,11 +1673,11 @@ static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
   if (d <= 8) return launch_rq<METHOD, 1, 8, false>(p, s);
   if (d <= 16) return launch_rq<METHOD, 1, 16, false>(p, s);
   if (d <= 32) return launch_rq<METHOD, 1, 32, false>(p, s);
-  if (d <= 64) return launch_rq<METHOD, 2, 32, false>(p, s);
-  if (d <= 128) return launch_rq<METHOD, 4, 32, false>(p, s);
-  if (d <= 256) return launch_rq<METHOD, 8, 32, false>(p, s);
-  if (d <= 512) return launch_rq<METHOD, 16, 32, false>(p, s);
-  if (d <= 1024) return launch_rq<METHOD, 32, 32, false>(p, s);
+  if (d <= 64) return launch_rq<METHOD, 1, 64, false>(p, s);
+  if (d <= 128) return launch_rq<METHOD, 2, 64, false>(p, s);
+  if (d <= 256) return launch_rq<METHOD, 4, 64, false>(p, s);
+  if (d <= 512) return launch_rq<METHOD, 8, 64, false>(p, s);
+  if (d <= 1024) return launch_rq<METHOD, 16, 64, false>(p, s);
   if (d <= 2048) return launch_rq<METHOD, 32, 64, false>(p, s);
   return fail(EQ4_EUNSUPPORTED, "dim > 2048 is not supported by the B200 path");
   }
