@@ -296,6 +296,26 @@ def secondary(eq, workloads, torch, dev, peaks):
             r["hbm_frac"] = r["GBps"] / float(peaks.get("hbm_gbs", 6546.9))
         res[name] = r
         del x, out
+    # config 4: HIST-BRUTE b=200 on 16,384 x 64 N(0,1) (compute-bound, no roofline target):
+    # per-row time and the reference's bin-visit counter rate (histclip.py:162-164)
+    x = workloads.gaussian_table(16384, 64, 7, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    out = torch.empty(16384 * eq.packed_row_stride(64, AUX), dtype=torch.uint8, device=dev)
+    f = lambda: eq.quantize_pack_table4(x, "hist-brute", AUX, 200, out=out, status=st, check=False)
+    for _ in range(2):
+        f()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(5):
+        f()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / 5
+    visits = 16384 * 200 * (200 * 201 // 2)
+    res["hist_brute_16384x64_config4"] = {"ms": ms, "us_per_row": ms * 1e3 / 16384,
+                                          "bin_visits_per_s": visits / ms * 1e3}
+    del x, out
     return res
 
 
