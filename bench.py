@@ -200,9 +200,22 @@ def run_ours(args, rank: int, world: int):
     # end to end through the public API: pinned host table in, packed bytes out
     e2e = None
     if not args.no_e2e:
-        xh = torch.empty((rows, DIM), dtype=torch.float32, pin_memory=True)
+        # every rank pins its own table + output; all ranks agree before any collective
+        ok, why = 1, ""
+        try:
+            xh = torch.empty((rows, DIM), dtype=torch.float32, pin_memory=True)
+            oh = torch.empty(rows * stride, dtype=torch.uint8, pin_memory=True)
+        except RuntimeError as ex:
+            ok, why = 0, f"pinned host allocation failed: {ex}".splitlines()[0]
+        if dist:
+            okt = torch.tensor([ok], device=dev)
+            torch.distributed.all_reduce(okt, op=torch.distributed.ReduceOp.MIN)
+            ok = int(okt.item())
+        if not ok:
+            e2e = {"value": None, "unit": "rows/s", "h2d_bytes_per_step": rows * DIM * 4,
+                   "d2h_bytes_per_step": rows * stride, "error": why or "a rank could not pin its table"}
+    if not args.no_e2e and e2e is None:
         xh.copy_(x)
-        oh = torch.empty(rows * stride, dtype=torch.uint8, pin_memory=True)
         table = eq.EmbeddingTable(xh.numpy())   # validated once, like the reference's constructor
         del x
         torch.cuda.empty_cache()
