@@ -23,7 +23,9 @@
 // differently.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <map>
 #include <mutex>
@@ -87,6 +89,43 @@ struct HistSlice {
   __host__ __device__ size_t codes_off() const { return xs_off() + (size_t)d * 4; }         // u8[d]
   __host__ __device__ size_t bytes() const { return (codes_off() + (size_t)d + 15) & ~(size_t)15; }
 };
+
+// codes (uniform.py:60-80) + packed row (packed.py:68-83) + per-row outputs.  Warp-collective.
+__device__ __forceinline__ void hist_emit(const HistParams& p, int64_t row, int d, int lane, bool bad,
+                                          const float* xs, uint8_t* codes, double wlo, double whi,
+                                          int best_s, int best_n, double norm) {
+  const bool ok = !bad;
+  const CodeParams cp = make_code_params(ok ? wlo : 0.0, ok ? whi : 0.0);
+  for (int k = lane; k < d; k += 32) {
+    bool ne;
+    unsigned c = code_of(xs[k], cp, ne);
+    if (ne) c = code_exact(xs[k], cp);
+    codes[k] = ok ? (uint8_t)c : 0;
+  }
+  __syncwarp();
+  uint8_t* orow = p.packed + row * (int64_t)p.stride;
+  for (int m = lane; m < p.half; m += 32) {
+    const unsigned c0 = codes[2 * m];
+    const unsigned c1 = (2 * m + 1 < d) ? codes[2 * m + 1] : 0u;
+    orow[m] = (uint8_t)(c0 | (c1 << 4));
+  }
+  if (lane == 0) {
+    const double sc = (ok && whi != wlo) ? div15(__dsub_rn(whi, wlo)) : 0.0;
+    uint8_t* a = orow + p.half;
+    if (p.aux == EQ4_AUX_FP16) {
+      const uint32_t s16 = aux_bits_f16(sc), b16 = aux_bits_f16(wlo);
+      a[0] = s16 & 0xff; a[1] = s16 >> 8; a[2] = b16 & 0xff; a[3] = b16 >> 8;
+    } else {
+      const uint32_t s32 = aux_bits_f32(sc), b32 = aux_bits_f32(wlo);
+      for (int k = 0; k < 4; ++k) { a[k] = (s32 >> (8 * k)) & 0xff; a[4 + k] = (b32 >> (8 * k)) & 0xff; }
+    }
+    if (p.lo_out) { p.lo_out[row] = wlo; p.hi_out[row] = whi; }
+    if (p.info0) p.info0[row] = best_s;
+    if (p.info1) p.info1[row] = best_n;
+    if (p.norm_out) p.norm_out[row] = norm;
+  }
+  __syncwarp();
+}
 
 __global__ void __launch_bounds__(32) k_hist(const HistParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -172,7 +211,7 @@ __global__ void __launch_bounds__(32) k_hist(const HistParams p) {
           double acc = 0.0;
           const int i1 = lb[s + n];
           for (int i = lb[s]; i < i1; i++) acc = fma(nzc[i], __ldg(Un + (nzj[i] - s)), acc);
-          const double v = (A3[s] + R3[s + n]) * (1.0 / 3.0) + acc;
+          const double v = __fma_rn(__dadd_rn(A3[s], R3[s + n]), 1.0 / 3.0, acc);   // one rounding
           if (v < bv) { bv = v; bn = n; bs = s; }
         }
       }
@@ -188,38 +227,188 @@ __global__ void __launch_bounds__(32) k_hist(const HistParams p) {
       whi = __dadd_rn(lo, __dmul_rn(w, (double)(bs + bn)));
       norm = bv * w * w;
     }
-    // ---- codes (uniform.py:60-80) + packed row (packed.py:68-83) ----
-    const bool ok = !bad;
-    const CodeParams cp = make_code_params(ok ? wlo : 0.0, ok ? whi : 0.0);
+    hist_emit(p, row, d, lane, bad, xs, codes, wlo, whi, best_s, best_n, norm);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_hist_s: the same search with the U table resident in shared memory (one
+// copy per block, shared by NW row-warps), so the window loop's gathers are
+// shared-memory loads instead of L2 round trips.  The per-row preparation is
+// warp-parallel: non-empty bins by ballot compaction, and the outside-window
+// sums from prefix sums of c, c*j, c*j^2 over the bins:
+//   3L(t) = sum_{j<t} c_j (3m^2 - 3m + 1), m = t - j
+//         = P0 (3t^2 - 3t + 1) + P1 (3 - 6t) + 3 P2          (P = prefix sums over j < t)
+//   3R(t) = sum_{j>=t} c_j (3k^2 + 3k + 1), k = j - t
+//         = (T0-P0)(3t^2 - 3t + 1) + (T1-P1)(3 - 6t) + 3(T2-P2)
+// all exact integers in float64, so every window's value is bit-identical to
+// k_hist's (same fma order over the non-empty bins inside the window).
+// ---------------------------------------------------------------------------
+struct HistSliceS {
+  int b, d, m;   // m = min(b, d): most non-empty bins a row can have
+  __host__ __device__ size_t a3_off() const { return 0; }                                   // double[b+1]
+  __host__ __device__ size_t r3_off() const { return a3_off() + (size_t)(b + 1) * 8; }      // double[b+1]
+  __host__ __device__ size_t nzc_off() const { return r3_off() + (size_t)(b + 1) * 8; }     // double[m]
+  __host__ __device__ size_t cnt_off() const { return nzc_off() + (size_t)m * 8; }          // int[b]
+  __host__ __device__ size_t lb_off() const { return cnt_off() + (size_t)b * 4; }           // int[b+1]
+  __host__ __device__ size_t nzj_off() const { return lb_off() + (size_t)(b + 1) * 4; }     // int[m]
+  __host__ __device__ size_t xs_off() const { return nzj_off() + (size_t)m * 4; }           // float[d]
+  __host__ __device__ size_t codes_off() const { return xs_off() + (size_t)d * 4; }         // u8[d]
+  __host__ __device__ size_t bytes() const { return (codes_off() + (size_t)d + 15) & ~(size_t)15; }
+};
+
+__host__ __device__ inline size_t hist_u_bytes(int b) { return (((size_t)b * (b + 1) / 2) * 8 + 15) & ~(size_t)15; }
+
+__device__ __forceinline__ double warp_incl_scan(double v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v = __dadd_rn(v, t);
+  }
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+
+__global__ void __launch_bounds__(512) k_hist_s(const HistParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int b = p.b, d = p.d;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const HistSliceS S{b, d, min(b, d)};
+  // the whole U table, once per block
+  double* Us = reinterpret_cast<double*>(smem);
+  {
+    const size_t nu = (size_t)b * (b + 1) / 2;
+    for (size_t k = threadIdx.x; k < nu; k += blockDim.x) Us[k] = __ldg(p.U + k);
+  }
+  __syncthreads();
+  unsigned char* ws = smem + hist_u_bytes(b) + (size_t)warp * S.bytes();
+  double* A3 = reinterpret_cast<double*>(ws + S.a3_off());
+  double* R3 = reinterpret_cast<double*>(ws + S.r3_off());
+  double* nzc = reinterpret_cast<double*>(ws + S.nzc_off());
+  int* cnt = reinterpret_cast<int*>(ws + S.cnt_off());
+  int* lb = reinterpret_cast<int*>(ws + S.lb_off());
+  int* nzj = reinterpret_cast<int*>(ws + S.nzj_off());
+  float* xs = reinterpret_cast<float*>(ws + S.xs_off());
+  uint8_t* codes = ws + S.codes_off();
+
+  for (int64_t row = (int64_t)blockIdx.x * nw + warp; row < p.rows; row += (int64_t)gridDim.x * nw) {
+    // ---- row, min/max, finiteness ----
+    float mn = INFINITY, mx = -INFINITY;
+    bool bad = false;
     for (int k = lane; k < d; k += 32) {
-      bool ne;
-      unsigned c = code_of(xs[k], cp, ne);
-      if (ne) c = code_exact(xs[k], cp);
-      codes[k] = ok ? (uint8_t)c : 0;
+      const float v = p.x[row * p.ld + k];
+      xs[k] = v;
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+      bad |= !isfinite(v);
     }
-    __syncwarp();
-    uint8_t* orow = p.packed + row * (int64_t)p.stride;
-    for (int m = lane; m < p.half; m += 32) {
-      const unsigned c0 = codes[2 * m];
-      const unsigned c1 = (2 * m + 1 < d) ? codes[2 * m + 1] : 0u;
-      orow[m] = (uint8_t)(c0 | (c1 << 4));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(FULL, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
     }
-    if (lane == 0) {
-      const double sc = (ok && whi != wlo) ? div15(__dsub_rn(whi, wlo)) : 0.0;
-      uint8_t* a = orow + p.half;
-      if (p.aux == EQ4_AUX_FP16) {
-        const uint32_t s16 = aux_bits_f16(sc), b16 = aux_bits_f16(wlo);
-        a[0] = s16 & 0xff; a[1] = s16 >> 8; a[2] = b16 & 0xff; a[3] = b16 >> 8;
-      } else {
-        const uint32_t s32 = aux_bits_f32(sc), b32 = aux_bits_f32(wlo);
-        for (int k = 0; k < 4; ++k) { a[k] = (s32 >> (8 * k)) & 0xff; a[4 + k] = (b32 >> (8 * k)) & 0xff; }
+    bad = __any_sync(FULL, bad);
+    if (bad && lane == 0 && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
+    const double lo = (double)mn, hi = (double)mx;
+    double wlo = lo, whi = hi, norm = 0.0;
+    int best_s = 0, best_n = 1;
+    if (!bad && lo != hi) {
+      // ---- histogram (histclip.py:52-67), float64 bin index ----
+      const double w = __ddiv_rn(__dsub_rn(hi, lo), (double)b);
+      for (int j = lane; j < b; j += 32) cnt[j] = 0;
+      __syncwarp();
+      for (int k = lane; k < d; k += 32) {
+        const double q = floor(__ddiv_rn(__dsub_rn((double)xs[k], lo), w));
+        const int idx = (int)np_clip(q, 0.0, (double)(b - 1));
+        atomicAdd(&cnt[idx], 1);
       }
-      if (p.lo_out) { p.lo_out[row] = wlo; p.hi_out[row] = whi; }
-      if (p.info0) p.info0[row] = best_s;
-      if (p.info1) p.info1[row] = best_n;
-      if (p.norm_out) p.norm_out[row] = norm;
+      __syncwarp();
+      // ---- non-empty bins by ballot compaction; lb[x] = #non-empty bins below x ----
+      int m = 0;
+      double t1 = 0.0, t2 = 0.0;
+      for (int base = 0; base < b; base += 32) {
+        const int j = base + lane;
+        const int c = j < b ? cnt[j] : 0;
+        const unsigned bal = __ballot_sync(FULL, c != 0);
+        const int pos = m + __popc(bal & ((1u << lane) - 1u));
+        if (j < b) lb[j] = pos;
+        if (c) { nzc[pos] = (double)c; nzj[pos] = j; }
+        t1 += (double)c * j;
+        t2 += (double)c * j * j;
+        m += __popc(bal);
+      }
+      if (lane == 0) lb[b] = m;
+      const double T0 = (double)d, T1 = warp_sum_d(t1), T2 = warp_sum_d(t2);
+      // ---- outside-window parts 3L(t), 3R(t) for t = 0..b from prefix sums ----
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0;   // carries: sums over bins below the chunk
+      for (int base = 0; base <= b; base += 32) {
+        const int t = base + lane;
+        const double c = (t < b) ? (double)cnt[t] : 0.0;
+        const double i0 = warp_incl_scan(c, lane), i1 = warp_incl_scan(c * t, lane),
+                     i2 = warp_incl_scan(c * t * t, lane);
+        const double P0 = c0 + (i0 - c), P1 = c1 + (i1 - c * t), P2 = c2 + (i2 - c * t * t);
+        const double tt = (double)t;
+        const double q2 = 3.0 * tt * tt - 3.0 * tt + 1.0, q1 = 3.0 - 6.0 * tt;
+        if (t <= b) {
+          A3[t] = P0 * q2 + P1 * q1 + 3.0 * P2;
+          R3[t] = (T0 - P0) * q2 + (T1 - P1) * q1 + 3.0 * (T2 - P2);
+        }
+        c0 += __shfl_sync(FULL, i0, 31);
+        c1 += __shfl_sync(FULL, i1, 31);
+        c2 += __shfl_sync(FULL, i2, 31);
+      }
+      __syncwarp();
+      // ---- every window, first minimum in (n asc, s asc) order ----
+      // Pruning: v = (A3 + R3)/3 + acc with acc >= 0, so a window whose outside
+      // part alone exceeds a value some window attains cannot be the minimum
+      // (strict >, so equal values -- first-minimum ties -- are still scored).
+      // The bound starts at the full window's value (scored exactly as the scan
+      // scores it) and tightens to the warp's running minimum after every width.
+      double bound;
+      {
+        const double* Ub = Us + (size_t)(b - 1) * b / 2;
+        double acc = 0.0;
+        if (lane == 0)
+          for (int i = 0; i < m; i++) acc = fma(nzc[i], Ub[nzj[i]], acc);
+        bound = __shfl_sync(FULL, __fma_rn(__dadd_rn(A3[0], R3[b]), 1.0 / 3.0, acc), 0);
+      }
+      double bv = INFINITY;
+      int bn = 1 << 30, bs = 1 << 30;
+      for (int n = 1; n <= b; n++) {
+        const double* Un = Us + (size_t)(n - 1) * n / 2;
+        for (int s = lane; s <= b - n; s += 32) {
+          if (__dmul_rn(__dadd_rn(A3[s], R3[s + n]), 1.0 / 3.0) > bound) continue;   // <= v
+          double acc = 0.0;
+          const int i1 = lb[s + n];
+          const double* Ub = Un - s;
+#pragma unroll 4
+          for (int i = lb[s]; i < i1; i++) acc = fma(nzc[i], Ub[nzj[i]], acc);
+          const double v = __fma_rn(__dadd_rn(A3[s], R3[s + n]), 1.0 / 3.0, acc);   // one rounding
+          if (v < bv) { bv = v; bn = n; bs = s; }
+        }
+        double wm = bv;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) wm = fmin(wm, __shfl_xor_sync(FULL, wm, o));
+        bound = fmin(bound, wm);
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const double ov = __shfl_xor_sync(FULL, bv, o);
+        const int on = __shfl_xor_sync(FULL, bn, o), os = __shfl_xor_sync(FULL, bs, o);
+        if (ov < bv || (ov == bv && (on < bn || (on == bn && os < bs)))) { bv = ov; bn = on; bs = os; }
+      }
+      best_s = bs;
+      best_n = bn;
+      wlo = __dadd_rn(lo, __dmul_rn(w, (double)bs));                 // histclip.py:170
+      whi = __dadd_rn(lo, __dmul_rn(w, (double)(bs + bn)));
+      norm = bv * w * w;
     }
-    __syncwarp();
+    hist_emit(p, row, d, lane, bad, xs, codes, wlo, whi, best_s, best_n, norm);
   }
 }
 
@@ -260,6 +449,32 @@ int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b
   p.half = (int)((dim + 1) / 2);
   p.packed = packed; p.lo_out = xmin; p.hi_out = xmax; p.norm_out = norm;
   p.info0 = info0; p.info1 = info1; p.status = status; p.U = U;
+  int dev = 0, sms = 148, max_optin = 227 * 1024;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  // preferred: U resident in shared memory, as many row-warps per block as fit (>= 4)
+  const char* legacy = getenv("EQ4_HIST_LEGACY");   // A/B switch for the global-U kernel
+  {
+    const HistSliceS SS{b, (int)dim, (int)std::min<int64_t>(b, dim)};
+    const size_t ub = hist_u_bytes(b), per = SS.bytes();
+    int nw = 0;
+    if (ub + 4 * per <= (size_t)max_optin) nw = (int)std::min<size_t>(16, (max_optin - ub) / per);
+    if (nw >= 4 && !(legacy && legacy[0] == '1')) {
+      const size_t smem = ub + (size_t)nw * per;
+      cudaError_t e = cudaFuncSetAttribute(k_hist_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) { err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hist_s, nw * 32, smem);
+      if (occ < 1) occ = 1;
+      const int64_t need = (rows + nw - 1) / nw;
+      const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * occ));
+      k_hist_s<<<(unsigned)grid, nw * 32, smem, s>>>(p);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) { err = std::string("k_hist_s launch: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+      return EQ4_OK;
+    }
+  }
   const HistSlice S{b, (int)dim};
   const size_t smem = S.bytes();
   if (smem > 227 * 1024) { err = "hist-brute: row does not fit in shared memory"; return EQ4_EUNSUPPORTED; }
@@ -267,9 +482,7 @@ int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b
     cudaError_t e = cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) { err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
   }
-  int occ = 0, dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hist, 32, smem);
   if (occ < 1) occ = 1;
   const int64_t grid = std::min<int64_t>(rows, (int64_t)sms * occ);

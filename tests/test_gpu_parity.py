@@ -238,6 +238,26 @@ def test_hist_brute_vs_oracle_config4_sample(eq):
     assert len(ties) <= 1
 
 
+@pytest.mark.parametrize("b,d", [(8, 7), (16, 64), (40, 1), (64, 300), (200, 64), (200, 17), (200, 2048),
+                                 (250, 64), (400, 64)])
+def test_hist_brute_shared_table_kernel_matches_global_table_kernel(eq, b, d, monkeypatch):
+    """k_hist_s (U table in shared memory, warp-parallel prefix sums) against k_hist (U in
+    global memory, serial prep): bit-identical windows, norms, thresholds and packed rows.
+    b = 400 does not fit the shared table and exercises the fallback on both sides."""
+    x = rng.mixed_table(700, d, 99 + b)
+    x[3] = 2.5                       # constant row
+    x[5, : max(1, d // 2)] = -1.0    # ties in the histogram
+    outs = []
+    for legacy in ("1", "0"):
+        monkeypatch.setenv("EQ4_HIST_LEGACY", legacy)
+        p, rr = eq.quantize_pack_table4(_dev(x), "hist-brute", "fp16", b, with_rows=True)
+        torch.cuda.synchronize()
+        outs.append((p.buffer.copy(), rr.xmin.cpu().numpy(), rr.xmax.cpu().numpy(),
+                     rr.info0.cpu().numpy(), rr.info1.cpu().numpy(), rr.norm.cpu().numpy()))
+    for a, g in zip(*outs):
+        assert np.array_equal(a, g)
+
+
 def test_hist_brute_api_counters(eq):
     x = rng.gaussian_row(5, 64)
     c = eq.WorkCounters()
