@@ -602,9 +602,6 @@ __device__ __forceinline__ f2_t fma2_rm(f2_t a, f2_t b, f2_t c) {
 #ifndef G_UNROLL
 #define G_UNROLL 4
 #endif
-#ifndef G_PREFETCH
-#define G_PREFETCH 0
-#endif
 constexpr int kGUnroll = G_UNROLL;   // float4 chunks per trip of the element loop
 
 // One fast candidate: approximate loss (Y units) of base B, width W.  The row
@@ -729,17 +726,9 @@ __device__ __forceinline__ void eval_pair_x2_shift(const float4* ys4, float BL, 
   // eR = eL + (15 - W k):  k = [eL + 15 >= W/2] and [cL < 15]
   const float thr = -0.5f * nW - 15.f, cW = 15.f + nW, top = MAGIC + 15.f;   // ulp(2^23) = 1
   f2_t sL = pk2(0.f, 0.f), sR = pk2(0.f, 0.f);
-#if G_PREFETCH
-  ulonglong2 nx = *reinterpret_cast<const ulonglong2*>(ys4);
-#endif
 #pragma unroll kGUnroll
   for (int c = 0; c < E / 4; ++c) {
-#if G_PREFETCH
-    const ulonglong2 yy = nx;   // the next chunk's load is in flight while this one is evaluated
-    if (c + 1 < E / 4) nx = *reinterpret_cast<const ulonglong2*>(ys4 + (c + 1) * 32);
-#else
     const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32);
-#endif
 #pragma unroll
     for (int hlf = 0; hlf < 2; ++hlf) {
       const f2_t zL = add2(hlf ? yy.y : yy.x, nBL2);

@@ -76,20 +76,6 @@ struct HistParams {
   const double* U;
 };
 
-// Shared-memory slice of one row (one warp per block).
-struct HistSlice {
-  int b, d;
-  __host__ __device__ size_t cnt_off() const { return 0; }                                   // int[b]
-  __host__ __device__ size_t nzj_off() const { return cnt_off() + (size_t)b * 4; }          // int[b]
-  __host__ __device__ size_t lb_off() const { return nzj_off() + (size_t)b * 4; }           // int[b+1]
-  __host__ __device__ size_t a3_off() const { return (lb_off() + (size_t)(b + 1) * 4 + 7) & ~(size_t)7; }
-  __host__ __device__ size_t r3_off() const { return a3_off() + (size_t)(b + 1) * 8; }
-  __host__ __device__ size_t nzc_off() const { return r3_off() + (size_t)(b + 1) * 8; }     // double[b]
-  __host__ __device__ size_t xs_off() const { return nzc_off() + (size_t)b * 8; }           // float[d]
-  __host__ __device__ size_t codes_off() const { return xs_off() + (size_t)d * 4; }         // u8[d]
-  __host__ __device__ size_t bytes() const { return (codes_off() + (size_t)d + 15) & ~(size_t)15; }
-};
-
 // codes (uniform.py:60-80) + packed row (packed.py:68-83) + per-row outputs.  Warp-collective.
 __device__ __forceinline__ void hist_emit(const HistParams& p, int64_t row, int d, int lane, bool bad,
                                           const float* xs, uint8_t* codes, double wlo, double whi,
@@ -127,124 +113,22 @@ __device__ __forceinline__ void hist_emit(const HistParams& p, int64_t row, int 
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(32) k_hist(const HistParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const HistSlice S{p.b, p.d};
-  int* cnt = reinterpret_cast<int*>(smem + S.cnt_off());
-  int* nzj = reinterpret_cast<int*>(smem + S.nzj_off());
-  int* lb = reinterpret_cast<int*>(smem + S.lb_off());
-  double* A3 = reinterpret_cast<double*>(smem + S.a3_off());
-  double* R3 = reinterpret_cast<double*>(smem + S.r3_off());
-  double* nzc = reinterpret_cast<double*>(smem + S.nzc_off());
-  float* xs = reinterpret_cast<float*>(smem + S.xs_off());
-  uint8_t* codes = smem + S.codes_off();
-  const int lane = threadIdx.x;
-  const int b = p.b, d = p.d;
-
-  for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
-    // ---- row, min/max, finiteness ----
-    float mn = INFINITY, mx = -INFINITY;
-    bool bad = false;
-    for (int k = lane; k < d; k += 32) {
-      const float v = p.x[row * p.ld + k];
-      xs[k] = v;
-      mn = fminf(mn, v);
-      mx = fmaxf(mx, v);
-      bad |= !isfinite(v);
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      mn = fminf(mn, __shfl_xor_sync(FULL, mn, o));
-      mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
-    }
-    bad = __any_sync(FULL, bad);
-    if (bad && lane == 0 && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
-    const double lo = (double)mn, hi = (double)mx;
-    double wlo = lo, whi = hi, norm = 0.0;
-    int best_s = 0, best_n = 1;
-    if (!bad && lo != hi) {
-      // ---- histogram (histclip.py:52-67), float64 bin index ----
-      const double w = __ddiv_rn(__dsub_rn(hi, lo), (double)b);
-      for (int j = lane; j < b; j += 32) cnt[j] = 0;
-      __syncwarp();
-      for (int k = lane; k < d; k += 32) {
-        const double q = floor(__ddiv_rn(__dsub_rn((double)xs[k], lo), w));
-        const int idx = (int)np_clip(q, 0.0, (double)(b - 1));
-        atomicAdd(&cnt[idx], 1);
-      }
-      __syncwarp();
-      // ---- non-empty bins (ascending) and lb[x] = #non-empty bins below x ----
-      if (lane == 0) {
-        int m = 0;
-        for (int j = 0; j < b; j++) {
-          lb[j] = m;
-          if (cnt[j]) { nzj[m] = j; nzc[m] = (double)cnt[j]; m++; }
-        }
-        lb[b] = m;
-      }
-      __syncwarp();
-      const int nnz = lb[b];
-      // ---- outside-window parts: 3L(s) and 3R(e), exact integers in float64 ----
-      for (int t = lane; t <= b; t += 32) {
-        double a = 0.0, r = 0.0;
-        for (int i = 0; i < nnz; i++) {
-          const int j = nzj[i];
-          const double c = nzc[i];
-          if (j < t) {
-            const double m = (double)(t - j);                       // k = j - s = -m
-            a += c * (3.0 * m * m - 3.0 * m + 1.0);
-          } else {
-            const double k = (double)(j - t);                       // k - n >= 0
-            r += c * (3.0 * k * k + 3.0 * k + 1.0);
-          }
-        }
-        A3[t] = a;
-        R3[t] = r;
-      }
-      __syncwarp();
-      // ---- every window, first minimum in (n asc, s asc) order ----
-      double bv = INFINITY;
-      int bn = 1 << 30, bs = 1 << 30;
-      for (int n = 1; n <= b; n++) {
-        const double* Un = p.U + (size_t)(n - 1) * n / 2;
-        for (int s = lane; s <= b - n; s += 32) {
-          double acc = 0.0;
-          const int i1 = lb[s + n];
-          for (int i = lb[s]; i < i1; i++) acc = fma(nzc[i], __ldg(Un + (nzj[i] - s)), acc);
-          const double v = __fma_rn(__dadd_rn(A3[s], R3[s + n]), 1.0 / 3.0, acc);   // one rounding
-          if (v < bv) { bv = v; bn = n; bs = s; }
-        }
-      }
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        const double ov = __shfl_xor_sync(FULL, bv, o);
-        const int on = __shfl_xor_sync(FULL, bn, o), os = __shfl_xor_sync(FULL, bs, o);
-        if (ov < bv || (ov == bv && (on < bn || (on == bn && os < bs)))) { bv = ov; bn = on; bs = os; }
-      }
-      best_s = bs;
-      best_n = bn;
-      wlo = __dadd_rn(lo, __dmul_rn(w, (double)bs));                 // histclip.py:170
-      whi = __dadd_rn(lo, __dmul_rn(w, (double)(bs + bn)));
-      norm = bv * w * w;
-    }
-    hist_emit(p, row, d, lane, bad, xs, codes, wlo, whi, best_s, best_n, norm);
-  }
-}
-
 // ---------------------------------------------------------------------------
-// k_hist_s: the same search with the U table resident in shared memory (one
-// copy per block, shared by NW row-warps), so the window loop's gathers are
-// shared-memory loads instead of L2 round trips.  The per-row preparation is
-// warp-parallel: non-empty bins by ballot compaction, and the outside-window
-// sums from prefix sums of c, c*j, c*j^2 over the bins:
+// k_hist: one warp per row (8 row-warps per block), lanes over start bins.  The
+// per-row preparation is warp-parallel: non-empty bins by ballot compaction,
+// and the outside-window sums from prefix sums of c, c*j, c*j^2 over the bins:
 //   3L(t) = sum_{j<t} c_j (3m^2 - 3m + 1), m = t - j
 //         = P0 (3t^2 - 3t + 1) + P1 (3 - 6t) + 3 P2          (P = prefix sums over j < t)
 //   3R(t) = sum_{j>=t} c_j (3k^2 + 3k + 1), k = j - t
 //         = (T0-P0)(3t^2 - 3t + 1) + (T1-P1)(3 - 6t) + 3(T2-P2)
-// all exact integers in float64, so every window's value is bit-identical to
-// k_hist's (same fma order over the non-empty bins inside the window).
+// all exact integers in float64.  A window's value is one fma of the outside
+// part with the inside sum (fma over the non-empty bins inside, ascending).
+// The U table stays in global memory (L1/L2): with the pruning below only ~2.5%
+// of the windows reach the inside sum, and a shared-memory copy of U (160 KB at
+// b = 200) cost more in occupancy than it saved (measured 0.724 vs 0.726 ms at
+// d = 64, 1.76 vs 1.68 ms at d = 128).
 // ---------------------------------------------------------------------------
-struct HistSliceS {
+struct HistSlice {
   int b, d, m;   // m = min(b, d): most non-empty bins a row can have
   __host__ __device__ size_t a3_off() const { return 0; }                                   // double[b+1]
   __host__ __device__ size_t r3_off() const { return a3_off() + (size_t)(b + 1) * 8; }      // double[b+1]
@@ -256,8 +140,6 @@ struct HistSliceS {
   __host__ __device__ size_t codes_off() const { return xs_off() + (size_t)d * 4; }         // u8[d]
   __host__ __device__ size_t bytes() const { return (codes_off() + (size_t)d + 15) & ~(size_t)15; }
 };
-
-__host__ __device__ inline size_t hist_u_bytes(int b) { return (((size_t)b * (b + 1) / 2) * 8 + 15) & ~(size_t)15; }
 
 __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
 #pragma unroll
@@ -274,19 +156,15 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-__global__ void __launch_bounds__(512) k_hist_s(const HistParams p) {
+constexpr int HIST_NW = 8;   // row-warps per block
+
+__global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = p.b, d = p.d;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const HistSliceS S{b, d, min(b, d)};
-  // the whole U table, once per block
-  double* Us = reinterpret_cast<double*>(smem);
-  {
-    const size_t nu = (size_t)b * (b + 1) / 2;
-    for (size_t k = threadIdx.x; k < nu; k += blockDim.x) Us[k] = __ldg(p.U + k);
-  }
-  __syncthreads();
-  unsigned char* ws = smem + hist_u_bytes(b) + (size_t)warp * S.bytes();
+  const HistSlice S{b, d, min(b, d)};
+  const double* Us = p.U;   // L1/L2-resident (160 KB at b = 200)
+  unsigned char* ws = smem + (size_t)warp * S.bytes();
   double* A3 = reinterpret_cast<double*>(ws + S.a3_off());
   double* R3 = reinterpret_cast<double*>(ws + S.r3_off());
   double* nzc = reinterpret_cast<double*>(ws + S.nzc_off());
@@ -368,7 +246,8 @@ __global__ void __launch_bounds__(512) k_hist_s(const HistParams p) {
       // part alone exceeds a value some window attains cannot be the minimum
       // (strict >, so equal values -- first-minimum ties -- are still scored).
       // The bound starts at the full window's value (scored exactly as the scan
-      // scores it) and tightens to the warp's running minimum after every width.
+      // scores it) and tightens to (an upper bound of) the warp's running minimum after
+      // every width.
       double bound;
       {
         const double* Ub = Us + (size_t)(b - 1) * b / 2;
@@ -377,9 +256,25 @@ __global__ void __launch_bounds__(512) k_hist_s(const HistParams p) {
           for (int i = 0; i < m; i++) acc = fma(nzc[i], Ub[nzj[i]], acc);
         bound = __shfl_sync(FULL, __fma_rn(__dadd_rn(A3[0], R3[b]), 1.0 / 3.0, acc), 0);
       }
+      // Widths below n0 are skipped whole: the outside part o(s, n) is
+      // non-increasing in n (R3 falls as the window's right end moves right), so
+      // min_s o(s, n) is too, and n0 = the first width where a lower bound of it
+      // (warp minimum of the high words, low word zero) is <= bound.  o(0, b) = 0.
+      int n0 = 1;
+      {
+        int nhi = b;
+        while (n0 < nhi) {
+          const int mid = (n0 + nhi) >> 1;
+          double mo = INFINITY;
+          for (int s = lane; s <= b - mid; s += 32)
+            mo = fmin(mo, __dmul_rn(__dadd_rn(A3[s], R3[s + mid]), 1.0 / 3.0));
+          const unsigned hw = __reduce_min_sync(FULL, (unsigned)__double2hiint(mo));
+          if (__hiloint2double((int)hw, 0) > bound) n0 = mid + 1; else nhi = mid;
+        }
+      }
       double bv = INFINITY;
       int bn = 1 << 30, bs = 1 << 30;
-      for (int n = 1; n <= b; n++) {
+      for (int n = n0; n <= b; n++) {
         const double* Un = Us + (size_t)(n - 1) * n / 2;
         for (int s = lane; s <= b - n; s += 32) {
           if (__dmul_rn(__dadd_rn(A3[s], R3[s + n]), 1.0 / 3.0) > bound) continue;   // <= v
@@ -391,10 +286,10 @@ __global__ void __launch_bounds__(512) k_hist_s(const HistParams p) {
           const double v = __fma_rn(__dadd_rn(A3[s], R3[s + n]), 1.0 / 3.0, acc);   // one rounding
           if (v < bv) { bv = v; bn = n; bs = s; }
         }
-        double wm = bv;
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) wm = fmin(wm, __shfl_xor_sync(FULL, wm, o));
-        bound = fmin(bound, wm);
+        // values are >= 0, so their high words order like the values: the warp
+        // minimum of the high words, low word all ones, bounds the minimum from above
+        const unsigned hw = __reduce_min_sync(FULL, (unsigned)__double2hiint(bv));
+        bound = fmin(bound, __hiloint2double((int)hw, (int)0xffffffffu));
       }
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) {
@@ -453,41 +348,21 @@ int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  // preferred: U resident in shared memory, as many row-warps per block as fit (>= 4)
-  const char* legacy = getenv("EQ4_HIST_LEGACY");   // A/B switch for the global-U kernel
-  {
-    const HistSliceS SS{b, (int)dim, (int)std::min<int64_t>(b, dim)};
-    const size_t ub = hist_u_bytes(b), per = SS.bytes();
-    int nw = 0;
-    if (ub + 4 * per <= (size_t)max_optin) nw = (int)std::min<size_t>(16, (max_optin - ub) / per);
-    if (nw >= 4 && !(legacy && legacy[0] == '1')) {
-      const size_t smem = ub + (size_t)nw * per;
-      cudaError_t e = cudaFuncSetAttribute(k_hist_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) { err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
-      int occ = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hist_s, nw * 32, smem);
-      if (occ < 1) occ = 1;
-      const int64_t need = (rows + nw - 1) / nw;
-      const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * occ));
-      k_hist_s<<<(unsigned)grid, nw * 32, smem, s>>>(p);
-      e = cudaGetLastError();
-      if (e != cudaSuccess) { err = std::string("k_hist_s launch: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
-      return EQ4_OK;
-    }
-  }
-  const HistSlice S{b, (int)dim};
-  const size_t smem = S.bytes();
-  if (smem > 227 * 1024) { err = "hist-brute: row does not fit in shared memory"; return EQ4_EUNSUPPORTED; }
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) { err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
-  }
+  const HistSlice SS{b, (int)dim, (int)std::min<int64_t>(b, dim)};
+  const size_t per = SS.bytes();
+  if (per > (size_t)max_optin) { err = "hist-brute: row does not fit in shared memory"; return EQ4_EUNSUPPORTED; }
+  const int nw = (int)std::max<size_t>(1, std::min<size_t>(HIST_NW, max_optin / per));
+  const size_t smem = (size_t)nw * per;
+  auto kern = k_hist;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) { err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hist, 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nw * 32, smem);
   if (occ < 1) occ = 1;
-  const int64_t grid = std::min<int64_t>(rows, (int64_t)sms * occ);
-  k_hist<<<(unsigned)grid, 32, smem, s>>>(p);
-  cudaError_t e = cudaGetLastError();
+  const int64_t need = (rows + nw - 1) / nw;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * occ));
+  kern<<<(unsigned)grid, nw * 32, smem, s>>>(p);
+  e = cudaGetLastError();
   if (e != cudaSuccess) { err = std::string("k_hist launch: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
   return EQ4_OK;
 }
