@@ -1830,10 +1830,16 @@ static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t
     cudaFreeAsync(keys, s);
     return rc;
   }
-  if (method == EQ4_METHOD_ACIQ || method == EQ4_METHOD_GSS || method == EQ4_METHOD_HIST_APPRX) {
+  if (method == EQ4_METHOD_ACIQ || method == EQ4_METHOD_GSS) {
     std::string err;
     const int rc = eq4_rowrange_launch(x, rows, dim, ld, method, aux, packed, xmin, xmax, info0,
-                                       status, s, err, b, info1, norm);
+                                       status, s, err);
+    return rc == EQ4_OK ? rc : fail(rc, err);
+  }
+  if (method == EQ4_METHOD_HIST_APPRX) {
+    std::string err;
+    const int rc = eq4_hist_launch(x, rows, dim, ld, b, aux, packed, xmin, xmax, info0, info1, norm,
+                                   status, s, err, true);
     return rc == EQ4_OK ? rc : fail(rc, err);
   }
   if (method == EQ4_METHOD_GREEDY) {
@@ -1869,7 +1875,7 @@ static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t
   if (method == EQ4_METHOD_HIST_BRUTE) {
     std::string err;
     const int rc = eq4_hist_launch(x, rows, dim, ld, b, aux, packed, xmin, xmax, info0, info1, norm,
-                                   status, s, err);
+                                   status, s, err, false);
     return rc == EQ4_OK ? rc : fail(rc, err);
   }
   return fail(EQ4_EINVAL, "unknown method " + std::to_string(method));

@@ -301,4 +301,77 @@ __device__ __forceinline__ uint32_t aux_bits_f32(double v) {
   return r;
 }
 
+// ---- HIST-APPRX exact window norm (histclip.py:110-121), the reference's float64 order ----
+// x^3 through a double-double product (the reference's numpy `**3` is SVML /
+// libm pow, itself host-dependent in the last bit)
+__device__ __forceinline__ double cube_dd(double x) {
+  const double h = __dmul_rn(x, x), l = __fma_rn(x, x, -h);
+  const double t = __dmul_rn(h, x);
+  const double e = __fma_rn(h, x, -t) + __dmul_rn(l, x);
+  return __dadd_rn(t, e);
+}
+// histclip.py:70-82 bin_l2_norm(db, de, 1.0)
+__device__ __forceinline__ double l2u(double db, double de) {
+  return __ddiv_rn(__dmul_rn(1.0, __dsub_rn(cube_dd(de), cube_dd(db))), 3.0);
+}
+
+// histclip.py:85-109 _offset_unit_norms(j - s, w, dst_w) * density for bin j (count c > 0)
+__device__ __forceinline__ double apprx_term(int c, int j, double w, int s, double dst_w, double half,
+                                             double cw) {
+  const double density = __ddiv_rn((double)c, w);
+  const double k = __dsub_rn((double)j, (double)s);
+  const double begin = __dmul_rn(k, w), end = __dadd_rn(begin, w);
+  const double dob = np_clip(floor(__ddiv_rn(__dadd_rn(begin, half), dst_w)), 0.0, 15.0);
+  const double doe = np_clip(floor(__ddiv_rn(__dadd_rn(end, half), dst_w)), 0.0, 15.0);
+  const double bc = __dmul_rn(dob, dst_w), ec = __dmul_rn(doe, dst_w);
+  const double db = __dsub_rn(begin, bc);
+  double contrib;
+  if (dob == doe) {
+    contrib = l2u(db, __dsub_rn(end, bc));
+  } else {
+    contrib = __dadd_rn(__dadd_rn(l2u(db, half), __dmul_rn(__dsub_rn(__dsub_rn(doe, dob), 1.0), cw)),
+                        l2u(-half, __dsub_rn(end, ec)));
+  }
+  return __dmul_rn(density, contrib);
+}
+
+// histclip.py:110-121 window_norm = np.sum over the b bins of density * unit norm, in
+// numpy's pairwise order (b <= 256: one or two leaves of 8 accumulator chains, the
+// fixed ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree, then the remainder in order).
+// Warp-collective: lanes compute the bins' terms into t[0..b) (empty bins give the
+// +0.0 numpy adds, which leave every partial sum unchanged), lanes 8l..8l+7 run
+// leaf l's chains.  Every lane returns the value.
+static __device__ __noinline__ double apprx_norm_np_warp(const int* cnt, int b, double w, int s, int n,
+                                                  double* t, int lane) {
+  const double dst_w = __ddiv_rn(__dmul_rn(w, (double)n), 15.0);
+  const double half = __dmul_rn(0.5, dst_w);
+  const double cw = l2u(-half, half);
+  for (int j = lane; j < b; j += 32) {
+    const int c = cnt[j];
+    t[j] = c ? apprx_term(c, j, w, s, dst_w, half, cw) : 0.0;
+  }
+  __syncwarp();
+  const int nleaves = b > 128 ? 2 : 1;
+  int n2 = b;
+  if (b > 128) { n2 = b / 2; n2 -= n2 % 8; }
+  const int leaf = (lane >> 3) & 1, k = lane & 7;
+  const int ls = leaf ? n2 : 0, ln = leaf ? b - n2 : n2;
+  const int nfull = ln < 8 ? 0 : ln - (ln % 8);
+  double r = 0.0;
+  if (lane < 8 * nleaves)
+    for (int jj = k; jj < nfull; jj += 8) r = __dadd_rn(r, t[ls + jj]);
+  double rr[8];
+#pragma unroll
+  for (int q = 0; q < 8; q++) rr[q] = __shfl_sync(0xffffffffu, r, (lane & 8) + q);
+  double res = 0.0;
+  if (ln >= 8)
+    res = __dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
+                    __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7])));
+  for (int jj = nfull; jj < ln; jj++) res = __dadd_rn(res, t[ls + jj]);
+  const double leaf1 = __shfl_sync(0xffffffffu, res, 8);
+  const double total = nleaves == 2 ? __dadd_rn(res, leaf1) : res;   // lane 0: leaf 0 + leaf 1
+  __syncwarp();
+  return __shfl_sync(0xffffffffu, __dadd_rn(0.0, total), 0);
+}
+
 }  // namespace eq4

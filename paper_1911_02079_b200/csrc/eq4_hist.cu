@@ -132,7 +132,8 @@ struct HistSlice {
   int b, d, m;   // m = min(b, d): most non-empty bins a row can have
   __host__ __device__ size_t a3_off() const { return 0; }                                   // double[b+1]
   __host__ __device__ size_t r3_off() const { return a3_off() + (size_t)(b + 1) * 8; }      // double[b+1]
-  __host__ __device__ size_t nzc_off() const { return r3_off() + (size_t)(b + 1) * 8; }     // double[m]
+  __host__ __device__ size_t tmp_off() const { return r3_off() + (size_t)(b + 1) * 8; }     // double[b] (HIST-APPRX)
+  __host__ __device__ size_t nzc_off() const { return tmp_off() + (size_t)b * 8; }          // double[m]
   __host__ __device__ size_t cnt_off() const { return nzc_off() + (size_t)m * 8; }          // int[b]
   __host__ __device__ size_t lb_off() const { return cnt_off() + (size_t)b * 4; }           // int[b+1]
   __host__ __device__ size_t nzj_off() const { return lb_off() + (size_t)(b + 1) * 4; }     // int[m]
@@ -156,8 +157,82 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
+constexpr double APPRX_TOL = 1e-11;   // relative gap below which the walk re-decides exactly
+
+// HIST-APPRX (histclip.py:181-217): from the full window, drop one bin from the
+// end whose removal scores lower (ties drop the right end), keeping the first
+// best window seen.  Warp-collective, one row.  Each step scores its two
+// windows (st + 1, nn) and (st, nn), nn = en - st - 1, with the brute scan's
+// formula (outside part from A3/R3, inside sum over the non-empty bins with
+// U_nn, lanes over bins, xor-butterfly sum so every lane holds the same value;
+// w^2 dropped).  Those values are within ~1e-13 relative of the reference's
+// window_norm, so a comparison whose operands differ by more than APPRX_TOL
+// relative is the reference's; a closer one is re-decided on the reference's
+// own float64 values (apprx_norm_np_warp: its elementwise formula in numpy's
+// pairwise order), as is the reported norm of the chosen window.
+__device__ __forceinline__ void hist_apprx_walk(const double* Us, const double* A3, const double* R3,
+                                                const double* nzc, const int* nzj, const int* cnt,
+                                                double* tmp, int m, int b, double w, int lane, int& best_s,
+                                                int& best_n, double& norm) {
+  auto exact = [&](int s0, int n0) -> double { return apprx_norm_np_warp(cnt, b, w, s0, n0, tmp, lane); };
+  int st = 0, en = b;
+  double bestF;
+  {
+    const double* Ub = Us + (size_t)(b - 1) * b / 2;
+    double a = 0.0;
+    for (int i = lane; i < m; i += 32) a = fma(nzc[i], Ub[nzj[i]], a);
+    bestF = __fma_rn(__dadd_rn(A3[0], R3[b]), 1.0 / 3.0, warp_sum_d(a));
+  }
+  double bestN = 0.0;
+  bool have_bestN = false;
+  int bs = 0, be = b;
+  while (en - st > 1) {                                              // histclip.py:202
+    const int nn = en - st - 1;
+    const double* Un = Us + (size_t)(nn - 1) * nn / 2;
+    double aL = 0.0, aR = 0.0;
+    for (int i = lane; i < m; i += 32) {
+      const int j = nzj[i];
+      const double c = nzc[i];
+      const int kL = j - st - 1, kR = j - st;
+      if ((unsigned)kL < (unsigned)nn) aL = fma(c, Un[kL], aL);
+      if ((unsigned)kR < (unsigned)nn) aR = fma(c, Un[kR], aR);
+    }
+    const double FL = __fma_rn(__dadd_rn(A3[st + 1], R3[en]), 1.0 / 3.0, warp_sum_d(aL));
+    const double FR = __fma_rn(__dadd_rn(A3[st], R3[en - 1]), 1.0 / 3.0, warp_sum_d(aR));
+    bool goL, have_cur = false;
+    double curN = 0.0;
+    if (fabs(FL - FR) > APPRX_TOL * fmax(FL, FR)) {
+      goL = FL < FR;
+    } else {
+      const double NL = exact(st + 1, nn), NR = exact(st, nn);
+      goL = NL < NR;                                                 // histclip.py:205-206
+      curN = goL ? NL : NR;
+      have_cur = true;
+    }
+    const double curF = goL ? FL : FR;
+    if (goL) ++st; else --en;
+    bool better;
+    if (fabs(curF - bestF) > APPRX_TOL * fmax(curF, bestF)) {
+      better = curF < bestF;
+    } else {
+      if (!have_cur) { curN = exact(st, en - st); have_cur = true; }
+      if (!have_bestN) { bestN = exact(bs, be - bs); have_bestN = true; }
+      better = curN < bestN;                                         // histclip.py:211-213
+    }
+    if (better) {
+      bestF = curF; bs = st; be = en;
+      bestN = curN; have_bestN = have_cur;
+    }
+  }
+  if (!have_bestN) bestN = exact(bs, be - bs);
+  best_s = bs;
+  best_n = be - bs;
+  norm = bestN;
+}
+
 constexpr int HIST_NW = 8;   // row-warps per block
 
+template <bool APPRX>
 __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = p.b, d = p.d;
@@ -241,6 +316,12 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
         c2 += __shfl_sync(FULL, i2, 31);
       }
       __syncwarp();
+      if constexpr (APPRX) {
+        hist_apprx_walk(Us, A3, R3, nzc, nzj, cnt, reinterpret_cast<double*>(ws + S.tmp_off()), m, b, w, lane,
+                        best_s, best_n, norm);
+        wlo = __dadd_rn(lo, __dmul_rn(w, (double)best_s));          // histclip.py:214-219
+        whi = __dadd_rn(lo, __dmul_rn(w, (double)(best_s + best_n)));
+      } else {
       // ---- every window, first minimum in (n asc, s asc) order ----
       // Pruning: v = (A3 + R3)/3 + acc with acc >= 0, so a window whose outside
       // part alone exceeds a value some window attains cannot be the minimum
@@ -302,6 +383,7 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
       wlo = __dadd_rn(lo, __dmul_rn(w, (double)bs));                 // histclip.py:170
       whi = __dadd_rn(lo, __dmul_rn(w, (double)(bs + bn)));
       norm = bv * w * w;
+      }
     }
     hist_emit(p, row, d, lane, bad, xs, codes, wlo, whi, best_s, best_n, norm);
   }
@@ -334,8 +416,9 @@ static const double* hist_table(int b, cudaStream_t s, std::string& err) {
 
 int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b, int aux,
                     uint8_t* packed, double* xmin, double* xmax, int32_t* info0, int32_t* info1,
-                    double* norm, int32_t* status, cudaStream_t s, std::string& err) {
+                    double* norm, int32_t* status, cudaStream_t s, std::string& err, bool apprx) {
   if (b > 4096) { err = "hist-brute with b > 4096 is not supported by the B200 path"; return EQ4_EUNSUPPORTED; }
+  if (apprx && b > 256) { err = "hist-apprx with b > 256 is not supported by the B200 path"; return EQ4_EUNSUPPORTED; }
   const double* U = hist_table(b, s, err);
   if (!U) return EQ4_ECUDA;
   HistParams p;
@@ -353,7 +436,7 @@ int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b
   if (per > (size_t)max_optin) { err = "hist-brute: row does not fit in shared memory"; return EQ4_EUNSUPPORTED; }
   const int nw = (int)std::max<size_t>(1, std::min<size_t>(HIST_NW, max_optin / per));
   const size_t smem = (size_t)nw * per;
-  auto kern = k_hist;
+  auto kern = apprx ? k_hist<true> : k_hist<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) { err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
   int occ = 0;

@@ -5,11 +5,11 @@
 #include <cstdint>
 #include <string>
 
-// HIST-BRUTE fused search + quantize + pack (eq4_hist.cu).  Returns an EQ4_* code;
-// on failure err holds the message.
+// HIST-BRUTE (apprx = false) / HIST-APPRX (apprx = true) fused search + quantize +
+// pack (eq4_hist.cu).  Returns an EQ4_* code; on failure err holds the message.
 int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b, int aux,
                     uint8_t* packed, double* xmin, double* xmax, int32_t* info0, int32_t* info1,
-                    double* norm, int32_t* status, cudaStream_t s, std::string& err);
+                    double* norm, int32_t* status, cudaStream_t s, std::string& err, bool apprx);
 
 // Pooled lookup over packed rows (eq4_sls.cu).  Returns an EQ4_* code.
 int eq4_sls_launch(const uint8_t* packed, int64_t rows, int64_t dim, int aux,
@@ -26,8 +26,7 @@ int eq4_io_write_embq(const char* path, const uint8_t* packed, int64_t rows, int
 // ACIQ / GSS row-range searches + quantize + pack (eq4_rowrange.cu).
 int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, int aux,
                         uint8_t* packed, double* xmin, double* xmax, int32_t* info0,
-                        int32_t* status, cudaStream_t s, std::string& err, int b, int32_t* info1,
-                        double* norm);
+                        int32_t* status, cudaStream_t s, std::string& err);
 
 // Row-wise KMEANS codebooks (eq4_kmeans.cu).
 int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int aux, uint8_t* out,

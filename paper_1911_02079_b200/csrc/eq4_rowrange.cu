@@ -47,9 +47,6 @@ struct RRParams {
   double invphi;     // (sqrt(5) - 1) / 2, clipping.py:27
   int staged;
   size_t warp_bytes;
-  int b;             // HIST-APPRX bins
-  int32_t* info1;
-  double* norm_out;
 };
 
 // Element k of this lane's row.
@@ -226,106 +223,6 @@ __device__ __forceinline__ int lane_gss(const RowView& xr, int d, float mn, floa
   return n;
 }
 
-// ---- HIST-APPRX (histclip.py:181-217) ----
-// x^3 through a double-double product (the reference's numpy `**3` is SVML /
-// libm pow, itself host-dependent in the last bit)
-__device__ __forceinline__ double cube_dd(double x) {
-  const double h = __dmul_rn(x, x), l = __fma_rn(x, x, -h);
-  const double t = __dmul_rn(h, x);
-  const double e = __fma_rn(h, x, -t) + __dmul_rn(l, x);
-  return __dadd_rn(t, e);
-}
-// histclip.py:70-82 bin_l2_norm(db, de, 1.0)
-__device__ __forceinline__ double l2u(double db, double de) {
-  return __ddiv_rn(__dmul_rn(1.0, __dsub_rn(cube_dd(de), cube_dd(db))), 3.0);
-}
-
-// histclip.py:110-121 window_norm: np.sum over the b bins of density * unit norm
-// (histclip.py:85-109), zero bins skipped (+0.0 terms leave a pairwise sum
-// unchanged), the rest placed in numpy's leaf accumulators (b <= 256: at most
-// two leaves).  cnt: this lane's counts column.
-__device__ double apprx_norm(const uint16_t* cnt, int b, double w, int s, int n) {
-  const double dst_w = __ddiv_rn(__dmul_rn(w, (double)n), 15.0);
-  const double half = __dmul_rn(0.5, dst_w);
-  const double cw = l2u(-half, half);
-  int n2 = b;
-  if (b > 128) { n2 = b / 2; n2 -= n2 % 8; }
-  double total = 0.0;
-  for (int leaf = 0; leaf < (b > 128 ? 2 : 1); leaf++) {
-    const int ls = leaf ? n2 : 0, ln = leaf ? b - n2 : n2;
-    const int nfull = ln < 8 ? 0 : ln - (ln % 8);
-    double r[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    double tail = 0.0;   // ln < 8: res = 0. + ...; else the post-tree remainder
-    bool tree_done = ln < 8;
-    double res = 0.0;
-    for (int jj = 0; jj < ln; jj++) {
-      const int j = ls + jj;
-      if (!tree_done && jj >= nfull) {
-        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        tree_done = true;
-      }
-      const int c = cnt[j * 32];
-      if (!c) continue;
-      const double density = __ddiv_rn((double)c, w);
-      const double k = __dsub_rn((double)j, (double)s);
-      const double begin = __dmul_rn(k, w), end = __dadd_rn(begin, w);
-      const double dob = np_clip(floor(__ddiv_rn(__dadd_rn(begin, half), dst_w)), 0.0, 15.0);
-      const double doe = np_clip(floor(__ddiv_rn(__dadd_rn(end, half), dst_w)), 0.0, 15.0);
-      const double bc = __dmul_rn(dob, dst_w), ec = __dmul_rn(doe, dst_w);
-      const double db = __dsub_rn(begin, bc);
-      double contrib;
-      if (dob == doe) {
-        contrib = l2u(db, __dsub_rn(end, bc));
-      } else {
-        contrib = __dadd_rn(__dadd_rn(l2u(db, half), __dmul_rn(__dsub_rn(__dsub_rn(doe, dob), 1.0), cw)),
-                            l2u(-half, __dsub_rn(end, ec)));
-      }
-      const double t = __dmul_rn(density, contrib);
-      if (ln < 8) tail = __dadd_rn(tail, t);
-      else if (jj < nfull) r[jj & 7] = __dadd_rn(r[jj & 7], t);
-      else res = __dadd_rn(res, t);
-    }
-    if (!tree_done)
-      res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    const double leaf_sum = ln < 8 ? tail : res;
-    total = leaf ? __dadd_rn(total, leaf_sum) : leaf_sum;
-  }
-  return __dadd_rn(0.0, total);
-}
-
-// histclip.py:52-67 histogram + the greedy window walk; returns the range and window.
-__device__ __forceinline__ void lane_hist_apprx(const RowView& xr, int d, int b, float mn, float mx,
-                                                uint16_t* cnt, double& lo, double& hi, int& start,
-                                                int& nsel, double& norm) {
-  const double hlo = (double)mn, hhi = (double)mx;
-  if (hlo == hhi) {   // histclip.py:193-197
-    lo = hlo; hi = hhi; start = 0; nsel = 1; norm = 0.0;
-    return;
-  }
-  const double w = __ddiv_rn(__dsub_rn(hhi, hlo), (double)b);
-  for (int j = 0; j < b; j++) cnt[j * 32] = 0;
-  for (int k = 0; k < d; k++) {
-    const double q = floor(__ddiv_rn(__dsub_rn((double)xr[k], hlo), w));
-    const int idx = (int)np_clip(q, 0.0, (double)(b - 1));
-    cnt[idx * 32] += 1;
-  }
-  int st = 0, en = b;
-  double best = apprx_norm(cnt, b, w, st, en - st);
-  int bs = st, be = en;
-  while (en - st > 1) {
-    const double nl = apprx_norm(cnt, b, w, st + 1, en - st - 1);
-    const double nr = apprx_norm(cnt, b, w, st, en - st - 1);
-    double cur;
-    if (nl < nr) { st += 1; cur = nl; } else { en -= 1; cur = nr; }
-    if (cur < best) { best = cur; bs = st; be = en; }
-  }
-  lo = __dadd_rn(hlo, __dmul_rn(w, (double)bs));   // histclip.py:214-219
-  hi = __dadd_rn(hlo, __dmul_rn(w, (double)be));
-  start = bs; nsel = be - bs; norm = best;
-}
-
 __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -333,7 +230,6 @@ __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
   float* xs = reinterpret_cast<float*>(ws);
   const size_t xs_bytes = p.staged ? (size_t)p.d * RR_COL * 4 : 0;
   uint8_t* out_base = ws + ((xs_bytes + 15) & ~(size_t)15);
-  uint16_t* cnt_base = reinterpret_cast<uint16_t*>(out_base + (((size_t)32 * p.stride + 32 + 15) & ~(size_t)15));
   const int d = p.d;
   const int64_t nblk = (p.rows + 31) / 32;
   for (int64_t blk = (int64_t)blockIdx.x * RR_WARPS + warp; blk < nblk;
@@ -372,15 +268,8 @@ __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
     if (rvalid && !bad) {
       if (p.method == EQ4_METHOD_ACIQ) {
         lane_aciq(xr, d, mn, mx, lo, hi);
-      } else if (p.method == EQ4_METHOD_GSS) {
-        evals = lane_gss(xr, d, mn, mx, p.invphi, lo, hi);
       } else {
-        int st = 0, ns = 1;
-        double nv = 0.0;
-        lane_hist_apprx(xr, d, p.b, mn, mx, cnt_base + lane, lo, hi, st, ns, nv);
-        evals = st;
-        if (p.info1) p.info1[row] = ns;
-        if (p.norm_out) p.norm_out[row] = nv;
+        evals = lane_gss(xr, d, mn, mx, p.invphi, lo, hi);
       }
     }
     // codes (uniform.py:60-80) + packed row (packed.py:68-83), staged then copied out
@@ -435,14 +324,8 @@ using namespace eq4;
 
 int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, int aux,
                         uint8_t* packed, double* xmin, double* xmax, int32_t* info0,
-                        int32_t* status, cudaStream_t s, std::string& err, int b, int32_t* info1,
-                        double* norm) {
-  if (method == EQ4_METHOD_HIST_APPRX && (b < 1 || b > 256)) {
-    err = "hist-apprx with b > 256 is not supported by the B200 path";
-    return EQ4_EUNSUPPORTED;
-  }
+                        int32_t* status, cudaStream_t s, std::string& err) {
   RRParams p;
-  p.b = b; p.info1 = info1; p.norm_out = norm;
   p.x = x; p.rows = rows; p.ld = ld; p.d = (int)dim; p.aux = aux; p.method = method;
   p.half = (int)((dim + 1) / 2);
   p.stride = p.half + 2 * (aux == EQ4_AUX_FP16 ? 2 : 4);
@@ -451,7 +334,6 @@ int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, i
   p.staged = dim <= RR_MAX_STAGED;
   const size_t xs_bytes = p.staged ? (size_t)dim * RR_COL * 4 : 0;
   p.warp_bytes = ((xs_bytes + 15) & ~(size_t)15) + (((size_t)32 * p.stride + 32 + 15) & ~(size_t)15);
-  if (method == EQ4_METHOD_HIST_APPRX) p.warp_bytes += (size_t)b * 32 * 2;   // per-lane counts columns
   p.warp_bytes = (p.warp_bytes + 15) & ~(size_t)15;
   const size_t smem = p.warp_bytes * RR_WARPS;
   cudaError_t e = cudaFuncSetAttribute(k_rowrange, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
