@@ -46,6 +46,7 @@ struct RRParams {
   int32_t* status;
   double invphi;     // (sqrt(5) - 1) / 2, clipping.py:27
   int staged;
+  int vec4;          // rows 16-byte aligned (d % 4 == 0, ld % 4 == 0, aligned base)
   size_t warp_bytes;
 };
 
@@ -239,10 +240,35 @@ __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
     const int nrows = (int)min((int64_t)32, p.rows - row0);
     RowView xr;
     if (p.staged) {
-      for (int r = 0; r < nrows; r++) {
-        const float* src = p.x + (row0 + r) * p.ld;
-#pragma unroll 4
-        for (int k = lane; k < d; k += 32) xs[k * RR_COL + r] = __ldcs(src + k);
+      // lane r stages row row0 + r into column r: all of a lane's loads are
+      // independent (16-byte loads, 8 in flight per group, when the rows are
+      // 16-byte aligned), and the column stores are conflict-free
+      if (p.vec4) {
+        const float4* src = reinterpret_cast<const float4*>(p.x + (rvalid ? row : row0) * p.ld);
+        const int n4 = d >> 2;
+        for (int c0 = 0; c0 < n4; c0 += 8) {
+          float4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++)
+            if (c0 + u < n4) v[u] = __ldcs(src + c0 + u);
+#pragma unroll
+          for (int u = 0; u < 8; u++)
+            if (c0 + u < n4) {
+              float* col = xs + (size_t)(4 * (c0 + u)) * RR_COL + lane;
+              col[0] = v[u].x; col[RR_COL] = v[u].y; col[2 * RR_COL] = v[u].z; col[3 * RR_COL] = v[u].w;
+            }
+        }
+      } else {
+        const float* src = p.x + (rvalid ? row : row0) * p.ld;
+        for (int k0 = 0; k0 < d; k0 += 8) {
+          float v[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++)
+            if (k0 + u < d) v[u] = __ldcs(src + k0 + u);
+#pragma unroll
+          for (int u = 0; u < 8; u++)
+            if (k0 + u < d) xs[(size_t)(k0 + u) * RR_COL + lane] = v[u];
+        }
       }
       __syncwarp();
       xr.base = xs + lane;
@@ -277,17 +303,24 @@ __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
     if (rvalid) {
       uint8_t* orow = out_tile + (size_t)lane * p.stride;
       const bool degenerate = bad || hi == lo;
-      Codec cd;
-      if (!degenerate) cd = make_codec(lo, hi);
+      // fp32 code estimate, float64 codec within NEAR of a rounding boundary
+      const CodeParams cp = make_code_params(degenerate ? 0.0 : lo, degenerate ? 0.0 : hi);
       for (int m = 0; m < p.half; m++) {
         unsigned c0 = 0, c1 = 0;
         if (!degenerate) {
-          c0 = (unsigned)cd.code((double)xr[2 * m]);
-          if (2 * m + 1 < d) c1 = (unsigned)cd.code((double)xr[2 * m + 1]);
+          bool ne0, ne1 = false;
+          const float x0 = xr[2 * m];
+          c0 = code_of(x0, cp, ne0);
+          if (2 * m + 1 < d) {
+            const float x1 = xr[2 * m + 1];
+            c1 = code_of(x1, cp, ne1);
+            if (ne1) c1 = code_exact(x1, cp);
+          }
+          if (ne0) c0 = code_exact(x0, cp);
         }
         orow[m] = (uint8_t)(c0 | (c1 << 4));
       }
-      const double sc = degenerate ? 0.0 : cd.scale;   // uniform.py:74-80
+      const double sc = degenerate ? 0.0 : cp.scale;   // uniform.py:74-80
       uint8_t* a = orow + p.half;
       if (p.aux == EQ4_AUX_FP16) {
         const uint32_t s16 = aux_bits_f16(sc), b16 = aux_bits_f16(lo);
@@ -332,6 +365,7 @@ int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, i
   p.packed = packed; p.lo_out = xmin; p.hi_out = xmax; p.info0 = info0; p.status = status;
   p.invphi = (std::sqrt(5.0) - 1.0) / 2.0;
   p.staged = dim <= RR_MAX_STAGED;
+  p.vec4 = (dim % 4 == 0) && (ld % 4 == 0) && (((uintptr_t)x & 15) == 0);
   const size_t xs_bytes = p.staged ? (size_t)dim * RR_COL * 4 : 0;
   p.warp_bytes = ((xs_bytes + 15) & ~(size_t)15) + (((size_t)32 * p.stride + 32 + 15) & ~(size_t)15);
   p.warp_bytes = (p.warp_bytes + 15) & ~(size_t)15;
