@@ -278,57 +278,90 @@ def run_ours(args, rank: int, world: int):
         "clocks": clocks.summary(),
     }
     if args.secondary:
-        line["secondary"] = secondary(eq, workloads, torch, dev, peaks)
+        line["secondary"] = secondary(eq, workloads, torch, dev, peaks, fp32_peak)
         line["secondary"]["sls_20Mx64_greedy_packed"] = sls_secondary(eq, torch, dev, peaks, out, rows)
     print(json.dumps(line), flush=True)
 
 
-def secondary(eq, workloads, torch, dev, peaks):
-    """Config 2 (ASYM 4M x 64 HBM path) and config 3 (GREEDY 4M x 128 mixed), device-timed."""
-    res = {}
-    for name, method, rows, d, gen in (("asym_4Mx64_config2", "asym", 4_194_304, 64, "gauss"),
-                                       ("greedy_4Mx128_mixed_config3", "greedy", 4_194_304, 128, "mixed")):
-        x = (workloads.gaussian_table if gen == "gauss" else workloads.mixed_table)(rows, d, 7, device=dev)
-        st = torch.zeros(1, dtype=torch.int32, device=dev)
-        out = torch.empty(rows * eq.packed_row_stride(d, AUX), dtype=torch.uint8, device=dev)
-        f = lambda: eq.quantize_pack_table4(x, method, AUX, B, R, out=out, status=st, check=False)
-        for _ in range(3):
-            f()
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-        n = 10
-        e0.record()
-        for _ in range(n):
-            f()
-        e1.record()
-        torch.cuda.synchronize(dev)
-        ms = e0.elapsed_time(e1) / n
-        byt = rows * (4 * d + (d + 1) // 2 + 4)
-        r = {"ms": ms, "rows_per_s": rows / ms * 1e3, "GBps": byt / ms / 1e6}
-        if method == "asym":
-            r["hbm_frac"] = r["GBps"] / float(peaks.get("hbm_gbs", 6546.9))
-        res[name] = r
-        del x, out
-    # config 4: HIST-BRUTE b=200 on 16,384 x 64 N(0,1) (compute-bound, no roofline target):
-    # per-row time and the reference's bin-visit counter rate (histclip.py:162-164)
-    x = workloads.gaussian_table(16384, 64, 7, device=dev)
+def _time_method(eq, torch, dev, x, method, b, n=10, warm=3):
+    """Device time (CUDA events on the current stream) of one fused launch over x, plus the
+    GREEDY loss-evaluation count of that launch (clipping.py:174,183-184) for the roofline."""
+    rows, d = x.shape
     st = torch.zeros(1, dtype=torch.int32, device=dev)
-    out = torch.empty(16384 * eq.packed_row_stride(64, AUX), dtype=torch.uint8, device=dev)
-    f = lambda: eq.quantize_pack_table4(x, "hist-brute", AUX, 200, out=out, status=st, check=False)
-    for _ in range(2):
+    out = torch.empty(rows * eq.packed_row_stride(d, AUX), dtype=torch.uint8, device=dev)
+    evals = None
+    if method == "greedy":
+        rr = eq.RowResults(None, None, torch.empty(rows, dtype=torch.int32, device=dev), None, None)
+        eq.quantize_pack_table4(x, method, AUX, b, R, out=out, rows_out=rr)
+        it = rr.info0.to(torch.int64)
+        evals = int(torch.where(it >= 0, 1 + 2 * it, torch.zeros_like(it)).sum().item())
+        del rr, it
+    f = lambda: eq.quantize_pack_table4(x, method, AUX, b, R, out=out, status=st, check=False)
+    for _ in range(warm):
         f()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
-    for _ in range(5):
+    for _ in range(n):
         f()
     e1.record()
     torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1) / 5
+    if int(st.item()):
+        raise SystemExit(f"kernel status {int(st.item())} in a secondary workload ({method})")
+    del out
+    return e0.elapsed_time(e1) / n, evals
+
+
+def secondary(eq, workloads, torch, dev, peaks, fp32_peak):
+    """The other BASELINE.json configs, device-timed (each table >> L2 or re-read per launch):
+    config 2 (ASYM 4M x 64, HBM-bound), config 3 (GREEDY 4M x 128 mixed), config 4 (HIST-BRUTE
+    16,384 x 64), config 5a (GREEDY d-sweep over 1 GiB N(0,1) tables), plus the HIST-APPRX and
+    ACIQ searches on their own representative tables."""
+    hbm = float(peaks.get("hbm_gbs", 6546.9))
+    res = {}
+
+    def greedy_line(x, d, ms, evals):
+        rows = x.shape[0]
+        flop = float(FLOP_PER_ELEM_EVAL) * d * evals
+        return {"ms": ms, "rows_per_s": rows / ms * 1e3,
+                "GBps": rows * (4 * d + (d + 1) // 2 + 4) / ms / 1e6,
+                "alg_TFLOPs": flop / ms / 1e9, "fp32_frac": flop / ms / 1e9 / fp32_peak}
+
+    x = workloads.gaussian_table(4_194_304, 64, 7, device=dev)
+    ms, _ = _time_method(eq, torch, dev, x, "asym", B)
+    byt = 4_194_304 * (4 * 64 + 32 + 4)
+    res["asym_4Mx64_config2"] = {"ms": ms, "rows_per_s": 4_194_304 / ms * 1e3, "GBps": byt / ms / 1e6,
+                                 "hbm_frac": byt / ms / 1e6 / hbm}
+    del x
+    x = workloads.mixed_table(4_194_304, 128, 7, device=dev)
+    ms, ev = _time_method(eq, torch, dev, x, "greedy", B)
+    res["greedy_4Mx128_mixed_config3"] = greedy_line(x, 128, ms, ev)
+    del x
+    # config 4: HIST-BRUTE b=200 (compute-bound, no roofline target): per-row time and the
+    # reference's bin-visit counter rate (histclip.py:162-164)
+    x = workloads.gaussian_table(16384, 64, 7, device=dev)
+    ms, _ = _time_method(eq, torch, dev, x, "hist-brute", 200, n=5, warm=2)
     visits = 16384 * 200 * (200 * 201 // 2)
     res["hist_brute_16384x64_config4"] = {"ms": ms, "us_per_row": ms * 1e3 / 16384,
                                           "bin_visits_per_s": visits / ms * 1e3}
-    del x, out
+    # HIST-APPRX (histclip.py:181-217) on the same table: 2b - 1 = 399 window norms per row
+    ms, _ = _time_method(eq, torch, dev, x, "hist-apprx", 200, n=5, warm=2)
+    res["hist_apprx_16384x64"] = {"ms": ms, "us_per_row": ms * 1e3 / 16384}
+    del x
+    # ACIQ (clipping.py:115-139): two numpy-order float64 sums per row + codes, bandwidth-class
+    x = workloads.gaussian_table(4_194_304, 64, 7, device=dev)
+    ms, _ = _time_method(eq, torch, dev, x, "aciq", B)
+    res["aciq_4Mx64"] = {"ms": ms, "GBps": byt / ms / 1e6, "hbm_frac": byt / ms / 1e6 / hbm}
+    del x
+    # config 5a: GREEDY d-sweep, rows = 2^30 / (4 d): 1 GiB of fp32 per table
+    sweep = {}
+    for d in (16, 32, 64, 128, 256, 512, 1024, 2048):
+        rows = (1 << 30) // (4 * d)
+        x = workloads.gaussian_table(rows, d, 7, device=dev)
+        ms, ev = _time_method(eq, torch, dev, x, "greedy", B, n=5, warm=2)
+        sweep[str(d)] = greedy_line(x, d, ms, ev)
+        del x
+    res["greedy_dsweep_1GiB_config5a"] = sweep
     return res
 
 
