@@ -14,9 +14,8 @@
 // summation order for its own row sequentially (8 accumulator chains per
 // <=128-element leaf, recursive halving n2 = n/2 - (n/2 % 8) above), 32 rows
 // in flight per warp instead of one warp-cooperative row at a time.  Codes use
-// a divide-free estimate of (c - lo) / scale and take the IEEE divide only
-// when the estimate is within 1e-12 of a rounding boundary (numpy's q is the
-// correctly rounded quotient; the estimate is within a few ulp of it).
+// the fp32 estimate of eq4_device.cuh (code_of) and the float64 codec only
+// within NEAR of a rounding boundary, so every code is numpy's.
 // Rows wider than 256 read their elements straight from global memory.
 #include <cuda_runtime.h>
 
@@ -126,31 +125,6 @@ __device__ __forceinline__ double np_sum(const F& f, int n) {
   return __dadd_rn(0.0, np_pw(f, 0, n));
 }
 
-// uniform.py:77-79 / table.py:100-101 code of x under (lo, hi) with scale =
-// (hi - lo) / 15 (hi > lo): floor((clip(x) - lo) / scale + 0.5) clipped to [0, 15].
-struct Codec {
-  double lo, hi, scale, inv;
-  __device__ __forceinline__ double code(double x) const {
-    const double c = np_clip(x, lo, hi);
-    const double dl = __dsub_rn(c, lo);
-    const double t = __dadd_rn(__dmul_rn(dl, inv), 0.5);
-    const double fl = floor(t);
-    const double fr = __dsub_rn(t, fl);
-    double q = fl;
-    if (!(fr > 1e-12 && fr < 1.0 - 1e-12)) q = floor(__dadd_rn(__ddiv_rn(dl, scale), 0.5));
-    return np_clip(q, 0.0, 15.0);
-  }
-};
-
-__device__ __forceinline__ Codec make_codec(double lo, double hi) {
-  Codec c;
-  c.lo = lo;
-  c.hi = hi;
-  c.scale = div15(__dsub_rn(hi, lo));       // table.py:99 (exactly rounded w / 15)
-  c.inv = __drcp_rn(c.scale);
-  return c;
-}
-
 // table.py:81-103 quant_mse(x, (lo, hi), 4) of this lane's row, bit-exact.
 __device__ __forceinline__ double lane_quant_mse(const RowView& xr, int d, double lo, double hi) {
   if (hi == lo) {
@@ -159,11 +133,15 @@ __device__ __forceinline__ double lane_quant_mse(const RowView& xr, int d, doubl
       return __dmul_rn(e, e);
     }, d);
   }
-  const Codec cd = make_codec(lo, hi);
+  // codes: fp32 estimate, float64 codec within NEAR of a rounding boundary (exact either way)
+  const CodeParams cp = make_code_params(lo, hi);
   return np_sum([&](int k) {
-    const double x = (double)xr[k];
-    const double recon = __dadd_rn(__dmul_rn(cd.scale, cd.code(x)), lo);
-    const double e = __dsub_rn(x, recon);
+    const float xf = xr[k];
+    bool ne;
+    unsigned c = code_of(xf, cp, ne);
+    if (ne) c = code_exact(xf, cp);
+    const double recon = __dadd_rn(__dmul_rn(cp.scale, (double)c), lo);
+    const double e = __dsub_rn((double)xf, recon);
     return __dmul_rn(e, e);
   }, d);
 }
