@@ -11,9 +11,11 @@
 // the best SSE, movement < 1e-7 * spread), so each lane runs its own row's
 // Lloyd loop while the warp stages 32 rows as a [d][33] column tile.  The 16
 // centers live in registers (fully unrolled cluster loops); assignments are a
-// per-lane byte column in shared memory.
+// per-lane byte column in shared memory; each round's cluster means run over a
+// stable counting sort of the element indices by cluster (a byte column too).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -47,50 +49,39 @@ struct KMLane {
   __device__ __forceinline__ double v(int k) const { return (double)xs[k * KM_COL]; }
 };
 
-// numpy leaf (loops_utils.h.src) over the members [ms, me) of cluster j, in element order
-__device__ __forceinline__ double km_member_leaf(const KMLane& L, int d, int j, int ms, int me) {
-  const int n = me - ms;
+// numpy leaf over members [s0, s0 + n) of the cluster-sorted index column perm
+// (perm holds each cluster's members in element order: a stable counting sort)
+__device__ __forceinline__ double km_sorted_leaf(const KMLane& L, const uint8_t* perm, int s0, int n) {
+  auto f = [&](int i) { return L.v(perm[(s0 + i) * 32]); };
   if (n < 8) {
     double res = 0.0;
-    int mi = 0;
-    for (int k = 0; k < d && mi < me; k++) {
-      if (L.a[k * 32] != j) continue;
-      if (mi >= ms) res = __dadd_rn(res, L.v(k));
-      mi++;
-    }
+    for (int i = 0; i < n; i++) res = __dadd_rn(res, f(i));
     return res;
   }
-  const int nfull = n - (n % 8);
-  double r[8];
-  double tail[8];
-  int nt = 0;
-  int mi = 0;
-  for (int k = 0; k < d && mi < me; k++) {
-    if (L.a[k * 32] != j) continue;
-    if (mi >= ms) {
-      const int t = mi - ms;
-      const double x = L.v(k);
-      if (t < 8) r[t] = x;
-      else if (t < nfull) r[t & 7] = __dadd_rn(r[t & 7], x);
-      else tail[nt++] = x;
-    }
-    mi++;
+  double r0 = f(0), r1 = f(1), r2 = f(2), r3 = f(3), r4 = f(4), r5 = f(5), r6 = f(6), r7 = f(7);
+  const int nf = n - (n % 8);
+  int i = 8;
+  for (; i < nf; i += 8) {
+    r0 = __dadd_rn(r0, f(i));     r1 = __dadd_rn(r1, f(i + 1));
+    r2 = __dadd_rn(r2, f(i + 2)); r3 = __dadd_rn(r3, f(i + 3));
+    r4 = __dadd_rn(r4, f(i + 4)); r5 = __dadd_rn(r5, f(i + 5));
+    r6 = __dadd_rn(r6, f(i + 6)); r7 = __dadd_rn(r7, f(i + 7));
   }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (int i = 0; i < nt; i++) res = __dadd_rn(res, tail[i]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < n; i++) res = __dadd_rn(res, f(i));
   return res;
 }
 
-// members.mean(): 0.0 + pairwise sum (<= 256 members: at most two leaves) / m
-__device__ __forceinline__ double km_member_mean(const KMLane& L, int d, int j, int m) {
+// members.mean() of the m members at perm[s0 ..]: 0.0 + pairwise sum / m
+__device__ __forceinline__ double km_sorted_mean(const KMLane& L, const uint8_t* perm, int s0, int m) {
   double s;
   if (m <= 128) {
-    s = km_member_leaf(L, d, j, 0, m);
+    s = km_sorted_leaf(L, perm, s0, m);
   } else {
     int n2 = m / 2;
     n2 -= n2 % 8;
-    s = __dadd_rn(km_member_leaf(L, d, j, 0, n2), km_member_leaf(L, d, j, n2, m));
+    s = __dadd_rn(km_sorted_leaf(L, perm, s0, n2), km_sorted_leaf(L, perm, s0 + n2, m - n2));
   }
   return __ddiv_rn(__dadd_rn(0.0, s), (double)m);
 }
@@ -157,11 +148,13 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
   float* xs = reinterpret_cast<float*>(ws);
   uint8_t* abuf = ws + (((size_t)d * KM_COL * 4 + 15) & ~(size_t)15);
   uint8_t* bbuf = abuf + (size_t)d * 32;
-  uint8_t* out_base = bbuf + (((size_t)d * 32 + 15) & ~(size_t)15);
+  uint8_t* pbuf = bbuf + (size_t)d * 32;                                     // cluster-sorted indices
+  int* obuf = reinterpret_cast<int*>(pbuf + (((size_t)d * 32 + 15) & ~(size_t)15));   // [16][32] offsets
+  uint8_t* out_base = reinterpret_cast<uint8_t*>(obuf + KM_K * 32);
   const int ab = p.aux == EQ4_AUX_FP16 ? 2 : 4;
   const int64_t nblk = (p.rows + 31) / 32;
-  for (int64_t blk = (int64_t)blockIdx.x * KM_WARPS + warp; blk < nblk;
-       blk += (int64_t)gridDim.x * KM_WARPS) {
+  const int nw = blockDim.x >> 5;
+  for (int64_t blk = (int64_t)blockIdx.x * nw + warp; blk < nblk; blk += (int64_t)gridDim.x * nw) {
     const int64_t row0 = blk * 32, row = row0 + lane;
     const bool rvalid = row < p.rows;
     const int nrows = (int)min((int64_t)32, p.rows - row0);
@@ -174,6 +167,8 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
     L.xs = xs + lane;
     L.a = abuf + lane;
     L.ba = bbuf + lane;
+    uint8_t* perm = pbuf + lane;
+    int* offs = obuf + lane;
     double c[KM_K];
     int iters = -1;
     bool bad = false;
@@ -232,15 +227,30 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
             for (int j = 0; j < KM_K; j++) bc[j] = c[j];
             for (int k = 0; k < d; k++) L.ba[k * 32] = L.a[k * 32];
           }
+          // stable counting sort of the element indices by cluster (O(d), instead of a
+          // members scan per cluster), then each cluster's mean over its contiguous run
+          {
+            int o = 0;
+#pragma unroll
+            for (int j = 0; j < KM_K; j++) { offs[j * 32] = o; o += cnt[j]; }
+            for (int k = 0; k < d; k++) {
+              const int j = L.a[k * 32];
+              const int pos = offs[j * 32];
+              perm[pos * 32] = (uint8_t)k;
+              offs[j * 32] = pos + 1;
+            }
+          }
           double movement = 0.0;
+          int s0 = 0;
 #pragma unroll
           for (int j = 0; j < KM_K; j++) {
             if (cnt[j]) {
-              const double nc = km_member_mean(L, d, j, cnt[j]);
+              const double nc = km_sorted_mean(L, perm, s0, cnt[j]);
               const double t = fabs(__dsub_rn(nc, c[j]));
               movement = t > movement ? t : movement;
               c[j] = nc;
             }
+            s0 += cnt[j];
           }
           if (movement < stop) break;
         }
@@ -328,22 +338,27 @@ int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int
   p.half = (int)((dim + 1) / 2);
   p.stride = KM_K * (aux == EQ4_AUX_FP16 ? 2 : 4) + p.half;
   p.out = out; p.iters = iters; p.status = status;
-  size_t wb = (((size_t)dim * KM_COL * 4 + 15) & ~(size_t)15) + (((size_t)dim * 32 + 15) & ~(size_t)15) * 2 +
-              (size_t)32 * p.stride + 32;
+  // staged rows, assignments + best assignments, cluster-sorted indices, offsets, packed tile
+  size_t wb = (((size_t)dim * KM_COL * 4 + 15) & ~(size_t)15) + (size_t)dim * 32 * 2 +
+              (((size_t)dim * 32 + 15) & ~(size_t)15) + (size_t)KM_K * 32 * 4 + (size_t)32 * p.stride + 32;
   p.warp_bytes = (wb + 15) & ~(size_t)15;
-  const size_t smem = p.warp_bytes * KM_WARPS;
-  cudaError_t e = cudaFuncSetAttribute(k_kmeans_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int dev = 0, sms = 0, per_sm = 0;
-  if (e == cudaSuccess) e = cudaGetDevice(&dev);
+  int dev = 0, sms = 0, per_sm = 0, max_optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_rows, KM_THREADS, smem);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) { err = std::string("k_kmeans_rows setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+  // up to KM_WARPS row-block warps per block, fewer when a warp's slice is large (d = 256)
+  const int nw = (int)std::max<size_t>(1, std::min<size_t>(KM_WARPS, (size_t)max_optin / p.warp_bytes));
+  const size_t smem = p.warp_bytes * nw;
+  e = cudaFuncSetAttribute(k_kmeans_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_rows, nw * 32, smem);
   if (e != cudaSuccess) { err = std::string("k_kmeans_rows setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
   const int64_t nblk = (rows + 31) / 32;
-  int64_t grid = (nblk + KM_WARPS - 1) / KM_WARPS;
+  int64_t grid = (nblk + nw - 1) / nw;
   const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  k_kmeans_rows<<<(unsigned)grid, KM_THREADS, smem, s>>>(p);
+  k_kmeans_rows<<<(unsigned)grid, nw * 32, smem, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) { err = std::string("k_kmeans_rows: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
   return EQ4_OK;
