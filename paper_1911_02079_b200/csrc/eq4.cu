@@ -1926,6 +1926,14 @@ int eq4_quant_mse(const float* x, int64_t rows, int64_t dim, int64_t ld, const d
 // Host-buffer entry point: chunks of rows are staged through device memory on
 // two streams so that the H2D copy of chunk i+1, the kernel of chunk i and
 // the D2H copy of chunk i-1 overlap (copy engines run beside the SMs).
+// nr rows of a host table (row pitch ld floats) into a dense device chunk: one
+// linear copy when the rows are contiguous, a pitched copy otherwise
+static cudaError_t h2d_rows(float* dst, const float* src, int64_t nr, int64_t dim, int64_t ld,
+                            cudaStream_t s) {
+  if (ld == dim) return cudaMemcpyAsync(dst, src, (size_t)nr * dim * 4, cudaMemcpyHostToDevice, s);
+  return cudaMemcpy2DAsync(dst, dim * 4, src, ld * 4, dim * 4, nr, cudaMemcpyHostToDevice, s);
+}
+
 int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld, int method,
                            int b, double r, int aux, uint8_t* packed, double* xmin, double* xmax,
                            int32_t* info0, int32_t* info1, double* norm, int64_t chunk_rows,
@@ -1934,10 +1942,10 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
   if (ld < dim) return fail(EQ4_EINVAL, "ld must be >= dim");
   if (!x || !packed) return fail(EQ4_EINVAL, "null buffer");
   const int64_t stride = eq4_packed_row_stride(dim, aux);
-  int64_t chunk = chunk_rows > 0 ? chunk_rows : std::max<int64_t>(1024, (64ll << 20) / (dim * 4));
+  int64_t chunk = chunk_rows > 0 ? chunk_rows : std::max<int64_t>(1024, (16ll << 20) / (dim * 4));
   chunk = std::min(chunk, rows);
   const int64_t nchunks = (rows + chunk - 1) / chunk;
-  const int NS = 2;
+  const int NS = 3;   // chunk c's H2D overlaps chunk c-1's kernel and chunk c-2's D2H
   cudaStream_t st[NS];
   for (int i = 0; i < NS; i++) cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking);
   struct Buf { float* x; uint8_t* out; double* lo; double* hi; int32_t* i0; int32_t* i1; int32_t* status; };
@@ -1968,7 +1976,7 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
     for (int64_t c = 0; c < nchunks && rc == EQ4_OK; c++) {
       const int si = (int)(c % NS);
       const int64_t r0 = c * chunk, nr = std::min(chunk, rows - r0);
-      e = cudaMemcpy2DAsync(bf[si].x, dim * 4, x + r0 * ld, ld * 4, dim * 4, nr, cudaMemcpyHostToDevice, st[si]);
+      e = h2d_rows(bf[si].x, x + r0 * ld, nr, dim, ld, st[si]);
       if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
       rc = table_keys_accumulate(bf[si].x, nr, dim, dim, tkeys, st[si]);
     }
@@ -1982,7 +1990,7 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
     cudaStream_t s = st[si];
     Buf& B = bf[si];
     const int64_t r0 = c * chunk, nr = std::min(chunk, rows - r0);
-    e = cudaMemcpy2DAsync(B.x, dim * 4, x + r0 * ld, ld * 4, dim * 4, nr, cudaMemcpyHostToDevice, s);
+    e = h2d_rows(B.x, x + r0 * ld, nr, dim, ld, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(B.status, 0, 4, s);
     if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
     rc = quantize_pack_impl(B.x, nr, dim, dim, method, b, r, aux, B.out, B.lo, B.hi, B.i0, B.i1,
