@@ -47,7 +47,8 @@ def test_hist_apprx_reference_windows():
                 assert np.array_equal(p.buffer, f[f"packed_{tname}"]), tname
 
 
-@pytest.mark.parametrize("rows,d,b", [(3000, 64, 200), (1000, 17, 256), (2000, 128, 100), (500, 300, 200)])
+@pytest.mark.parametrize("rows,d,b", [(3000, 64, 200), (1000, 17, 256), (2000, 128, 100), (500, 300, 200),
+                                      (300, 64, 1), (300, 9, 2), (200, 2048, 64), (400, 1, 16)])
 def test_hist_apprx_vs_oracle(rows, d, b):
     x = rng.mixed_table(rows, d, d + b)
     want = oracle.quantize_pack_table(x, "hist-apprx", b, 0.16, "fp16")

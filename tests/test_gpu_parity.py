@@ -238,8 +238,9 @@ def test_hist_brute_vs_oracle_config4_sample(eq):
     assert len(ties) <= 1
 
 
-@pytest.mark.parametrize("b,d,rows", [(8, 7, 400), (16, 64, 400), (40, 1, 50), (64, 300, 200),
-                                      (200, 17, 200), (200, 2048, 24), (250, 64, 48), (400, 33, 16)])
+@pytest.mark.parametrize("b,d,rows", [(1, 64, 100), (2, 9, 100), (8, 7, 400), (16, 64, 400), (40, 1, 50),
+                                      (64, 300, 200), (200, 17, 200), (200, 2048, 24), (250, 64, 48),
+                                      (400, 33, 16)])
 def test_hist_brute_vs_oracle_shapes(eq, b, d, rows):
     """Other b and d (incl. d = 1, ragged d, d > b, and the longest rows) with constant rows
     and repeated values; windows must match the oracle except genuine norm ties."""
