@@ -477,7 +477,7 @@ def _apply_counters(counters: WorkCounters, method: str, b: int, rr: RowResults)
 def quantize_table(table, method: str, nbits: int = 4, aux_precision: str = "fp32", b: int = 200,
                    r: float = 0.16, k: int | None = None, seed: int = 0,
                    counters: WorkCounters | None = None) -> UniformQuantTable:
-    """methods.py:63-89 for the GPU methods (asym, greedy, hist-brute; 4-bit)."""
+    """methods.py:63-89: every uniform method (GPU_METHODS) and row-wise kmeans at 4 bits."""
     if method not in ALL_METHODS:
         raise ValueError(f"unknown method {method!r}; expected one of {ALL_METHODS}")
     if method in CODEBOOK_METHODS and nbits != 4:
