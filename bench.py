@@ -65,6 +65,11 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi takes ~0.1-0.5 s to emit its first sample: start the timed region only
+            # once it is sampling, so the samples cover the whole region
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3.0 and self.proc.poll() is None:
+                time.sleep(0.005)
         except OSError:
             self.proc = None
         return self
