@@ -139,7 +139,8 @@ struct HistSlice {
   __host__ __device__ size_t nzj_off() const { return lb_off() + (size_t)(b + 1) * 4; }     // int[m]
   __host__ __device__ size_t xs_off() const { return nzj_off() + (size_t)m * 4; }           // float[d]
   __host__ __device__ size_t codes_off() const { return xs_off() + (size_t)d * 4; }         // u8[d]
-  __host__ __device__ size_t bytes() const { return (codes_off() + (size_t)d + 15) & ~(size_t)15; }
+  __host__ __device__ size_t wq_off() const { return (codes_off() + (size_t)d + 15) & ~(size_t)15; }   // int[64]
+  __host__ __device__ size_t bytes() const { return wq_off() + 64 * 4; }
 };
 
 __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
   int* nzj = reinterpret_cast<int*>(ws + S.nzj_off());
   float* xs = reinterpret_cast<float*>(ws + S.xs_off());
   uint8_t* codes = ws + S.codes_off();
+  int* wq = reinterpret_cast<int*>(ws + S.wq_off());
 
   for (int64_t row = (int64_t)blockIdx.x * nw + warp; row < p.rows; row += (int64_t)gridDim.x * nw) {
     // ---- row, min/max, finiteness ----
@@ -353,25 +355,50 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
           if (__hiloint2double((int)hw, 0) > bound) n0 = mid + 1; else nhi = mid;
         }
       }
+      // Surviving windows are sparse (a few % of the starts of a width), so they
+      // are queued as packed (n << 16 | s) in (n asc, s asc) order and scored 32 at
+      // a time, one per lane, instead of idling most lanes of a width's pass.  The
+      // bound tightens after every batch.
       double bv = INFINITY;
       int bn = 1 << 30, bs = 1 << 30;
-      for (int n = n0; n <= b; n++) {
-        const double* Un = Us + (size_t)(n - 1) * n / 2;
-        for (int s = lane; s <= b - n; s += 32) {
-          if (__dmul_rn(__dadd_rn(A3[s], R3[s + n]), 1.0 / 3.0) > bound) continue;   // <= v
+      int qn = 0;   // queued windows (warp-uniform)
+      auto score_batch = [&](int cnt) {
+        if (lane < cnt) {
+          const int e = wq[lane];
+          const int n = e >> 16, s = e & 0xffff;
+          const double* Ub = Us + (size_t)(n - 1) * n / 2 - s;
           double acc = 0.0;
           const int i1 = lb[s + n];
-          const double* Ub = Un - s;
 #pragma unroll 4
           for (int i = lb[s]; i < i1; i++) acc = fma(nzc[i], Ub[nzj[i]], acc);
           const double v = __fma_rn(__dadd_rn(A3[s], R3[s + n]), 1.0 / 3.0, acc);   // one rounding
-          if (v < bv) { bv = v; bn = n; bs = s; }
+          if (v < bv || (v == bv && (n < bn || (n == bn && s < bs)))) { bv = v; bn = n; bs = s; }
         }
         // values are >= 0, so their high words order like the values: the warp
         // minimum of the high words, low word all ones, bounds the minimum from above
         const unsigned hw = __reduce_min_sync(FULL, (unsigned)__double2hiint(bv));
         bound = fmin(bound, __hiloint2double((int)hw, (int)0xffffffffu));
+      };
+      for (int n = n0; n <= b; n++) {
+        for (int s0 = 0; s0 <= b - n; s0 += 32) {
+          const int s = s0 + lane;
+          const bool keep = s <= b - n &&
+                            !(__dmul_rn(__dadd_rn(A3[s], R3[s + n]), 1.0 / 3.0) > bound);   // o <= v
+          const unsigned bal = __ballot_sync(FULL, keep);
+          if (keep) wq[qn + __popc(bal & ((1u << lane) - 1u))] = (n << 16) | s;
+          qn += __popc(bal);
+          __syncwarp();
+          if (qn >= 32) {
+            score_batch(32);
+            const int rest = lane < qn - 32 ? wq[32 + lane] : 0;
+            __syncwarp();
+            if (lane < qn - 32) wq[lane] = rest;
+            qn -= 32;
+            __syncwarp();
+          }
+        }
       }
+      if (qn > 0) score_batch(qn);
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) {
         const double ov = __shfl_xor_sync(FULL, bv, o);
