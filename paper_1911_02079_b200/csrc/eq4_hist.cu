@@ -128,16 +128,21 @@ __device__ __forceinline__ void hist_emit(const HistParams& p, int64_t row, int 
 // b = 200) cost more in occupancy than it saved (measured 0.724 vs 0.726 ms at
 // d = 64, 1.76 vs 1.68 ms at d = 128).
 // ---------------------------------------------------------------------------
+// a non-empty bin: index and count (as a double), loaded with one 16-byte access
+struct __align__(16) NzBin {
+  int j, pad;
+  double c;
+};
+
 struct HistSlice {
   int b, d, m;   // m = min(b, d): most non-empty bins a row can have
   __host__ __device__ size_t a3_off() const { return 0; }                                   // double[b+1]
   __host__ __device__ size_t r3_off() const { return a3_off() + (size_t)(b + 1) * 8; }      // double[b+1]
   __host__ __device__ size_t tmp_off() const { return r3_off() + (size_t)(b + 1) * 8; }     // double[b] (HIST-APPRX)
-  __host__ __device__ size_t nzc_off() const { return tmp_off() + (size_t)b * 8; }          // double[m]
-  __host__ __device__ size_t cnt_off() const { return nzc_off() + (size_t)m * 8; }          // int[b]
+  __host__ __device__ size_t nz_off() const { return (tmp_off() + (size_t)b * 8 + 15) & ~(size_t)15; }   // NzBin[m]
+  __host__ __device__ size_t cnt_off() const { return nz_off() + (size_t)m * 16; }          // int[b]
   __host__ __device__ size_t lb_off() const { return cnt_off() + (size_t)b * 4; }           // int[b+1]
-  __host__ __device__ size_t nzj_off() const { return lb_off() + (size_t)(b + 1) * 4; }     // int[m]
-  __host__ __device__ size_t xs_off() const { return nzj_off() + (size_t)m * 4; }           // float[d]
+  __host__ __device__ size_t xs_off() const { return lb_off() + (size_t)(b + 1) * 4; }      // float[d]
   __host__ __device__ size_t codes_off() const { return xs_off() + (size_t)d * 4; }         // u8[d]
   __host__ __device__ size_t wq_off() const { return (codes_off() + (size_t)d + 15) & ~(size_t)15; }   // int[64]
   __host__ __device__ size_t bytes() const { return wq_off() + 64 * 4; }
@@ -172,7 +177,7 @@ constexpr double APPRX_TOL = 1e-11;   // relative gap below which the walk re-de
 // own float64 values (apprx_norm_np_warp: its elementwise formula in numpy's
 // pairwise order), as is the reported norm of the chosen window.
 __device__ __forceinline__ void hist_apprx_walk(const double* Us, const double* A3, const double* R3,
-                                                const double* nzc, const int* nzj, const int* cnt,
+                                                const NzBin* nz, const int* cnt,
                                                 double* tmp, int m, int b, double w, int lane, int& best_s,
                                                 int& best_n, double& norm) {
   auto exact = [&](int s0, int n0) -> double { return apprx_norm_np_warp(cnt, b, w, s0, n0, tmp, lane); };
@@ -181,7 +186,7 @@ __device__ __forceinline__ void hist_apprx_walk(const double* Us, const double* 
   {
     const double* Ub = Us + (size_t)(b - 1) * b / 2;
     double a = 0.0;
-    for (int i = lane; i < m; i += 32) a = fma(nzc[i], Ub[nzj[i]], a);
+    for (int i = lane; i < m; i += 32) a = fma(nz[i].c, Ub[nz[i].j], a);
     bestF = __fma_rn(__dadd_rn(A3[0], R3[b]), 1.0 / 3.0, warp_sum_d(a));
   }
   double bestN = 0.0;
@@ -192,8 +197,9 @@ __device__ __forceinline__ void hist_apprx_walk(const double* Us, const double* 
     const double* Un = Us + (size_t)(nn - 1) * nn / 2;
     double aL = 0.0, aR = 0.0;
     for (int i = lane; i < m; i += 32) {
-      const int j = nzj[i];
-      const double c = nzc[i];
+      const NzBin e = nz[i];
+      const int j = e.j;
+      const double c = e.c;
       const int kL = j - st - 1, kR = j - st;
       if ((unsigned)kL < (unsigned)nn) aL = fma(c, Un[kL], aL);
       if ((unsigned)kR < (unsigned)nn) aR = fma(c, Un[kR], aR);
@@ -243,10 +249,9 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
   unsigned char* ws = smem + (size_t)warp * S.bytes();
   double* A3 = reinterpret_cast<double*>(ws + S.a3_off());
   double* R3 = reinterpret_cast<double*>(ws + S.r3_off());
-  double* nzc = reinterpret_cast<double*>(ws + S.nzc_off());
+  NzBin* nz = reinterpret_cast<NzBin*>(ws + S.nz_off());
   int* cnt = reinterpret_cast<int*>(ws + S.cnt_off());
   int* lb = reinterpret_cast<int*>(ws + S.lb_off());
-  int* nzj = reinterpret_cast<int*>(ws + S.nzj_off());
   float* xs = reinterpret_cast<float*>(ws + S.xs_off());
   uint8_t* codes = ws + S.codes_off();
   int* wq = reinterpret_cast<int*>(ws + S.wq_off());
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
         const unsigned bal = __ballot_sync(FULL, c != 0);
         const int pos = m + __popc(bal & ((1u << lane) - 1u));
         if (j < b) lb[j] = pos;
-        if (c) { nzc[pos] = (double)c; nzj[pos] = j; }
+        if (c) nz[pos] = NzBin{j, 0, (double)c};
         t1 += (double)c * j;
         t2 += (double)c * j * j;
         m += __popc(bal);
@@ -319,7 +324,7 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
       }
       __syncwarp();
       if constexpr (APPRX) {
-        hist_apprx_walk(Us, A3, R3, nzc, nzj, cnt, reinterpret_cast<double*>(ws + S.tmp_off()), m, b, w, lane,
+        hist_apprx_walk(Us, A3, R3, nz, cnt, reinterpret_cast<double*>(ws + S.tmp_off()), m, b, w, lane,
                         best_s, best_n, norm);
         wlo = __dadd_rn(lo, __dmul_rn(w, (double)best_s));          // histclip.py:214-219
         whi = __dadd_rn(lo, __dmul_rn(w, (double)(best_s + best_n)));
@@ -336,7 +341,7 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
         const double* Ub = Us + (size_t)(b - 1) * b / 2;
         double acc = 0.0;
         if (lane == 0)
-          for (int i = 0; i < m; i++) acc = fma(nzc[i], Ub[nzj[i]], acc);
+          for (int i = 0; i < m; i++) acc = fma(nz[i].c, Ub[nz[i].j], acc);
         bound = __shfl_sync(FULL, __fma_rn(__dadd_rn(A3[0], R3[b]), 1.0 / 3.0, acc), 0);
       }
       // Widths below n0 are skipped whole: the outside part o(s, n) is
@@ -370,7 +375,10 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
           double acc = 0.0;
           const int i1 = lb[s + n];
 #pragma unroll 4
-          for (int i = lb[s]; i < i1; i++) acc = fma(nzc[i], Ub[nzj[i]], acc);
+          for (int i = lb[s]; i < i1; i++) {
+            const NzBin e = nz[i];   // one 16-byte load
+            acc = fma(e.c, Ub[e.j], acc);
+          }
           const double v = __fma_rn(__dadd_rn(A3[s], R3[s + n]), 1.0 / 3.0, acc);   // one rounding
           if (v < bv || (v == bv && (n < bn || (n == bn && s < bs)))) { bv = v; bn = n; bs = s; }
         }
