@@ -1683,18 +1683,26 @@ static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
   }
 }
 
-// GREEDY error-band constants: per side, the fp32
-// loss carries <= (E - 1 + log2 LPR + 2) u relative summation error; both
-// sides -> x2; 5% margin.
-static float tau2_for(int d) {
+// GREEDY error-band constants.  The fp32 loss of one
+// candidate is a sum of exactly computed squares (each squared and added by one
+// FMA), so its error is <= gamma_h * S with h the most roundings any term passes
+// through: the packed kernels (d a power of two, 16-byte rows) accumulate E/2
+// terms per f32x2 half, add the halves and reduce LPR lanes (E/2 + 1 + log2 LPR);
+// the masked kernels run one chain of up to E terms per lane (E + log2 LPR).
+// (LPR, E) must follow dispatch_rq's GREEDY table.  Both sides -> x2; one extra
+// rounding and 5% margin.
+static float tau2_for(int d, bool vec) {
   int lpr, e;
-  if (d <= 16) { lpr = 1; e = 16; }
+  if (d <= 8) { lpr = 1; e = 8; }
+  else if (d <= 16) { lpr = 1; e = 16; }
   else if (d <= 32) { lpr = 1; e = 32; }
-  else if (d <= 1024) { lpr = 1; while (lpr * 32 < d) lpr *= 2; e = 32; }
-  else { lpr = 32; e = 64; }
+  else { lpr = 1; while (lpr * 64 < d) lpr *= 2; e = 64; }
+  const bool packed = vec && (d == 16 || d == 32 || d == 64 || d == 128 || d == 256 || d == 512 ||
+                              d == 1024 || d == 2048);
   int lg = 0;
   while ((1 << lg) < lpr) lg++;
-  return (float)(2.0 * 1.05 * (e - 1 + lg + 2) * 5.9604645e-8);
+  const int h = (packed ? e / 2 + 1 : e) + lg + 1;
+  return (float)(2.0 * 1.05 * h * 5.9604645e-8);
 }
 
 extern "C" {
@@ -1858,7 +1866,7 @@ static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t
     p.qY = std::ldexp(1.0, ey - 24);
     p.inv_qY = 1.0 / p.qY;
     p.delta = (float)(p.qY * 0.5);
-    p.tau2 = tau2_for((int)dim);
+    p.tau2 = tau2_for((int)dim, vec);
     // misround: the code argument alpha*s carries |error| <= eta = 4u*alpha
     // (approximate reciprocal 2u, product/add roundings), so a code can differ
     // from the reference's only for elements within eta of a rounding
