@@ -202,6 +202,9 @@ __device__ __forceinline__ int lane_gss(const RowView& xr, int d, float mn, floa
   return n;
 }
 
+// one instantiation per method: GSS's float64 search state must not shape
+// ACIQ's register allocation (ACIQ is a bandwidth-class path)
+template <int METHOD>
 __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
     double lo = 0.0, hi = 0.0;
     int evals = 0;
     if (rvalid && !bad) {
-      if (p.method == EQ4_METHOD_ACIQ) {
+      if constexpr (METHOD == EQ4_METHOD_ACIQ) {
         lane_aciq(xr, d, mn, mx, lo, hi);
       } else {
         evals = lane_gss(xr, d, mn, mx, p.invphi, lo, hi);
@@ -348,18 +351,19 @@ int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, i
   p.warp_bytes = ((xs_bytes + 15) & ~(size_t)15) + (((size_t)32 * p.stride + 32 + 15) & ~(size_t)15);
   p.warp_bytes = (p.warp_bytes + 15) & ~(size_t)15;
   const size_t smem = p.warp_bytes * RR_WARPS;
-  cudaError_t e = cudaFuncSetAttribute(k_rowrange, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = method == EQ4_METHOD_ACIQ ? k_rowrange<EQ4_METHOD_ACIQ> : k_rowrange<EQ4_METHOD_GSS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 0, per_sm = 0;
   if (e == cudaSuccess) e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rowrange, RR_THREADS, smem);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RR_THREADS, smem);
   if (e != cudaSuccess) { err = std::string("k_rowrange setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
   const int64_t nblk = (rows + 31) / 32;
   int64_t grid = (nblk + RR_WARPS - 1) / RR_WARPS;
   const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  k_rowrange<<<(unsigned)grid, RR_THREADS, smem, s>>>(p);
+  kern<<<(unsigned)grid, RR_THREADS, smem, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) { err = std::string("k_rowrange: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
   return EQ4_OK;
