@@ -54,6 +54,30 @@ def test_methods_random_vs_oracle(method, rows, d, gen):
         assert np.array_equal(rr.info0.cpu().numpy(), want.info0)
 
 
+@pytest.mark.parametrize("d", [8, 9, 15, 16, 17, 31, 63, 100, 127, 128, 129])
+def test_aciq_leaf_shapes_vs_oracle(d):
+    """The warp-cooperative ACIQ kernel (one numpy leaf per row, 8 <= d <= 128) and its
+    neighbours: ragged d, a row count that leaves a partial 4-row group, constant rows
+    (alpha == 0 -> the data range), all-zero rows, signed zeros and an unaligned table."""
+    rows = 4003
+    x = rng.mixed_table(rows, d, 500 + d)
+    x[1] = 3.25                     # constant row: alpha = 0
+    x[2] = 0.0                      # all zeros
+    x[3, ::2] = -0.0
+    x[5, : d // 2] = x[5, d // 2: 2 * (d // 2)]   # repeated values
+    for aux in ("fp16", "fp32"):
+        want = oracle.quantize_pack_table(x, "aciq", 200, 0.16, aux)
+        p, rr = eq.quantize_pack_table4(torch.from_numpy(x).cuda(), "aciq", aux, with_rows=True)
+        assert np.array_equal(p.buffer, want.packed), aux
+        assert np.array_equal(rr.xmin.cpu().numpy(), want.xmin)
+        assert np.array_equal(rr.xmax.cpu().numpy(), want.xmax)
+        assert np.array_equal(np.signbit(rr.xmin.cpu().numpy()), np.signbit(want.xmin))
+    # a column slice of a wider table (ld > d) starting at an odd float offset
+    wide = torch.from_numpy(np.ascontiguousarray(np.pad(x, ((0, 0), (1, 2))))).cuda()
+    p2, _ = eq.quantize_pack_table4(wide[:, 1:1 + d], "aciq", "fp16", with_rows=True)
+    assert np.array_equal(p2.buffer, oracle.quantize_pack_table(x, "aciq", 200, 0.16, "fp16").packed)
+
+
 def test_method_api_single_rows_and_counters():
     x = rng.sample_table("laplacian", 0.0, 1.0, 7, 5, 64)
     for row in x:
