@@ -33,6 +33,7 @@ constexpr int RR_THREADS = 128;
 constexpr int RR_WARPS = RR_THREADS / 32;
 constexpr int RR_MAX_STAGED = 256;   // d above this reads global memory
 constexpr int RR_COL = 33;           // padded column stride (floats) of the staged tile
+constexpr float MAGIC_F = 8388608.f;  // 2^23: x + 2^23 rounded down leaves floor(x) in the low mantissa bits
 
 struct RRParams {
   const float* x;
@@ -284,22 +285,40 @@ __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
     if (rvalid) {
       uint8_t* orow = out_tile + (size_t)lane * p.stride;
       const bool degenerate = bad || hi == lo;
-      // fp32 code estimate, float64 codec within NEAR of a rounding boundary
       const CodeParams cp = make_code_params(degenerate ? 0.0 : lo, degenerate ? 0.0 : hi);
-      for (int m = 0; m < p.half; m++) {
-        unsigned c0 = 0, c1 = 0;
-        if (!degenerate) {
-          bool ne0, ne1 = false;
+      // Branch-free fp32 codes: s = sat((x - lo) / (hi - lo)) clamps below lo / above hi
+      // (codes 0 / 15 there, as numpy's clip), code = floor(15 s + 1/2) by a round-down
+      // add of 2^23, and g = 15 s - code tracks the distance to a rounding boundary.
+      // A row with any element within NEAR of a boundary (or an extreme range) takes
+      // the exact codec for every element (rare).
+      bool exact_row = degenerate || cp.slow;
+      if (!exact_row) {
+        const float inv1 = cp.inv * (1.f / 15.f);
+        float gmax = 0.f;
+        for (int m = 0; m < p.half; m++) {
           const float x0 = xr[2 * m];
-          c0 = code_of(x0, cp, ne0);
-          if (2 * m + 1 < d) {
-            const float x1 = xr[2 * m + 1];
-            c1 = code_of(x1, cp, ne1);
-            if (ne1) c1 = code_exact(x1, cp);
-          }
-          if (ne0) c0 = code_exact(x0, cp);
+          const float x1 = (2 * m + 1 < d) ? xr[2 * m + 1] : cp.lo_hi;
+          const float s0 = __saturatef(__fmul_rn(__fadd_rn(__fadd_rn(x0, -cp.lo_hi), -cp.lo_lo), inv1));
+          const float s1 = __saturatef(__fmul_rn(__fadd_rn(__fadd_rn(x1, -cp.lo_hi), -cp.lo_lo), inv1));
+          const float m0 = __fadd_rd(__fmaf_rn(s0, 15.f, 0.5f), MAGIC_F), m1 = __fadd_rd(__fmaf_rn(s1, 15.f, 0.5f), MAGIC_F);
+          const float g0 = __fmaf_rn(s0, 15.f, -__fadd_rn(m0, -MAGIC_F));
+          const float g1 = __fmaf_rn(s1, 15.f, -__fadd_rn(m1, -MAGIC_F));
+          gmax = fmaxf(gmax, fmaxf(fabsf(g0), fabsf(g1)));
+          const unsigned c0 = __float_as_uint(m0) & 0xFu;
+          const unsigned c1 = (2 * m + 1 < d) ? (__float_as_uint(m1) & 0xFu) : 0u;   // packed.py:75-76
+          orow[m] = (uint8_t)(c0 | (c1 << 4));
         }
-        orow[m] = (uint8_t)(c0 | (c1 << 4));
+        exact_row = gmax > 0.5f - NEAR;
+      }
+      if (exact_row) {
+        for (int m = 0; m < p.half; m++) {
+          unsigned c0 = 0, c1 = 0;
+          if (!degenerate) {
+            c0 = code_exact(xr[2 * m], cp);
+            if (2 * m + 1 < d) c1 = code_exact(xr[2 * m + 1], cp);
+          }
+          orow[m] = (uint8_t)(c0 | (c1 << 4));
+        }
       }
       const double sc = degenerate ? 0.0 : cp.scale;   // uniform.py:74-80
       uint8_t* a = orow + p.half;
