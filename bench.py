@@ -255,7 +255,7 @@ def run_ours(args, rank: int, world: int):
         with open(tp) as f:
             traffic = json.load(f).get("greedy_20Mx64", {}).get("dram_bytes_per_launch")
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:   # the reported CPU baseline: rank 0 at N = 1 only
         rate, cores, t = cpu_reference_rate(args.cpu_rows)
         cpu = {"value": rate, "unit": "rows/s", "cores": cores, "kind": "port",
                "sample": f"{args.cpu_rows} rows x {DIM} mixed, GREEDY b=200 r=0.16 fp16 "
@@ -282,7 +282,7 @@ def run_ours(args, rank: int, world: int):
         "gpu_launches": args.steps,
         "clocks": clocks.summary(),
     }
-    if args.secondary:
+    if args.secondary and world == 1:   # the other configs are single-GPU lines
         line["secondary"] = secondary(eq, workloads, torch, dev, peaks, fp32_peak)
         line["secondary"]["sls_20Mx64_greedy_packed"] = sls_secondary(eq, torch, dev, peaks, out, rows)
     print(json.dumps(line), flush=True)
