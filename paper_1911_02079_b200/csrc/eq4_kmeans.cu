@@ -347,11 +347,21 @@ int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e != cudaSuccess) { err = std::string("k_kmeans_rows setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
-  // up to KM_WARPS row-block warps per block, fewer when a warp's slice is large (d = 256)
-  const int nw = (int)std::max<size_t>(1, std::min<size_t>(KM_WARPS, (size_t)max_optin / p.warp_bytes));
+  // The per-warp slice (staged rows, assignment columns) makes shared memory the
+  // occupancy limit: pick the block width (1..KM_WARPS row-warps) that keeps the
+  // most warps resident per SM (the Lloyd loops are latency chains).
+  int nw = 1, best_warps = 0;
+  for (int w = 1; w <= KM_WARPS; w++) {
+    const size_t sm_w = p.warp_bytes * w;
+    if (sm_w > (size_t)max_optin) break;
+    int blocks = 0;
+    e = cudaFuncSetAttribute(k_kmeans_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_kmeans_rows, w * 32, sm_w);
+    if (e != cudaSuccess) { err = std::string("k_kmeans_rows setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+    if (blocks * w > best_warps) { best_warps = blocks * w; nw = w; per_sm = blocks; }
+  }
   const size_t smem = p.warp_bytes * nw;
   e = cudaFuncSetAttribute(k_kmeans_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_rows, nw * 32, smem);
   if (e != cudaSuccess) { err = std::string("k_kmeans_rows setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
   const int64_t nblk = (rows + 31) / 32;
   int64_t grid = (nblk + nw - 1) / nw;
