@@ -367,17 +367,17 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
       double bv = INFINITY;
       int bn = 1 << 30, bs = 1 << 30;
       int qn = 0;   // queued windows (warp-uniform)
-      auto score_batch = [&](int cnt) {
-        if (lane < cnt) {
-          const int e = wq[lane];
-          const int n = e >> 16, s = e & 0xffff;
+      auto score_batch = [&](int count) {
+        if (lane < count) {
+          const int qe = wq[lane];
+          const int n = qe >> 16, s = qe & 0xffff;
           const double* Ub = Us + (size_t)(n - 1) * n / 2 - s;
           double acc = 0.0;
           const int i1 = lb[s + n];
 #pragma unroll 4
           for (int i = lb[s]; i < i1; i++) {
-            const NzBin e = nz[i];   // one 16-byte load
-            acc = fma(e.c, Ub[e.j], acc);
+            const NzBin nb = nz[i];   // one 16-byte load
+            acc = fma(nb.c, Ub[nb.j], acc);
           }
           const double v = __fma_rn(__dadd_rn(A3[s], R3[s + n]), 1.0 / 3.0, acc);   // one rounding
           if (v < bv || (v == bv && (n < bn || (n == bn && s < bs)))) { bv = v; bn = n; bs = s; }
