@@ -320,8 +320,8 @@ def _time_method(eq, torch, dev, x, method, b, n=10, warm=3):
 def secondary(eq, workloads, torch, dev, peaks, fp32_peak):
     """The other BASELINE.json configs, device-timed (each table >> L2 or re-read per launch):
     config 2 (ASYM 4M x 64, HBM-bound), config 3 (GREEDY 4M x 128 mixed), config 4 (HIST-BRUTE
-    16,384 x 64), config 5a (GREEDY d-sweep over 1 GiB N(0,1) tables), plus the HIST-APPRX and
-    ACIQ searches on their own representative tables."""
+    16,384 x 64), config 5a (GREEDY d-sweep over 1 GiB N(0,1) tables), plus the HIST-APPRX, ACIQ
+    and GSS searches and row-wise KMEANS (§8f.4) on representative tables."""
     hbm = float(peaks.get("hbm_gbs", 6546.9))
     res = {}
 
@@ -358,6 +358,28 @@ def secondary(eq, workloads, torch, dev, peaks, fp32_peak):
     ms, _ = _time_method(eq, torch, dev, x, "aciq", B)
     res["aciq_4Mx64"] = {"ms": ms, "GBps": byt / ms / 1e6, "hbm_frac": byt / ms / 1e6 / hbm}
     del x
+    # GSS (clipping.py:70-112): ~23 exact float64 quant_mse per row
+    x = workloads.gaussian_table(1_048_576, 64, 7, device=dev)
+    ms, _ = _time_method(eq, torch, dev, x, "gss", B, n=5, warm=2)
+    res["gss_1Mx64"] = {"ms": ms, "rows_per_s": 1_048_576 / ms * 1e3}
+    del x
+    # row-wise KMEANS codebooks (codebook.py:35-172), the EMBQ kmeans_row payload
+    from paper_1911_02079_b200.codebook import kmeans_rows, kmeans_row_stride
+    x = workloads.gaussian_table(262_144, 128, 7, device=dev)
+    kout = torch.empty(262_144 * kmeans_row_stride(128, AUX), dtype=torch.uint8, device=dev)
+    kit = torch.empty(262_144, dtype=torch.int32, device=dev)
+    kmeans_rows(x, AUX, out=kout, iters=kit)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(5):
+        kmeans_rows(x, AUX, out=kout, iters=kit, check=False)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / 5
+    res["kmeans_rows_262144x128"] = {"ms": ms, "rows_per_s": 262_144 / ms * 1e3,
+                                     "mean_lloyd_rounds": float(kit.clamp(min=0).float().mean().item())}
+    del x, kout, kit
     # config 5a: GREEDY d-sweep, rows = 2^30 / (4 d): 1 GiB of fp32 per table
     sweep = {}
     for d in (16, 32, 64, 128, 256, 512, 1024, 2048):
