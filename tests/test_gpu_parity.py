@@ -318,6 +318,42 @@ def test_greedy_other_b_r_vs_oracle(eq, b, r):
     assert np.array_equal(rr.xmax.cpu().numpy(), want.xmax)
 
 
+def _grid_rows(rows, d, seed):
+    """Rows of few distinct values (integers, dyadic grids, a handful of repeated centres):
+    many elements sit exactly on, or just off, the candidates' code boundaries."""
+    g = np.random.default_rng(seed)
+    x = np.empty((rows, d), np.float32)
+    for i in range(rows):
+        kind = i % 4
+        if kind == 0:
+            x[i] = g.integers(0, g.integers(2, 41), d)
+        elif kind == 1:
+            x[i] = g.integers(-64, 64, d) * np.float32(2.0 ** -int(g.integers(0, 8)))
+        elif kind == 2:
+            c = g.normal(size=int(g.integers(3, 11))).astype(np.float32)
+            x[i] = c[g.integers(0, c.size, d)]
+        else:
+            x[i] = np.round(g.normal(size=d) * 8) / 8 * np.float32(g.choice([1.0, 3.0, 0.1, 1e3]))
+    return x
+
+
+@pytest.mark.parametrize("d,b,r", [(64, 200, 0.16), (16, 200, 0.16), (128, 150, 0.3), (33, 64, 0.16),
+                                   (256, 200, 0.16)])
+def test_greedy_grid_valued_rows_vs_oracle(eq, d, b, r):
+    """Repeated and grid-aligned values: code flips of many elements at once (the error
+    band's code-flip term) and exact loss ties; every row must still match the oracle."""
+    import torch
+
+    x = _grid_rows(6000, d, 1000 * d + b)
+    want = oracle.quantize_pack_table(x, "greedy", b, r, "fp16")
+    p, rr = eq.quantize_pack_table4(torch.from_numpy(x).cuda(), "greedy", "fp16", b, r, with_rows=True)
+    stride = eq.packed_row_stride(d, "fp16")
+    bad = _mismatch_rows(p.buffer, want.packed, stride)
+    assert bad.size == 0, bad[:10]
+    assert np.array_equal(rr.xmin.cpu().numpy(), want.xmin)
+    assert np.array_equal(rr.xmax.cpu().numpy(), want.xmax)
+
+
 @pytest.mark.slow
 def test_large_table_beyond_int32_elements(eq):
     """rows * d > 2^31 (40M x 64 = 10.2 GB): 64-bit addressing in the GREEDY and ASYM kernels;
