@@ -45,7 +45,6 @@ struct KMParams {
 struct KMLane {
   const float* xs;   // this lane's column: element k at xs[k * KM_COL]
   uint8_t* a;        // assignments, element k at a[k * 32]
-  uint8_t* ba;       // best assignments
   __device__ __forceinline__ double v(int k) const { return (double)xs[k * KM_COL]; }
 };
 
@@ -147,8 +146,7 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
   const int d = p.d;
   float* xs = reinterpret_cast<float*>(ws);
   uint8_t* abuf = ws + (((size_t)d * KM_COL * 4 + 15) & ~(size_t)15);
-  uint8_t* bbuf = abuf + (size_t)d * 32;
-  uint8_t* pbuf = bbuf + (size_t)d * 32;                                     // cluster-sorted indices
+  uint8_t* pbuf = abuf + (size_t)d * 32;                                     // cluster-sorted indices
   int* obuf = reinterpret_cast<int*>(pbuf + (((size_t)d * 32 + 15) & ~(size_t)15));   // [16][32] offsets
   uint8_t* out_base = reinterpret_cast<uint8_t*>(obuf + KM_K * 32);
   const int ab = p.aux == EQ4_AUX_FP16 ? 2 : 4;
@@ -166,7 +164,6 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
     KMLane L;
     L.xs = xs + lane;
     L.a = abuf + lane;
-    L.ba = bbuf + lane;
     uint8_t* perm = pbuf + lane;
     int* offs = obuf + lane;
     double c[KM_K];
@@ -197,7 +194,7 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
       if (bad) {
 #pragma unroll
         for (int j = 0; j < KM_K; j++) c[j] = 0.0;
-        for (int k = 0; k < d; k++) L.ba[k * 32] = 0;
+        for (int k = 0; k < d; k++) L.a[k * 32] = 0;
       } else if (nu <= KM_K) {
 #pragma unroll
         for (int j = 0; j < KM_K; j++) c[j] = j < nu ? uq[j] : uq[nu - 1];
@@ -205,7 +202,7 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
           const double x = L.v(k);
           int pos = 0;
           while (uq[pos] < x) pos++;   // searchsorted(side='left')
-          L.ba[k * 32] = (uint8_t)pos;
+          L.a[k * 32] = (uint8_t)pos;
         }
       } else {
         const double scale = __ddiv_rn(__dsub_rn(hi, lo), 15.0);   // _uniform_grid
@@ -225,7 +222,6 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
             best_sse = sse;
 #pragma unroll
             for (int j = 0; j < KM_K; j++) bc[j] = c[j];
-            for (int k = 0; k < d; k++) L.ba[k * 32] = L.a[k * 32];
           }
           // stable counting sort of the element indices by cluster (O(d), instead of a
           // members scan per cluster), then each cluster's mean over its contiguous run
@@ -259,11 +255,12 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
 #pragma unroll
         for (int j = 0; j < KM_K; j++) cl[j] = c[j];
         const double sse = km_sse(L, cl, d);
-        if (sse < best_sse) {
-          for (int k = 0; k < d; k++) L.ba[k * 32] = L.a[k * 32];
-        } else {
+        if (!(sse < best_sse)) {
+          // the best scored assignment is argmin |v - c| under the best centers, a function of
+          // the centers alone: recompute it instead of keeping a copy per improvement
 #pragma unroll
           for (int j = 0; j < KM_K; j++) c[j] = bc[j];
+          km_assign(L, c, d, cnt);
         }
       }
     }
@@ -293,8 +290,8 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
       }
       uint8_t* nib = orow + KM_K * ab;
       for (int m = 0; m < p.half; m++) {
-        const int a0 = L.ba[(2 * m) * 32];
-        const int a1 = 2 * m + 1 < d ? L.ba[(2 * m + 1) * 32] : -1;
+        const int a0 = L.a[(2 * m) * 32];
+        const int a1 = 2 * m + 1 < d ? L.a[(2 * m + 1) * 32] : -1;
         unsigned c0 = 0, c1 = 0;
 #pragma unroll
         for (int j = 0; j < KM_K; j++) {
@@ -338,8 +335,8 @@ int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int
   p.half = (int)((dim + 1) / 2);
   p.stride = KM_K * (aux == EQ4_AUX_FP16 ? 2 : 4) + p.half;
   p.out = out; p.iters = iters; p.status = status;
-  // staged rows, assignments + best assignments, cluster-sorted indices, offsets, packed tile
-  size_t wb = (((size_t)dim * KM_COL * 4 + 15) & ~(size_t)15) + (size_t)dim * 32 * 2 +
+  // staged rows, assignments, cluster-sorted indices, offsets, packed tile
+  size_t wb = (((size_t)dim * KM_COL * 4 + 15) & ~(size_t)15) + (size_t)dim * 32 +
               (((size_t)dim * 32 + 15) & ~(size_t)15) + (size_t)KM_K * 32 * 4 + (size_t)32 * p.stride + 32;
   p.warp_bytes = (wb + 15) & ~(size_t)15;
   int dev = 0, sms = 0, per_sm = 0, max_optin = 0;
