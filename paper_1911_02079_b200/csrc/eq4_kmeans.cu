@@ -119,11 +119,13 @@ __device__ __forceinline__ double km_sse(const KMLane& L, const double* cl, int 
   return __dadd_rn(0.0, __dadd_rn(km_sse_leaf(L, cl, 0, n2), km_sse_leaf(L, cl, n2, d - n2)));
 }
 
-// argmin_j |v - c_j| (first minimum), assignments to L.a, per-cluster counts
+// argmin_j |v - c_j| (first minimum), assignments to L.a, per-cluster counts (counted in
+// the lane's shared-memory column hist[j * 32], then read back: one increment per
+// element instead of a 16-way compare-and-add)
 __device__ __forceinline__ void km_assign(const KMLane& L, const double (&c)[KM_K], int d,
-                                          int (&cnt)[KM_K]) {
+                                          int (&cnt)[KM_K], int* hist) {
 #pragma unroll
-  for (int j = 0; j < KM_K; j++) cnt[j] = 0;
+  for (int j = 0; j < KM_K; j++) hist[j * 32] = 0;
   for (int k = 0; k < d; k++) {
     const double x = L.v(k);
     double best = fabs(__dsub_rn(x, c[0]));
@@ -134,9 +136,10 @@ __device__ __forceinline__ void km_assign(const KMLane& L, const double (&c)[KM_
       if (t < best) { best = t; bj = j; }
     }
     L.a[k * 32] = (uint8_t)bj;
-#pragma unroll
-    for (int j = 0; j < KM_K; j++) cnt[j] += (bj == j);
+    hist[bj * 32] += 1;
   }
+#pragma unroll
+  for (int j = 0; j < KM_K; j++) cnt[j] = hist[j * 32];
 }
 
 __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
         int cnt[KM_K];
         int it = 0;
         for (it = 0; it < 100; it++) {
-          km_assign(L, c, d, cnt);
+          km_assign(L, c, d, cnt, offs);
 #pragma unroll
           for (int j = 0; j < KM_K; j++) cl[j] = c[j];
           const double sse = km_sse(L, cl, d);
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
           if (movement < stop) break;
         }
         iters = it < 100 ? it + 1 : 100;
-        km_assign(L, c, d, cnt);   // score the final center update
+        km_assign(L, c, d, cnt, offs);   // score the final center update
 #pragma unroll
         for (int j = 0; j < KM_K; j++) cl[j] = c[j];
         const double sse = km_sse(L, cl, d);
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
           // the centers alone: recompute it instead of keeping a copy per improvement
 #pragma unroll
           for (int j = 0; j < KM_K; j++) c[j] = bc[j];
-          km_assign(L, c, d, cnt);
+          km_assign(L, c, d, cnt, offs);
         }
       }
     }
