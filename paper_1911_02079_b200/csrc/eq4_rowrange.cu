@@ -134,8 +134,26 @@ __device__ __forceinline__ double lane_quant_mse(const RowView& xr, int d, doubl
       return __dmul_rn(e, e);
     }, d);
   }
-  // codes: fp32 estimate, float64 codec within NEAR of a rounding boundary (exact either way)
   const CodeParams cp = make_code_params(lo, hi);
+  if (!cp.slow) {
+    // branch-free fp32 codes (as the emit below: saturating scale, round-down add) with the
+    // distance to a rounding boundary tracked; if any element came within NEAR of one, the
+    // loss is recomputed with the exact codec (rare)
+    const float inv1 = cp.inv * (1.f / 15.f);
+    float gmax = 0.f;
+    const double v = np_sum([&](int k) {
+      const float xf = xr[k];
+      const float sv = __saturatef(__fmul_rn(__fadd_rn(__fadd_rn(xf, -cp.lo_hi), -cp.lo_lo), inv1));
+      const float m = __fadd_rd(__fmaf_rn(sv, 15.f, 0.5f), MAGIC_F);
+      gmax = fmaxf(gmax, fabsf(__fmaf_rn(sv, 15.f, -__fadd_rn(m, -MAGIC_F))));
+      const double c = (double)(__float_as_uint(m) & 0xFu);
+      const double recon = __dadd_rn(__dmul_rn(cp.scale, c), lo);
+      const double e = __dsub_rn((double)xf, recon);
+      return __dmul_rn(e, e);
+    }, d);
+    if (!(gmax > 0.5f - NEAR)) return v;
+  }
+  // codes: fp32 estimate, float64 codec within NEAR of a rounding boundary (exact either way)
   return np_sum([&](int k) {
     const float xf = xr[k];
     bool ne;
