@@ -42,6 +42,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "../../include/eq4.h"
@@ -1705,6 +1706,78 @@ static float tau2_for(int d, bool vec) {
   return (float)(2.0 * 1.05 * h * 5.9604645e-8);
 }
 
+// Streams, chunk buffers and the pinned status words of the host pipeline are kept
+// per device and reused by later calls (grow-only): creating / freeing them per call
+// (stream create/destroy, cudaMallocHost/cudaFreeHost, pool allocations released at
+// every synchronisation) cost 0.1-0.5 s on some calls.  Calls on one device are
+// serialised by the context's mutex.
+namespace {
+constexpr int HP_NS = 3;   // chunk c's H2D overlaps chunk c-1's kernel and chunk c-2's D2H
+struct HostBuf {
+  float* x = nullptr; uint8_t* out = nullptr; double* lo = nullptr; double* hi = nullptr;
+  int32_t* i0 = nullptr; int32_t* i1 = nullptr; int32_t* status = nullptr;
+};
+struct HostPipe {
+  std::mutex mu;
+  bool init = false;
+  cudaStream_t st[HP_NS] = {};
+  HostBuf bf[HP_NS];
+  size_t x_bytes = 0, out_bytes = 0, i0_rows = 0, i1_rows = 0, lohi_rows = 0;   // capacities
+  int32_t* hstatus = nullptr;
+  int64_t hstatus_n = 0;
+};
+HostPipe g_pipes[64];
+
+template <class T>
+cudaError_t grow(T** p, size_t have, size_t want) {
+  if (*p && have >= want) return cudaSuccess;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  return cudaMalloc((void**)p, want);
+}
+
+// capacity for chunks of `chunk` rows (grow-only); returns a cudaError_t
+cudaError_t pipe_reserve(HostPipe& hp, int64_t chunk, int64_t dim, int64_t stride, bool want_i1,
+                         bool want_lohi, int64_t nchunks) {
+  cudaError_t e = cudaSuccess;
+  if (!hp.init) {
+    for (int i = 0; i < HP_NS && e == cudaSuccess; i++)
+      e = cudaStreamCreateWithFlags(&hp.st[i], cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+    hp.init = true;
+  }
+  const size_t xb = (size_t)chunk * dim * 4, ob = (size_t)chunk * stride, rows = (size_t)chunk;
+  for (int i = 0; i < HP_NS && e == cudaSuccess; i++) {
+    HostBuf& B = hp.bf[i];
+    e = grow(&B.x, hp.x_bytes, xb);
+    if (e == cudaSuccess) e = grow(&B.out, hp.out_bytes, ob);
+    if (e == cudaSuccess) e = grow(&B.i0, hp.i0_rows * 4, rows * 4);
+    if (e == cudaSuccess && !B.status) e = cudaMalloc((void**)&B.status, 4);
+    if (e == cudaSuccess && want_i1) e = grow(&B.i1, hp.i1_rows * 4, rows * 4);
+    if (e == cudaSuccess && want_lohi) e = grow(&B.lo, hp.lohi_rows * 8, rows * 8);
+    if (e == cudaSuccess && want_lohi) e = grow(&B.hi, hp.lohi_rows * 8, rows * 8);
+  }
+  if (e != cudaSuccess) {   // partially grown: forget every capacity, the next call reallocates
+    hp.x_bytes = hp.out_bytes = hp.i0_rows = hp.i1_rows = hp.lohi_rows = 0;
+    return e;
+  }
+  hp.x_bytes = std::max(hp.x_bytes, xb);
+  hp.out_bytes = std::max(hp.out_bytes, ob);
+  hp.i0_rows = std::max(hp.i0_rows, rows);
+  if (want_i1) hp.i1_rows = std::max(hp.i1_rows, rows);
+  if (want_lohi) hp.lohi_rows = std::max(hp.lohi_rows, rows);
+  if (hp.hstatus_n < nchunks) {
+    if (hp.hstatus) cudaFreeHost(hp.hstatus);
+    hp.hstatus = nullptr;
+    hp.hstatus_n = 0;
+    e = cudaMallocHost((void**)&hp.hstatus, sizeof(int32_t) * nchunks);
+    if (e != cudaSuccess) return e;
+    hp.hstatus_n = nchunks;
+  }
+  return cudaSuccess;
+}
+}  // namespace
+
 extern "C" {
 
 const char* eq4_version(void) { return "eq4 0.1.0 (sm_100a)"; }
@@ -1942,6 +2015,7 @@ static cudaError_t h2d_rows(float* dst, const float* src, int64_t nr, int64_t di
   return cudaMemcpy2DAsync(dst, dim * 4, src, ld * 4, dim * 4, nr, cudaMemcpyHostToDevice, s);
 }
 
+
 int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld, int method,
                            int b, double r, int aux, uint8_t* packed, double* xmin, double* xmax,
                            int32_t* info0, int32_t* info1, double* norm, int64_t chunk_rows,
@@ -1953,27 +2027,19 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
   int64_t chunk = chunk_rows > 0 ? chunk_rows : std::max<int64_t>(1024, (16ll << 20) / (dim * 4));
   chunk = std::min(chunk, rows);
   const int64_t nchunks = (rows + chunk - 1) / chunk;
-  const int NS = 3;   // chunk c's H2D overlaps chunk c-1's kernel and chunk c-2's D2H
-  cudaStream_t st[NS];
-  for (int i = 0; i < NS; i++) cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking);
-  struct Buf { float* x; uint8_t* out; double* lo; double* hi; int32_t* i0; int32_t* i1; int32_t* status; };
-  Buf bf[NS];
-  memset(bf, 0, sizeof(bf));
-  int32_t* hstatus = nullptr;
-  int rc = EQ4_OK;
-  cudaError_t e = cudaMallocHost(&hstatus, sizeof(int32_t) * nchunks);
-  if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocHost");
+  const int NS = HP_NS;
   const bool want_lohi = xmin != nullptr;
-  for (int i = 0; i < NS && rc == EQ4_OK; i++) {
-    e = cudaMallocAsync(&bf[i].x, chunk * dim * 4, st[i]);
-    if (e == cudaSuccess) e = cudaMallocAsync(&bf[i].out, chunk * stride, st[i]);
-    if (e == cudaSuccess) e = cudaMallocAsync(&bf[i].i0, chunk * 4, st[i]);
-    if (e == cudaSuccess) e = cudaMallocAsync(&bf[i].status, 4, st[i]);
-    if (e == cudaSuccess && info1) e = cudaMallocAsync(&bf[i].i1, chunk * 4, st[i]);
-    if (e == cudaSuccess && want_lohi) e = cudaMallocAsync(&bf[i].lo, chunk * 8, st[i]);
-    if (e == cudaSuccess && want_lohi) e = cudaMallocAsync(&bf[i].hi, chunk * 8, st[i]);
-    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocAsync");
-  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return fail(EQ4_EUNSUPPORTED, "device index out of range");
+  HostPipe& hp = g_pipes[dev];
+  std::lock_guard<std::mutex> lk(hp.mu);
+  int rc = EQ4_OK;
+  cudaError_t e = pipe_reserve(hp, chunk, dim, stride, info1 != nullptr, want_lohi, nchunks);
+  if (e != cudaSuccess) return cuda_fail(e, "host pipeline buffers");
+  cudaStream_t* st = hp.st;
+  HostBuf* bf = hp.bf;
+  int32_t* hstatus = hp.hstatus;
   // TABLE: one range over the whole table -> a first streaming pass for the min / max keys
   int* tkeys = nullptr;
   if (rc == EQ4_OK && method == EQ4_METHOD_TABLE) {
@@ -1996,13 +2062,14 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
   for (int64_t c = 0; c < nchunks && rc == EQ4_OK; c++) {
     const int si = (int)(c % NS);
     cudaStream_t s = st[si];
-    Buf& B = bf[si];
+    HostBuf& B = bf[si];
     const int64_t r0 = c * chunk, nr = std::min(chunk, rows - r0);
     e = h2d_rows(B.x, x + r0 * ld, nr, dim, ld, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(B.status, 0, 4, s);
     if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
-    rc = quantize_pack_impl(B.x, nr, dim, dim, method, b, r, aux, B.out, B.lo, B.hi, B.i0, B.i1,
-                            nullptr, B.status, s, tkeys);
+    rc = quantize_pack_impl(B.x, nr, dim, dim, method, b, r, aux, B.out, want_lohi ? B.lo : nullptr,
+                            want_lohi ? B.hi : nullptr, B.i0, info1 ? B.i1 : nullptr, nullptr, B.status, s,
+                            tkeys);
     if (rc) break;
     e = cudaMemcpyAsync(packed + r0 * stride, B.out, nr * stride, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && info0) e = cudaMemcpyAsync(info0 + r0, B.i0, nr * 4, cudaMemcpyDeviceToHost, s);
@@ -2029,7 +2096,7 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
       double elo = 0, ehi = 0;
       if (hstatus[c] & EQ4_STATUS_RANGE) {
         // re-run this chunk with per-row outputs to locate the row
-        Buf& B = bf[0];
+        HostBuf& B = bf[0];
         double *dlo = nullptr, *dhi = nullptr;
         cudaMallocAsync(&dlo, nr * 8, st[0]);
         cudaMallocAsync(&dhi, nr * 8, st[0]);
@@ -2065,15 +2132,7 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
     }
   }
   if (tkeys) cudaFreeAsync(tkeys, st[0]);
-  for (int i = 0; i < NS; i++) {
-    cudaFreeAsync(bf[i].x, st[i]); cudaFreeAsync(bf[i].out, st[i]); cudaFreeAsync(bf[i].i0, st[i]);
-    cudaFreeAsync(bf[i].status, st[i]);
-    if (bf[i].i1) cudaFreeAsync(bf[i].i1, st[i]);
-    if (bf[i].lo) { cudaFreeAsync(bf[i].lo, st[i]); cudaFreeAsync(bf[i].hi, st[i]); }
-    cudaStreamSynchronize(st[i]);
-    cudaStreamDestroy(st[i]);
-  }
-  if (hstatus) cudaFreeHost(hstatus);
+  for (int i = 0; i < NS; i++) cudaStreamSynchronize(st[i]);
   return rc;
 }
 
