@@ -132,6 +132,34 @@ static __device__ __noinline__ double np_combine(int n, const double* leaf_sum, 
 // accumulator chains, a 3-level butterfly forms ((r0+r1)+(r2+r3))+(...),
 // lane 0 adds the leaf's remainder, and lane 0 combines leaf sums in the
 // recursion's association order.
+// Branch-free fp32 code of x under the float64 range [lo, hi] (saturating scale, round-down
+// add of 2^23): numpy's code (uniform.py:77-79) unless x lies within NEAR = 1e-5 of a
+// rounding boundary, which sets `near` (callers then redo the pass with the float64 codec).
+struct FastCodec {
+  float lo_hi, lo_lo, inv1;
+  bool slow;   // range too extreme for the estimate: always take the float64 codec
+};
+__device__ __forceinline__ FastCodec fast_codec(double lo, double hi) {
+  FastCodec f;
+  f.lo_hi = __double2float_rn(lo);
+  f.lo_lo = __double2float_rn(__dsub_rn(lo, (double)f.lo_hi));
+  const double w = __dsub_rn(hi, lo);
+  f.slow = hi != lo && !(w > 1e-30 && w < 1e30 && fabs(lo) < 1e30 && fabs(hi) < 1e30);
+  f.inv1 = (hi == lo) ? 0.f : __fdividef(1.f, __double2float_rn(w));
+  return f;
+}
+__device__ __forceinline__ double fast_code(float xf, const FastCodec& f, bool& near) {
+  const float sv = __saturatef(__fmul_rn(__fadd_rn(__fadd_rn(xf, -f.lo_hi), -f.lo_lo), f.inv1));
+  const float mm = __fadd_rd(__fmaf_rn(sv, 15.f, 0.5f), 8388608.f);
+  near |= fabsf(__fmaf_rn(sv, 15.f, -__fadd_rn(mm, -8388608.f))) > 0.5f - 1e-5f;
+  return (double)(__float_as_uint(mm) & 0xFu);
+}
+// (x - (scale * code + lo))^2 with the reference's float64 operations
+__device__ __forceinline__ double np_err2_code(double x, double code, const NpCodec& c) {
+  const double e = __dsub_rn(x, __dadd_rn(__dmul_rn(c.scale, code), c.lo));
+  return __dmul_rn(e, e);
+}
+
 static __device__ __noinline__ double warp_np_loss(const float* xs, int d, double lo, double hi,
                                             double* e2, double* leaf_sum, int* leaf_start,
                                             int* leaf_len, int max_leaves) {
@@ -144,6 +172,7 @@ static __device__ __noinline__ double warp_np_loss(const float* xs, int d, doubl
     res = __shfl_sync(FULL, res, 0);
     return __dadd_rn(0.0, res);
   }
+  const FastCodec fc = fast_codec(lo, hi);
   int nl = 0;
   if (lane == 0) nl = np_leaves(d, leaf_start, leaf_len, max_leaves);
   nl = __shfl_sync(FULL, nl, 0);
@@ -152,7 +181,15 @@ static __device__ __noinline__ double warp_np_loss(const float* xs, int d, doubl
   for (int base = 0; base < nl; base += 4) {
     const int last = min(base + 4, nl) - 1;
     const int r0 = leaf_start[base], r1 = leaf_start[last] + leaf_len[last];
-    for (int k = lane; k < r1 - r0; k += 32) e2[k] = np_err2_fast((double)xs[r0 + k], cd);
+    {
+      bool near = fc.slow;
+      for (int k = lane; k < r1 - r0; k += 32) {
+        const float xf = xs[r0 + k];
+        e2[k] = np_err2_code((double)xf, fast_code(xf, fc, near), cd);
+      }
+      if (__any_sync(FULL, near))   // an element near a rounding boundary: the float64 codec
+        for (int k = lane; k < r1 - r0; k += 32) e2[k] = np_err2_fast((double)xs[r0 + k], cd);
+    }
     __syncwarp();
     const int li = base + g;
     const bool ok = li < nl;
@@ -202,9 +239,27 @@ __device__ __forceinline__ void warp_np_loss3_leaf(const float* xs, int d, int n
   const int nfull = d - (d % 8);
   const int nch = nfull >> 3;   // chain length <= 16
   double r = 0.0;
-  if (act) {
-    r = np_err2_fast((double)xs[m], cd);
-    for (int u = 1; u < nch; u++) r = __dadd_rn(r, np_err2_fast((double)xs[m + 8 * u], cd));
+  // codes from the branch-free fp32 estimate (saturating scale, round-down add); they are
+  // numpy's unless an element lies within NEAR of a rounding boundary, in which case the
+  // whole pass is redone with the float64 codec.  The errors and sums are the reference's
+  // float64 operations either way.
+  {
+    const FastCodec fc = fast_codec(lo, hi);
+    bool flag = act && fc.slow;
+    if (act) {
+      for (int u = 0; u < nch; u++) {
+        const float xf = xs[m + 8 * u];
+        const double e2v = np_err2_code((double)xf, fast_code(xf, fc, flag), cd);
+        r = u == 0 ? e2v : __dadd_rn(r, e2v);
+      }
+    }
+    if (__any_sync(FULL, flag)) {
+      r = 0.0;
+      if (act) {
+        r = np_err2_fast((double)xs[m], cd);
+        for (int u = 1; u < nch; u++) r = __dadd_rn(r, np_err2_fast((double)xs[m + 8 * u], cd));
+      }
+    }
   }
   r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 1));
   r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 2));
