@@ -132,6 +132,14 @@ static __device__ __noinline__ double np_combine(int n, const double* leaf_sum, 
 // accumulator chains, a 3-level butterfly forms ((r0+r1)+(r2+r3))+(...),
 // lane 0 adds the leaf's remainder, and lane 0 combines leaf sums in the
 // recursion's association order.
+// The fp32 code estimates (code_of, fast_code) of x under (lo, hi): the argument
+// t' = (x - lo) * 15/(hi-lo) + 0.5 has absolute error < 7e-6 for interior x
+// (|t'| < 16, a few roundings of relative 2^-24 each on the range-scaled
+// quantities); when frac(t') is within NEAR of an integer the float64 codec
+// decides.  x <= lo gives code 0 and x >= hi code 15 exactly in the
+// reference (clip then floor(0 + .5) / floor(15 +- 1ulp + .5)).
+constexpr float NEAR = 1e-5f;
+
 // Branch-free fp32 code of x under the float64 range [lo, hi] (saturating scale, round-down
 // add of 2^23): numpy's code (uniform.py:77-79) unless x lies within NEAR = 1e-5 of a
 // rounding boundary, which sets `near` (callers then redo the pass with the float64 codec).
@@ -151,7 +159,7 @@ __device__ __forceinline__ FastCodec fast_codec(double lo, double hi) {
 __device__ __forceinline__ double fast_code(float xf, const FastCodec& f, bool& near) {
   const float sv = __saturatef(__fmul_rn(__fadd_rn(__fadd_rn(xf, -f.lo_hi), -f.lo_lo), f.inv1));
   const float mm = __fadd_rd(__fmaf_rn(sv, 15.f, 0.5f), 8388608.f);
-  near |= fabsf(__fmaf_rn(sv, 15.f, -__fadd_rn(mm, -8388608.f))) > 0.5f - 1e-5f;
+  near |= fabsf(__fmaf_rn(sv, 15.f, -__fadd_rn(mm, -8388608.f))) > 0.5f - NEAR;
   return (double)(__float_as_uint(mm) & 0xFu);
 }
 // (x - (scale * code + lo))^2 with the reference's float64 operations
@@ -309,14 +317,8 @@ __device__ __forceinline__ CodeParams make_code_params(double lo, double hi) {
   return p;
 }
 
-// Code of x under (lo, hi): exact numpy semantics.  The fp32 estimate
-// t' = (x - lo) * 15/(hi-lo) + 0.5 has absolute error < 4e-6 for interior x
-// (|t'| < 16, three roundings of relative 2^-24 each on the range-scaled
-// quantities); when frac(t') is within NEAR of an integer the float64 codec
-// decides.  x <= lo gives code 0 and x >= hi code 15 exactly in the
-// reference (clip then floor(0 + .5) / floor(15 +- 1ulp + .5)).
-constexpr float NEAR = 1e-5f;
 
+// Code of x under (lo, hi), numpy semantics (NEAR above).
 __device__ __forceinline__ unsigned code_of(float x, const CodeParams& p, bool& need_exact) {
   // branch-free: every element runs the same instruction stream
   const float dlt = __fadd_rn(__fadd_rn(x, -p.lo_hi), -p.lo_lo);
