@@ -204,8 +204,15 @@ __device__ __forceinline__ void hist_apprx_walk(const double* Us, const double* 
       if ((unsigned)kL < (unsigned)nn) aL = fma(c, Un[kL], aL);
       if ((unsigned)kR < (unsigned)nn) aR = fma(c, Un[kR], aR);
     }
-    const double FL = __fma_rn(__dadd_rn(A3[st + 1], R3[en]), 1.0 / 3.0, warp_sum_d(aL));
-    const double FR = __fma_rn(__dadd_rn(A3[st], R3[en - 1]), 1.0 / 3.0, warp_sum_d(aR));
+    // both sums with one transposing butterfly: the first level trades halves (lanes < 16
+    // keep L, the others R), four more levels finish each sum within its half
+    const bool upper = lane >= 16;
+    double keep = upper ? aR : aL;
+    keep = __dadd_rn(keep, __shfl_xor_sync(FULL, upper ? aL : aR, 16));
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) keep = __dadd_rn(keep, __shfl_xor_sync(FULL, keep, o));
+    const double FL = __fma_rn(__dadd_rn(A3[st + 1], R3[en]), 1.0 / 3.0, __shfl_sync(FULL, keep, 0));
+    const double FR = __fma_rn(__dadd_rn(A3[st], R3[en - 1]), 1.0 / 3.0, __shfl_sync(FULL, keep, 16));
     bool goL, have_cur = false;
     double curN = 0.0;
     if (fabs(FL - FR) > APPRX_TOL * fmax(FL, FR)) {
