@@ -141,6 +141,29 @@ def test_host_path_equals_device_path(eq):
     assert np.array_equal(rr.xmin[:5000], want.xmin)
 
 
+def test_host_pipeline_reuse_across_shapes(eq):
+    """The host pipeline keeps its streams and chunk buffers between calls (grow-only): a
+    sequence of shapes, methods and optional outputs, each equal to the device path, with a
+    data error in the middle (the reference's DataError text) and identical reruns after it."""
+    seq = [(70_001, 64, "greedy", "fp16", True), (3_000, 256, "asym", "fp32", False),
+           (200_000, 16, "greedy", "fp16", False), (5_000, 2048, "greedy", "fp32", True),
+           (70_001, 64, "hist-brute", "fp16", True), (1_000, 33, "table", "fp16", False),
+           (70_001, 64, "greedy", "fp16", True)]
+    for i, (rows, d, method, aux, rows_out) in enumerate(seq):
+        x = rng.mixed_table(rows, d, 40 + i)
+        dev, rd = eq.quantize_pack_table4(_dev(x), method, aux, with_rows=True)
+        host, rh = eq.quantize_pack_table4(x, method, aux, with_rows=rows_out)
+        assert np.array_equal(dev.buffer, host.buffer), (method, d)
+        if rows_out:
+            assert np.array_equal(rd.xmin.cpu().numpy(), rh.xmin), (method, d)
+            assert np.array_equal(rd.info0.cpu().numpy(), rh.info0), (method, d)
+        if i == 3:
+            bad = x.copy()
+            bad[4321 % rows, 3] = np.nan
+            with pytest.raises(ValueError, match="non-finite"):
+                eq.quantize_pack_table4(bad, method, aux)
+
+
 def test_public_api_drop_in(eq):
     x = rng.sample_table("gaussian", 0.0, 1.0, 12, 300, 64)
     t = eq.EmbeddingTable(x)
