@@ -98,7 +98,12 @@ int eq4_quantize_pack(const float *x, int64_t rows, int64_t dim, int64_t ld, int
  * first failing row in *bad_row and, for EQ4_ERANGE, the offending
  * (xmin, xmax) pair in bad_lohi[0..1] (both optional).  xmin/xmax/info0/
  * info1/norm are optional host arrays of length rows.  chunk_rows = 0 picks
- * a default (~64 MiB of input per chunk).
+ * a default (16 MiB of input per chunk).  The internal streams, device chunk
+ * buffers and pinned status words are created on the first call per device
+ * and reused (grown as needed) by later calls, which are serialised per
+ * device; they stay allocated for the life of the process (do not call
+ * cudaDeviceReset while the library is in use).  Pinned (page-locked) host
+ * buffers give full PCIe bandwidth; pageable ones are staged by the driver.
  */
 int eq4_quantize_pack_host(const float *x, int64_t rows, int64_t dim, int64_t ld, int method,
                            int b, double r, int aux, uint8_t *packed, double *xmin, double *xmax,
