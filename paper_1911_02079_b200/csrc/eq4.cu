@@ -453,11 +453,15 @@ __global__ void __launch_bounds__(256) k_table_minmax(const float* x, int64_t ro
       }
     }
   }
-  for (int o = 16; o >= 1; o >>= 1) {
-    kmin = min(kmin, __shfl_xor_sync(FULL, kmin, o));
-    kmax = max(kmax, __shfl_xor_sync(FULL, kmax, o));
-  }
-  if (lane == 0) {
+  kmin = __reduce_min_sync(FULL, kmin);
+  kmax = __reduce_max_sync(FULL, kmax);
+  // one pair of atomics per block (not per warp): the two global words are every block's target
+  __shared__ int bmin[8], bmax[8];
+  const int warp = threadIdx.x >> 5;
+  if (lane == 0) { bmin[warp] = kmin; bmax[warp] = kmax; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++) { kmin = min(kmin, bmin[w]); kmax = max(kmax, bmax[w]); }
     atomicMin(keys, kmin);
     atomicMax(keys + 1, kmax);
   }
