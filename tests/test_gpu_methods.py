@@ -78,6 +78,38 @@ def test_aciq_leaf_shapes_vs_oracle(d):
     assert np.array_equal(p2.buffer, oracle.quantize_pack_table(x, "aciq", 200, 0.16, "fp16").packed)
 
 
+@pytest.mark.parametrize("method", ["gss", "aciq", "sym", "table", "hist-apprx"])
+@pytest.mark.parametrize("d", [16, 64, 33])
+def test_methods_grid_valued_rows_vs_oracle(method, d):
+    """Few distinct values per row (integers, dyadic grids, repeated centres): many elements
+    on or next to code boundaries, exercising the fp32 code estimates' exact fallbacks."""
+    g = np.random.default_rng(d)
+    x = np.empty((3000, d), np.float32)
+    for i in range(3000):
+        k = i % 3
+        if k == 0:
+            x[i] = g.integers(0, g.integers(2, 33), d)
+        elif k == 1:
+            x[i] = g.integers(-32, 32, d) * np.float32(2.0 ** -int(g.integers(0, 6)))
+        else:
+            c = g.normal(size=int(g.integers(3, 9))).astype(np.float32)
+            x[i] = c[g.integers(0, c.size, d)]
+    b = 64 if method == "hist-apprx" else 200
+    want = oracle.quantize_pack_table(x, method, b, 0.16, "fp16")
+    p, rr = eq.quantize_pack_table4(torch.from_numpy(x).cuda(), method, "fp16", b, with_rows=True)
+    if method == "hist-apprx":   # windows may differ only at reference norm ties (see test_gpu_hist_apprx)
+        same = (rr.info0.cpu().numpy() == want.info0) & (rr.info1.cpu().numpy() == want.info1)
+        stride = eq.packed_row_stride(d, "fp16")
+        assert np.array_equal(p.buffer.reshape(-1, stride)[same], want.packed.reshape(-1, stride)[same])
+        assert same.mean() > 0.99
+        return
+    assert np.array_equal(p.buffer, want.packed)
+    assert np.array_equal(rr.xmin.cpu().numpy(), want.xmin)
+    assert np.array_equal(rr.xmax.cpu().numpy(), want.xmax)
+    if method == "gss":
+        assert np.array_equal(rr.info0.cpu().numpy(), want.info0)
+
+
 def test_method_api_single_rows_and_counters():
     x = rng.sample_table("laplacian", 0.0, 1.0, 7, 5, 64)
     for row in x:
