@@ -270,11 +270,12 @@ def test_hist_brute_vs_oracle_shapes(eq, b, d, rows):
     x = rng.mixed_table(rows, d, 99 + b)
     x[3 % rows] = 2.5                       # constant row
     x[5 % rows, : max(1, d // 2)] = -1.0    # one bin holding half the row
-    want = oracle.quantize_pack_table(x, "hist-brute", b, aux="fp16")
-    p, rr = eq.quantize_pack_table4(_dev(x), "hist-brute", "fp16", b, with_rows=True)
+    aux = "fp32" if d % 2 else "fp16"
+    want = oracle.quantize_pack_table(x, "hist-brute", b, aux=aux)
+    p, rr = eq.quantize_pack_table4(_dev(x), "hist-brute", aux, b, with_rows=True)
     ties = _hist_compare(x, b, rr.info0.cpu().numpy(), rr.info1.cpu().numpy(), want.info0, want.info1)
     keep = np.setdiff1d(np.arange(rows), ties)
-    stride = eq.packed_row_stride(d, "fp16")
+    stride = eq.packed_row_stride(d, aux)
     assert np.array_equal(p.buffer.reshape(-1, stride)[keep], want.packed.reshape(-1, stride)[keep])
     assert np.array_equal(rr.xmin.cpu().numpy()[keep], want.xmin[keep])
     np.testing.assert_allclose(rr.norm.cpu().numpy(), want.norm, rtol=1e-9)
