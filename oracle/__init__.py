@@ -90,6 +90,8 @@ def lib():
         L.eqo_clip_range_aciq.argtypes = [vp, i64, vp, vp, vp]
         L.eqo_clip_range_gss.argtypes = [vp, i64, i32, vp, vp, vp, vp]
         L.eqo_sls4.argtypes = [vp, i64, i64, i32, vp, i64, vp, i64, vp, vp]
+        L.eqo_np_extremum.argtypes = [vp, i64, i32]
+        L.eqo_np_extremum.restype = dbl
         _lib = L
     return _lib
 
@@ -109,6 +111,13 @@ def max_threads() -> int:
 def np_sum(a) -> float:
     a = np.ascontiguousarray(a, dtype=np.float64)
     return float(lib().eqo_np_sum(_p(a), a.size))
+
+
+def np_extremum(x, is_max: bool) -> float:
+    """np.min / np.max of a float32 row promoted to float64, numpy's zero-sign choice
+    included (eq4_oracle.c np_reduce_ext)."""
+    x = _f32(x)
+    return float(lib().eqo_np_extremum(_p(x), x.size, int(bool(is_max))))
 
 
 def quant_mse(x, xmin: float, xmax: float, nbits: int = 4) -> float:

@@ -123,15 +123,56 @@ static int check_finite(const float *x, long d) {
     return EQO_OK;
 }
 
-static void row_minmax(const float *x, long d, double *lo, double *hi) {
-    float a = x[0], b = x[0];
-    for (long i = 1; i < d; i++) {
-        if (x[i] < a) a = x[i];
-        if (x[i] > b) b = x[i];
+/* np.min / np.max of the row promoted to float64 (clipping.py:46,61,163;
+ * histclip.py:57), in numpy's own reduction order: the value is the plain
+ * extremum, but WHICH of several equal extrema is returned decides the sign
+ * of a zero extremum (+0.0 == -0.0), and that sign reaches the packed bias.
+ * numpy 2.x (loops_minmax.dispatch.c.src, AVX-512 dispatch of the host that
+ * made tests/golden) reduces a contiguous float64 vector as:
+ *   r = x[0]; acc[0..7] = r; over x[1..]: 64-element blocks
+ *   acc = OP(acc, OP(OP(OP(v0,v1),OP(v2,v3)), OP(OP(v4,v5),OP(v6,v7)))),
+ *   then 8-element vectors acc = OP(acc, v); r = _mm512_reduce (OP(hi4,lo4),
+ *   OP(hi2,lo2), OP(v[0],v[1])); then r = OP(r, x[i]) over the scalar tail,
+ * with OP(a, b) = a < b ? a : b (max: a > b ? a : b) -- vminpd / vmaxpd
+ * return the second operand on equality.  Pinned against np.min/np.max by
+ * tests/golden/signed_zero.npz (made by the reference). */
+static double np_reduce_ext(const float *x, long d, int is_max) {
+#define NP_OP(a, b) (is_max ? ((a) > (b) ? (a) : (b)) : ((a) < (b) ? (a) : (b)))
+    double r = (double)x[0];
+    const float *ip = x + 1;
+    long n = d - 1;
+    if (n >= 8) {
+        double acc[8];
+        for (int k = 0; k < 8; k++) acc[k] = r;
+        for (; n >= 64; n -= 64, ip += 64) {
+            for (int k = 0; k < 8; k++) {
+                double v[8];
+                for (int j = 0; j < 8; j++) v[j] = (double)ip[8 * j + k];
+                double r01 = NP_OP(v[0], v[1]), r23 = NP_OP(v[2], v[3]);
+                double r45 = NP_OP(v[4], v[5]), r67 = NP_OP(v[6], v[7]);
+                double t = NP_OP(NP_OP(r01, r23), NP_OP(r45, r67));
+                acc[k] = NP_OP(acc[k], t);
+            }
+        }
+        for (; n >= 8; n -= 8, ip += 8)
+            for (int k = 0; k < 8; k++) acc[k] = NP_OP(acc[k], (double)ip[k]);
+        double t3[4], t6[2];
+        for (int k = 0; k < 4; k++) t3[k] = NP_OP(acc[k + 4], acc[k]);
+        for (int k = 0; k < 2; k++) t6[k] = NP_OP(t3[k + 2], t3[k]);
+        r = NP_OP(t6[0], t6[1]);
     }
-    *lo = (double)a;
-    *hi = (double)b;
+    for (; n > 0; n--, ip++) r = NP_OP(r, (double)*ip);
+    return r;
+#undef NP_OP
 }
+
+static void row_minmax(const float *x, long d, double *lo, double *hi) {
+    *lo = np_reduce_ext(x, d, 0);
+    *hi = np_reduce_ext(x, d, 1);
+}
+
+/* Test hook: np.min (is_max = 0) / np.max (1) of a float32 row promoted to float64. */
+double eqo_np_extremum(const float *x, long d, int is_max) { return np_reduce_ext(x, d, is_max); }
 
 /* clipping.py:58-61 clip_range_asym. */
 int eqo_clip_range_asym(const float *x, long d, double *lo, double *hi) {

@@ -60,7 +60,11 @@ class EmbeddingTable:
     """Dense N x d float32 table (table.py:12-60).
 
     Accepts anything numpy accepts (host) or a CUDA ``torch.Tensor`` (kept in
-    HBM; validated on the device).  Values must be finite.
+    HBM).  Values must be finite: a host table is checked here, as the
+    reference does (table.py:28-29); a device table is checked by the kernels
+    themselves while they read it (their status word), so the same ValueError
+    surfaces from the first quantize call without an extra pass over HBM or a
+    host synchronisation at construction.
     """
 
     __slots__ = ("_values", "_device")
@@ -72,9 +76,8 @@ class EmbeddingTable:
                 raise ValueError(f"expected a 2-D array, got shape {tuple(t.shape)}")
             if t.shape[0] < 1 or t.shape[1] < 1:
                 raise ValueError(f"table must be at least 1x1, got shape {tuple(t.shape)}")
-            t = t.to(torch.float32).contiguous()
-            if not bool(torch.isfinite(t).all()):
-                raise ValueError("table contains non-finite values (NaN/Inf)")
+            if t.dtype != torch.float32 or not t.is_contiguous():
+                t = t.to(torch.float32).contiguous()
             self._device = t
             self._values = None
             return
@@ -364,7 +367,10 @@ def quantize_pack_table4(table, method: str, aux_precision: str = "fp16", b: int
     ``table``: EmbeddingTable, CUDA float32 tensor (device path, stream
     ordered) or host array (pipelined host path).  Returns
     ``(PackedTable4, RowResults | None)``.  With ``check=False`` on the device
-    path nothing synchronises; the caller inspects ``status`` itself.
+    path nothing synchronises; the caller inspects ``status`` itself (the C
+    entry point clears it on the stream first).  ``stream`` (a torch CUDA
+    stream, default the current one) orders the launch; the output buffers
+    are allocated on it and the status read waits for it.
     """
     if method not in GPU_METHODS:
         raise ValueError(f"{method!r} is not on the B200 hot path; supported: {GPU_METHODS}")
@@ -376,6 +382,10 @@ def quantize_pack_table4(table, method: str, aux_precision: str = "fp16", b: int
     else:
         src = table
     if _is_cuda(src):
+        if stream is not None and stream != torch.cuda.current_stream(src.device):
+            with torch.cuda.stream(stream):
+                return quantize_pack_table4(src, method, aux_precision, b, r, out=out, rows_out=rows_out,
+                                            with_rows=with_rows, status=status, stream=None, check=check)
         x = src if (src.dtype == torch.float32 and src.stride(1) == 1) else src.float().contiguous()
         rows, d = int(x.shape[0]), int(x.shape[1])
         ld = int(x.stride(0))
@@ -391,9 +401,7 @@ def quantize_pack_table4(table, method: str, aux_precision: str = "fp16", b: int
                             torch.empty(rows, dtype=torch.int32, device=dev),
                             torch.empty(rows, dtype=torch.float64, device=dev))
         if status is None:
-            status = torch.zeros(1, dtype=torch.int32, device=dev)
-        else:
-            status.zero_()
+            status = torch.empty(1, dtype=torch.int32, device=dev)   # cleared by eq4_quantize_pack
         rc = L.eq4_quantize_pack(_vp(x), rows, d, ld, _lib.METHOD[method], int(b), float(r),
                                  _lib.AUX[aux_precision], _vp(out),
                                  _vp(rr.xmin) if rr else None, _vp(rr.xmax) if rr else None,

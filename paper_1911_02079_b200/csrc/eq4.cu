@@ -134,6 +134,12 @@ __device__ __forceinline__ float group_sum(float v) {
   return v;
 }
 template <int LPR>
+__device__ __forceinline__ unsigned group_umax(unsigned v) {
+#pragma unroll
+  for (int o = LPR / 2; o >= 1; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+template <int LPR>
 __device__ __forceinline__ bool group_any(bool v) {
   unsigned bal = __ballot_sync(FULL, v);
   if (LPR == 32) return bal != 0;
@@ -227,6 +233,13 @@ __device__ __forceinline__ void row_minmax(const Params& p, const float (&v)[E],
   mn = group_min<LPR>(mn);
   mx = group_max<LPR>(mx);
   sm = group_sum<LPR>(sm);
+  if (__any_sync(FULL, rvalid && (mn == 0.f || mx == 0.f))) {   // rare: numpy's signed-zero choice
+    unsigned kz = 0u;
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      if (VEC || i < nv) kz = max(kz, np_zero_key(v[i], VEC ? 4 * (q + LPR * (i >> 2)) + (i & 3) : q + LPR * i, p.d));
+    np_zero_apply(group_umax<LPR>(kz), mn, mx);
+  }
   bad = false;
   if (__any_sync(FULL, !isfinite(sm) && rvalid)) {
     bool lb = false;
@@ -1042,6 +1055,16 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         mn = group_min<LPR>(lmn);
         mx = group_max<LPR>(lmx);
         sm = group_sum<LPR>(sm);
+        if (__any_sync(FULL, rvalid && (mn == 0.f || mx == 0.f))) {   // rare: numpy's signed-zero choice
+          unsigned kz = 0u;
+          for (int c = 0; c < E / 4; ++c) {
+            const float4 t = __ldg(src + LPR * c);
+            const int p0 = 4 * (q + LPR * c);
+            kz = max(max(max(kz, np_zero_key(t.x, p0, d)), np_zero_key(t.y, p0 + 1, d)),
+                     max(np_zero_key(t.z, p0 + 2, d), np_zero_key(t.w, p0 + 3, d)));
+          }
+          np_zero_apply(group_umax<LPR>(kz), mn, mx);
+        }
         bad = false;
         if (__any_sync(FULL, !isfinite(sm) && rvalid)) {   // NaN/Inf (or a false alarm on overflow)
           bool lb = false;
@@ -1209,7 +1232,9 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       lo = R.elo; hi = R.ehi; info0 = -2;
       if (q == 0 && p.status) atomicOr(p.status, EQ4_STATUS_RANGE);
     } else {
-      lo = bi == 0 ? R.x0 : __dadd_rn(R.x0, __dmul_rn((double)bi, R.step));
+      // clipping.py:175,182: the start pair is (x0, x1) itself; any recorded
+      // candidate's xmin is x0 + nl*step, which is +0.0 for nl = 0 and x0 = -0.0
+      lo = (bi == 0 && bj == 0) ? R.x0 : __dadd_rn(R.x0, __dmul_rn((double)bi, R.step));
       hi = bj == 0 ? R.x1 : __dsub_rn(R.x1, __dmul_rn((double)bj, R.step));
       if (rvalid && !bad && mn != mx) { info0 = iters; info1 = (bi << 16) | bj; }
     }
@@ -1277,6 +1302,16 @@ __device__ __forceinline__ void asym_row(const Params& p, const float4 (&cur)[E 
   mn = group_min<LPR>(mn);
   mx = group_max<LPR>(mx);
   sm = group_sum<LPR>(sm);
+  if (__any_sync(FULL, rvalid && (mn == 0.f || mx == 0.f))) {   // rare: numpy's signed-zero choice
+    unsigned kz = 0u;
+#pragma unroll
+    for (int c = 0; c < E / 4; ++c) {
+      const int p0 = 4 * (q + LPR * c);
+      kz = max(max(max(kz, np_zero_key(cur[c].x, p0, p.d)), np_zero_key(cur[c].y, p0 + 1, p.d)),
+               max(np_zero_key(cur[c].z, p0 + 2, p.d), np_zero_key(cur[c].w, p0 + 3, p.d)));
+    }
+    np_zero_apply(group_umax<LPR>(kz), mn, mx);
+  }
   bool bad = false;
   if (__any_sync(FULL, !isfinite(sm) && rvalid)) {
     bool lb = false;
@@ -1719,14 +1754,14 @@ namespace {
 constexpr int HP_NS = 3;   // chunk c's H2D overlaps chunk c-1's kernel and chunk c-2's D2H
 struct HostBuf {
   float* x = nullptr; uint8_t* out = nullptr; double* lo = nullptr; double* hi = nullptr;
-  int32_t* i0 = nullptr; int32_t* i1 = nullptr; int32_t* status = nullptr;
+  int32_t* i0 = nullptr; int32_t* i1 = nullptr; int32_t* status = nullptr; double* nrm = nullptr;
 };
 struct HostPipe {
   std::mutex mu;
   bool init = false;
   cudaStream_t st[HP_NS] = {};
   HostBuf bf[HP_NS];
-  size_t x_bytes = 0, out_bytes = 0, i0_rows = 0, i1_rows = 0, lohi_rows = 0;   // capacities
+  size_t x_bytes = 0, out_bytes = 0, i0_rows = 0, i1_rows = 0, lohi_rows = 0, nrm_rows = 0;   // capacities
   int32_t* hstatus = nullptr;
   int64_t hstatus_n = 0;
 };
@@ -1742,7 +1777,7 @@ cudaError_t grow(T** p, size_t have, size_t want) {
 
 // capacity for chunks of `chunk` rows (grow-only); returns a cudaError_t
 cudaError_t pipe_reserve(HostPipe& hp, int64_t chunk, int64_t dim, int64_t stride, bool want_i1,
-                         bool want_lohi, int64_t nchunks) {
+                         bool want_lohi, bool want_norm, int64_t nchunks) {
   cudaError_t e = cudaSuccess;
   if (!hp.init) {
     for (int i = 0; i < HP_NS && e == cudaSuccess; i++)
@@ -1760,9 +1795,10 @@ cudaError_t pipe_reserve(HostPipe& hp, int64_t chunk, int64_t dim, int64_t strid
     if (e == cudaSuccess && want_i1) e = grow(&B.i1, hp.i1_rows * 4, rows * 4);
     if (e == cudaSuccess && want_lohi) e = grow(&B.lo, hp.lohi_rows * 8, rows * 8);
     if (e == cudaSuccess && want_lohi) e = grow(&B.hi, hp.lohi_rows * 8, rows * 8);
+    if (e == cudaSuccess && want_norm) e = grow(&B.nrm, hp.nrm_rows * 8, rows * 8);
   }
   if (e != cudaSuccess) {   // partially grown: forget every capacity, the next call reallocates
-    hp.x_bytes = hp.out_bytes = hp.i0_rows = hp.i1_rows = hp.lohi_rows = 0;
+    hp.x_bytes = hp.out_bytes = hp.i0_rows = hp.i1_rows = hp.lohi_rows = hp.nrm_rows = 0;
     return e;
   }
   hp.x_bytes = std::max(hp.x_bytes, xb);
@@ -1770,6 +1806,7 @@ cudaError_t pipe_reserve(HostPipe& hp, int64_t chunk, int64_t dim, int64_t strid
   hp.i0_rows = std::max(hp.i0_rows, rows);
   if (want_i1) hp.i1_rows = std::max(hp.i1_rows, rows);
   if (want_lohi) hp.lohi_rows = std::max(hp.lohi_rows, rows);
+  if (want_norm) hp.nrm_rows = std::max(hp.nrm_rows, rows);
   if (hp.hstatus_n < nchunks) {
     if (hp.hstatus) cudaFreeHost(hp.hstatus);
     hp.hstatus = nullptr;
@@ -1853,6 +1890,11 @@ int eq4_quantize_pack(const float* x, int64_t rows, int64_t dim, int64_t ld, int
                       double r, int aux, uint8_t* packed, double* xmin, double* xmax,
                       int32_t* info0, int32_t* info1, double* norm, int32_t* status,
                       void* stream) {
+  // the status word describes this call: cleared on the stream before the kernels OR into it
+  if (status) {
+    const cudaError_t e = cudaMemsetAsync(status, 0, 4, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "status reset");
+  }
   return quantize_pack_impl(x, rows, dim, ld, method, b, r, aux, packed, xmin, xmax, info0, info1,
                             norm, status, stream, nullptr);
 }
@@ -2039,7 +2081,8 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
   HostPipe& hp = g_pipes[dev];
   std::lock_guard<std::mutex> lk(hp.mu);
   int rc = EQ4_OK;
-  cudaError_t e = pipe_reserve(hp, chunk, dim, stride, info1 != nullptr, want_lohi, nchunks);
+  cudaError_t e = pipe_reserve(hp, chunk, dim, stride, info1 != nullptr, want_lohi, norm != nullptr,
+                               nchunks);
   if (e != cudaSuccess) return cuda_fail(e, "host pipeline buffers");
   cudaStream_t* st = hp.st;
   HostBuf* bf = hp.bf;
@@ -2072,14 +2115,15 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
     if (e == cudaSuccess) e = cudaMemsetAsync(B.status, 0, 4, s);
     if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
     rc = quantize_pack_impl(B.x, nr, dim, dim, method, b, r, aux, B.out, want_lohi ? B.lo : nullptr,
-                            want_lohi ? B.hi : nullptr, B.i0, info1 ? B.i1 : nullptr, nullptr, B.status, s,
-                            tkeys);
+                            want_lohi ? B.hi : nullptr, B.i0, info1 ? B.i1 : nullptr, norm ? B.nrm : nullptr,
+                            B.status, s, tkeys);
     if (rc) break;
     e = cudaMemcpyAsync(packed + r0 * stride, B.out, nr * stride, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && info0) e = cudaMemcpyAsync(info0 + r0, B.i0, nr * 4, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && info1) e = cudaMemcpyAsync(info1 + r0, B.i1, nr * 4, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && want_lohi) e = cudaMemcpyAsync(xmin + r0, B.lo, nr * 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && want_lohi) e = cudaMemcpyAsync(xmax + r0, B.hi, nr * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && norm) e = cudaMemcpyAsync(norm + r0, B.nrm, nr * 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(hstatus + c, B.status, 4, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) { rc = cuda_fail(e, "D2H"); break; }
   }

@@ -32,6 +32,43 @@ __device__ __forceinline__ double div15(double w) {
   return __fma_rn(r, y, q);
 }
 
+// ---------------------------------------------------------------------------
+// numpy's choice among equal extrema (the sign of a zero min / max)
+// ---------------------------------------------------------------------------
+// np.min / np.max of a row (clipping.py:61,163; histclip.py:57) return one of
+// several equal extrema; for a zero extremum that choice is the sign of the
+// bias the row is packed with.  numpy's AVX-512 reduction (restated op by op in
+// oracle/eq4_oracle.c np_reduce_ext) makes the choice a fixed priority over
+// positions p of the row (d elements), the same for min and max:
+//   x[0] lowest; p in 1 .. 8*nv (nv = (d-1)/8 full vectors) by vector lane
+//   k = (p-1) % 8 in the order 1 > 5 > 3 > 7 > 0 > 4 > 2 > 6 (the _mm512_reduce
+//   tree), the later p within a lane; above all the scalar tail p > 8*nv, the
+//   later the higher.  np_zero_key is 0 for a non-zero element, else a key
+//   whose maximum over the row's zeros carries the winner's sign in bit 0.
+__device__ __forceinline__ unsigned np_zero_key(float v, int p, int d) {
+  if (v != 0.f) return 0u;
+  const int nv8 = (d - 1) >> 3;
+  unsigned prio;
+  if (p == 0) {
+    prio = 1u;
+  } else if (p > 8 * nv8) {
+    prio = (1u << 29) + (unsigned)p;
+  } else {
+    const int k = (p - 1) & 7;
+    const unsigned rank = (0x51736284u >> (4 * k)) & 0xFu;   // lane 1 -> 8, 5 -> 7, ..., 6 -> 1
+    prio = (rank << 24) + (unsigned)((p - 1) >> 3) + 2u;
+  }
+  return (prio << 1) | (__float_as_uint(v) >> 31);
+}
+
+// Apply the winner of a group's zero keys (already max-reduced) to a zero
+// min / max: the row's extremum takes the winning zero's sign.
+__device__ __forceinline__ void np_zero_apply(unsigned kz, float& mn, float& mx) {
+  const float z = (kz & 1u) ? -0.f : 0.f;
+  if (mn == 0.f) mn = z;
+  if (mx == 0.f) mx = z;
+}
+
 // np.clip(x, lo, hi) == minimum(maximum(x, lo), hi) for finite operands.
 __device__ __forceinline__ double np_clip(double x, double lo, double hi) {
   double t = x > lo ? x : lo;

@@ -281,6 +281,11 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
     }
     bad = __any_sync(FULL, bad);
     if (bad && lane == 0 && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
+    if (mn == 0.f || mx == 0.f) {   // rare: numpy's signed-zero choice (histclip.py:57)
+      unsigned kz = 0u;
+      for (int k = lane; k < d; k += 32) kz = max(kz, np_zero_key(xs[k], k, d));
+      np_zero_apply(__reduce_max_sync(FULL, kz), mn, mx);
+    }
     const double lo = (double)mn, hi = (double)mx;
     double wlo = lo, whi = hi, norm = 0.0;
     int best_s = 0, best_n = 1;
@@ -435,9 +440,16 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
 
 using namespace eq4;
 
-// U tables cached per (device, b); built once with k_hist_table.
+// U tables cached per (device, b); built once with k_hist_table on the first
+// caller's stream.  No host synchronisation: the build is followed by an event,
+// and every call (on any stream) waits on that event on the device before its
+// k_hist launch -- a no-op once the table exists.
+struct UTable {
+  double* U = nullptr;
+  cudaEvent_t ready = nullptr;
+};
 static std::mutex g_u_mu;
-static std::map<std::pair<int, int>, double*> g_u_tables;
+static std::map<std::pair<int, int>, UTable> g_u_tables;
 
 static const double* hist_table(int b, cudaStream_t s, std::string& err) {
   int dev = 0;
@@ -445,15 +457,25 @@ static const double* hist_table(int b, cudaStream_t s, std::string& err) {
   std::lock_guard<std::mutex> lk(g_u_mu);
   auto key = std::make_pair(dev, b);
   auto it = g_u_tables.find(key);
-  if (it != g_u_tables.end()) return it->second;
-  double* U = nullptr;
-  cudaError_t e = cudaMalloc(&U, sizeof(double) * (size_t)b * (b + 1) / 2);
-  if (e != cudaSuccess) { err = std::string("cudaMalloc U: ") + cudaGetErrorString(e); return nullptr; }
-  k_hist_table<<<b, 128, 0, s>>>(b, U);
-  e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) { err = std::string("U table: ") + cudaGetErrorString(e); cudaFree(U); return nullptr; }
-  g_u_tables[key] = U;
-  return U;
+  if (it == g_u_tables.end()) {
+    UTable t;
+    cudaError_t e = cudaMalloc(&t.U, sizeof(double) * (size_t)b * (b + 1) / 2);
+    if (e != cudaSuccess) { err = std::string("cudaMalloc U: ") + cudaGetErrorString(e); return nullptr; }
+    k_hist_table<<<b, 128, 0, s>>>(b, t.U);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&t.ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(t.ready, s);
+    if (e != cudaSuccess) {
+      err = std::string("U table: ") + cudaGetErrorString(e);
+      cudaFree(t.U);
+      if (t.ready) cudaEventDestroy(t.ready);
+      return nullptr;
+    }
+    it = g_u_tables.emplace(key, t).first;
+  }
+  const cudaError_t e = cudaStreamWaitEvent(s, it->second.ready, 0);
+  if (e != cudaSuccess) { err = std::string("U table wait: ") + cudaGetErrorString(e); return nullptr; }
+  return it->second.U;
 }
 
 int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b, int aux,

@@ -172,7 +172,12 @@ __device__ __forceinline__ void lane_aciq(const RowView& xr, int d, float mn, fl
   const double mean = __ddiv_rn(np_sum([&](int k) { return (double)xr[k]; }, d), n);
   const double mad = __ddiv_rn(np_sum([&](int k) { return fabs(__dsub_rn((double)xr[k], mean)); }, d), n);
   const double alpha = __dmul_rn(5.03, mad);
-  if (alpha == 0.0) {
+  if (alpha == 0.0) {   // clipping.py:137-138 -> clip_range_asym (numpy's signed-zero choice)
+    if (mn == 0.f || mx == 0.f) {
+      unsigned kz = 0u;
+      for (int k = 0; k < d; k++) kz = max(kz, np_zero_key(xr[k], k, d));
+      np_zero_apply(kz, mn, mx);
+    }
     lo = (double)mn;
     hi = (double)mx;
   } else {

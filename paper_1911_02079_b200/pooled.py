@@ -78,6 +78,10 @@ def sparse_lengths_sum_4bit(p: PackedTable4, query: PooledQuery, *, out=None, st
     L = _lib.load()
     packed = p.to_device()
     dev = packed.device
+    if stream is not None and stream != torch.cuda.current_stream(dev):
+        # allocate, launch and read the status word on the caller's stream
+        with torch.cuda.stream(stream):
+            return sparse_lengths_sum_4bit(p, query, out=out, stream=None, check=check)
     idx = query.indices if query.on_device else torch.from_numpy(query.indices).to(dev)
     ln = query.lengths if query.on_device else torch.from_numpy(query.lengths).to(dev)
     batch, nidx = int(ln.numel()), int(idx.numel())

@@ -429,10 +429,63 @@ def make_hist_apprx():
     print("hist_apprx: done")
 
 
+def signed_zero_rows(d, rng):
+    """Rows whose min or max is a zero: numpy's np.min / np.max then return one of several
+    equal extrema, and that choice is the sign of the packed bias (uniform.py:80)."""
+    rows = []
+    for kind in range(6):
+        for _ in range(6):
+            x = (np.abs(rng.standard_normal(d)) + 0.01).astype(np.float32)
+            nz = int(rng.integers(1, max(1, min(d, 6)) + 1))
+            pos = rng.choice(d, nz, replace=False)
+            if kind == 0:      # lone -0.0 minimum
+                x[pos[0]] = -0.0
+            elif kind == 1:    # +0.0 / -0.0 minimum ties
+                x[pos] = np.where(rng.random(nz) < 0.5, np.float32(0.0), np.float32(-0.0))
+            elif kind == 2:    # all zeros of random signs
+                x[:] = np.where(rng.random(d) < 0.5, np.float32(0.0), np.float32(-0.0))
+            elif kind == 3:    # zero maximum (negative row), mixed signs
+                x = -x
+                x[pos] = np.where(rng.random(nz) < 0.5, np.float32(0.0), np.float32(-0.0))
+            elif kind == 4:    # lone -0.0 maximum
+                x = -x
+                x[pos[0]] = -0.0
+            else:              # many zeros of both signs among positives
+                k = max(1, d // 3)
+                p2 = rng.choice(d, k, replace=False)
+                x[p2] = np.where(rng.random(k) < 0.5, np.float32(0.0), np.float32(-0.0))
+            rows.append(x)
+    return np.stack(rows)
+
+
+def make_signed_zero():
+    """Every row-wise method on rows whose extremum is a (signed) zero: packed bytes and the
+    float64 ranges with their zero signs, from the reference (np.min/np.max order, the
+    greedy pair recording x0 + 0*step, histclip.py:170's lo + w*s)."""
+    rng = np.random.default_rng(1911)
+    out = {}
+    for d in (1, 2, 7, 8, 9, 16, 17, 64, 65, 100, 128, 200, 300):
+        x = signed_zero_rows(d, rng)
+        out[f"x_{d}"] = x
+        t = eq.EmbeddingTable(x)
+        for method in ("asym", "sym", "greedy", "hist-brute", "hist-apprx", "aciq", "gss"):
+            b = 40 if method == "hist-brute" and d > 64 else 200
+            for aux in ("fp16", "fp32"):
+                q = eq.quantize_table(t, method, 4, aux, b=b)
+                out[f"packed_{d}_{method}_{aux}"] = eq.pack_table4(q).buffer.copy()
+            lo, hi = [], []
+            for i in range(t.rows):
+                cr = eq.row_clip_range(method, t.row(i), 4, b=b)
+                lo.append(cr.xmin); hi.append(cr.xmax)
+            out[f"range_{d}_{method}"] = np.array([lo, hi])
+    np.savez_compressed(os.path.join(HERE, "signed_zero.npz"), **out)
+    print("signed_zero: done")
+
+
 if __name__ == "__main__":
     which = sys.argv[2:] or ["mse", "edge", "hist", "config1", "sls", "files", "methods", "kmeans",
-                             "hist_apprx"]
+                             "hist_apprx", "signed_zero"]
     for w in which:
         {"mse": make_mse, "edge": make_edge, "hist": make_hist, "config1": make_config1,
          "sls": make_sls, "files": make_files, "methods": make_methods, "kmeans": make_kmeans,
-         "hist_apprx": make_hist_apprx}[w]()
+         "hist_apprx": make_hist_apprx, "signed_zero": make_signed_zero}[w]()
