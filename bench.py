@@ -126,6 +126,85 @@ def cpu_reference_rate(rows_sample: int, seed: int = 1911, steps: int = 1, warmu
     return rows_sample / t, nthreads, t
 
 
+def parity_report(eq, torch, dev, x, out, method, b, sample=0, x_host=None, nthreads=0):
+    """Check a timed launch's packed bytes against the CPU oracle on the same table.
+
+    x (device, rows x d) is the timed input and ``out`` the timed launch's packed output
+    (left untouched); per-row float64 ranges come from one more, untimed launch into a
+    scratch buffer.  ``sample`` = 0 checks every row, else a strided sample of that many
+    rows (first and last included).  GREEDY adds the reference's own near-ties from the
+    oracle's walk (relative gap < 1e-6 between the two competing losses, clipping.py:185,
+    and between candidate and best, :187,191) and the kernel's float64 re-decision count;
+    HIST-BRUTE counts windows that differ only at a norm tie (<= 1e-12 relative).  Run
+    outside every timed region; the oracle is the checker, not the thing measured."""
+    import oracle
+    import numpy as np
+
+    rows, d = int(x.shape[0]), int(x.shape[1])
+    stride = eq.packed_row_stride(d, AUX)
+    t0 = time.perf_counter()
+    rr = eq.RowResults(torch.empty(rows, dtype=torch.float64, device=dev),
+                       torch.empty(rows, dtype=torch.float64, device=dev),
+                       torch.empty(rows, dtype=torch.int32, device=dev),
+                       torch.empty(rows, dtype=torch.int32, device=dev),
+                       torch.empty(rows, dtype=torch.float64, device=dev))
+    from paper_1911_02079_b200 import _lib
+
+    _lib.diag_counters(reset=True)
+    scratch = torch.empty(rows * stride, dtype=torch.uint8, device=dev)
+    eq.quantize_pack_table4(x, method, AUX, b, R, out=scratch, rows_out=rr)
+    diag = _lib.diag_counters(reset=True)
+    same_as_timed = bool(torch.equal(scratch, out.view(-1)[: rows * stride]))
+    del scratch
+    if sample and sample < rows:
+        idx = torch.unique(torch.cat([torch.arange(0, rows, max(1, rows // sample), device=dev),
+                                      torch.tensor([rows - 1], device=dev)]))
+    else:
+        idx = None
+    sel = (lambda t: t) if idx is None else (lambda t: t[idx])
+    got = sel(out.view(rows, stride)).cpu().numpy()
+    glo, ghi = sel(rr.xmin).cpu().numpy(), sel(rr.xmax).cpu().numpy()
+    gi0, gi1 = sel(rr.info0).cpu().numpy(), sel(rr.info1).cpu().numpy()
+    if x_host is not None and idx is None:
+        xs = x_host
+    else:
+        xs = sel(x).cpu().numpy()
+    nthreads = nthreads or oracle.max_threads()
+    rep = {"rows_checked": int(xs.shape[0]), "of_rows": rows, "method": method}
+    if method == "greedy":
+        want, g_lr, g_best = oracle.quantize_pack_table_gaps(xs, b, R, AUX, nthreads)
+    else:
+        want = oracle.quantize_pack_table(xs, method, b, R, AUX, nthreads)
+    bad_bytes = np.nonzero((got != want.packed.reshape(-1, stride)).any(axis=1))[0]
+    bits = lambda a: np.ascontiguousarray(a, np.float64).view(np.uint64)
+    bad_range = np.nonzero((bits(glo) != bits(want.xmin)) | (bits(ghi) != bits(want.xmax)))[0]
+    rep["byte_mismatches"] = int(bad_bytes.size)
+    rep["range_mismatches"] = int(bad_range.size)
+    if method == "greedy":
+        rep["near_ties_lr"] = int(np.sum(g_lr < 1e-6))
+        rep["near_ties_best"] = int(np.sum(g_best < 1e-6))
+        bad = np.union1d(bad_bytes, bad_range)
+        # the only exception north_star permits: the reference's two competing losses within 1e-6
+        rep["excused_lr_ties"] = int(np.sum(g_lr[bad] < 1e-6)) if bad.size else 0
+        it = np.where(gi0 >= 0, gi0, 0).astype(np.int64)
+        rep["iterations_match"] = bool(np.array_equal(np.where(want.info0 >= 0, want.info0, 0), it))
+        rep["exact_redecisions"] = diag["exact_redecisions"]
+        rep["exact_code_rows"] = diag["exact_code_rows"]
+        rep["redecisions_over_rows"] = rows
+    if method == "hist-brute":
+        ties = 0
+        for i in np.union1d(bad_bytes, bad_range):
+            ng = oracle.hist_window_norm(xs[i], b, int(gi0[i]), int(gi1[i]))
+            no = oracle.hist_window_norm(xs[i], b, int(want.info0[i]), int(want.info1[i]))
+            if abs(ng - no) <= 1e-12 * max(abs(ng), abs(no)):
+                ties += 1
+        rep["hist_ties"] = ties
+    rep["launch_bytes_reproduced"] = same_as_timed
+    rep["oracle_threads"] = nthreads
+    rep["check_s"] = round(time.perf_counter() - t0, 2)
+    return rep
+
+
 def run_reference(args, rank: int):
     if rank != 0:
         return
@@ -204,6 +283,11 @@ def run_ours(args, rank: int, world: int):
 
     # end to end through the public API: pinned host table in, packed bytes out
     e2e = None
+    parity = None
+    if not args.no_parity:
+        # the timed bytes against the oracle on the same table (every row at N = 1)
+        psample = args.parity_rows if args.parity_rows >= 0 else (0 if world == 1 else 1_000_000)
+        parity = parity_report(eq, torch, dev, x, out, "greedy", B, sample=psample)
     if not args.no_e2e:
         # every rank pins its own table + output; all ranks agree before any collective
         ok, why = 1, ""
@@ -287,16 +371,17 @@ def run_ours(args, rank: int, world: int):
                      "hbm_floor_ms": bytes_per_step / (float(peaks.get('hbm_gbs', 6546.9)) * 1e9) * 1e3},
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "parity": parity,
         "gpu_launches": args.steps,
         "clocks": clocks.summary(),
     }
     if args.secondary and world == 1:   # the other configs are single-GPU lines
-        line["secondary"] = secondary(eq, workloads, torch, dev, peaks, fp32_peak)
+        line["secondary"] = secondary(eq, workloads, torch, dev, peaks, fp32_peak, check=not args.no_parity)
         line["secondary"]["sls_20Mx64_greedy_packed"] = sls_secondary(eq, torch, dev, peaks, out, rows)
     print(json.dumps(line), flush=True)
 
 
-def _time_method(eq, torch, dev, x, method, b, n=10, warm=3):
+def _time_method(eq, torch, dev, x, method, b, n=10, warm=3, parity=None, parity_sample=0):
     """Device time (CUDA events on the current stream) of one fused launch over x, plus the
     GREEDY loss-evaluation count of that launch (clipping.py:174,183-184) for the roofline."""
     rows, d = x.shape
@@ -321,11 +406,14 @@ def _time_method(eq, torch, dev, x, method, b, n=10, warm=3):
     torch.cuda.synchronize(dev)
     if int(st.item()):
         raise SystemExit(f"kernel status {int(st.item())} in a secondary workload ({method})")
+    ms = e0.elapsed_time(e1) / n
+    if parity is not None:   # the timed launches' bytes against the oracle (untimed)
+        parity.update(parity_report(eq, torch, dev, x, out, method, b, sample=parity_sample))
     del out
-    return e0.elapsed_time(e1) / n, evals
+    return ms, evals
 
 
-def secondary(eq, workloads, torch, dev, peaks, fp32_peak):
+def secondary(eq, workloads, torch, dev, peaks, fp32_peak, check=True):
     """The other BASELINE.json configs, device-timed (each table >> L2 or re-read per launch):
     config 2 (ASYM 4M x 64, HBM-bound), config 3 (GREEDY 4M x 128 mixed), config 4 (HIST-BRUTE
     16,384 x 64), config 5a (GREEDY d-sweep over 1 GiB N(0,1) tables), plus the HIST-APPRX, ACIQ
@@ -341,35 +429,44 @@ def secondary(eq, workloads, torch, dev, peaks, fp32_peak):
                 "alg_TFLOPs": flop / ms / 1e9, "fp32_frac": flop / ms / 1e9 / fp32_peak}
 
     x = workloads.gaussian_table(4_194_304, 64, 7, device=dev)
-    ms, _ = _time_method(eq, torch, dev, x, "asym", B)
+    par = {} if check else None
+    ms, _ = _time_method(eq, torch, dev, x, "asym", B, parity=par, parity_sample=0)
     byt = 4_194_304 * (4 * 64 + 32 + 4)
     res["asym_4Mx64_config2"] = {"ms": ms, "rows_per_s": 4_194_304 / ms * 1e3, "GBps": byt / ms / 1e6,
-                                 "hbm_frac": byt / ms / 1e6 / hbm}
+                                 "hbm_frac": byt / ms / 1e6 / hbm, "parity": par}
     del x
     x = workloads.mixed_table(4_194_304, 128, 7, device=dev)
-    ms, ev = _time_method(eq, torch, dev, x, "greedy", B)
-    res["greedy_4Mx128_mixed_config3"] = greedy_line(x, 128, ms, ev)
+    par = {} if check else None
+    ms, ev = _time_method(eq, torch, dev, x, "greedy", B, parity=par, parity_sample=1_000_000)
+    res["greedy_4Mx128_mixed_config3"] = dict(greedy_line(x, 128, ms, ev), parity=par)
     del x
     # config 4: HIST-BRUTE b=200 (compute-bound, no roofline target): per-row time and the
     # reference's bin-visit counter rate (histclip.py:162-164)
     x = workloads.gaussian_table(16384, 64, 7, device=dev)
-    ms, _ = _time_method(eq, torch, dev, x, "hist-brute", 200, n=5, warm=2)
+    par = {} if check else None
+    ms, _ = _time_method(eq, torch, dev, x, "hist-brute", 200, n=5, warm=2, parity=par, parity_sample=0)
     visits = 16384 * 200 * (200 * 201 // 2)
+    # the reference's bin-visit counter: the pruned kernel scores only a few % of the windows
     res["hist_brute_16384x64_config4"] = {"ms": ms, "us_per_row": ms * 1e3 / 16384,
-                                          "bin_visits_per_s": visits / ms * 1e3}
+                                          "reference_equivalent_bin_visits_per_s": visits / ms * 1e3,
+                                          "parity": par}
     # HIST-APPRX (histclip.py:181-217) on the same table: 2b - 1 = 399 window norms per row
-    ms, _ = _time_method(eq, torch, dev, x, "hist-apprx", 200, n=5, warm=2)
-    res["hist_apprx_16384x64"] = {"ms": ms, "us_per_row": ms * 1e3 / 16384}
+    par = {} if check else None
+    ms, _ = _time_method(eq, torch, dev, x, "hist-apprx", 200, n=5, warm=2, parity=par, parity_sample=0)
+    res["hist_apprx_16384x64"] = {"ms": ms, "us_per_row": ms * 1e3 / 16384, "parity": par}
     del x
     # ACIQ (clipping.py:115-139): two numpy-order float64 sums per row + codes, bandwidth-class
     x = workloads.gaussian_table(4_194_304, 64, 7, device=dev)
-    ms, _ = _time_method(eq, torch, dev, x, "aciq", B)
-    res["aciq_4Mx64"] = {"ms": ms, "GBps": byt / ms / 1e6, "hbm_frac": byt / ms / 1e6 / hbm}
+    par = {} if check else None
+    ms, _ = _time_method(eq, torch, dev, x, "aciq", B, parity=par, parity_sample=1_000_000)
+    res["aciq_4Mx64"] = {"ms": ms, "GBps": byt / ms / 1e6, "hbm_frac": byt / ms / 1e6 / hbm,
+                         "parity": par}
     del x
     # GSS (clipping.py:70-112): ~23 exact float64 quant_mse per row
     x = workloads.gaussian_table(1_048_576, 64, 7, device=dev)
-    ms, _ = _time_method(eq, torch, dev, x, "gss", B, n=5, warm=2)
-    res["gss_1Mx64"] = {"ms": ms, "rows_per_s": 1_048_576 / ms * 1e3}
+    par = {} if check else None
+    ms, _ = _time_method(eq, torch, dev, x, "gss", B, n=5, warm=2, parity=par, parity_sample=250_000)
+    res["gss_1Mx64"] = {"ms": ms, "rows_per_s": 1_048_576 / ms * 1e3, "parity": par}
     del x
     # row-wise KMEANS codebooks (codebook.py:35-172), the EMBQ kmeans_row payload
     from paper_1911_02079_b200.codebook import kmeans_rows, kmeans_row_stride
@@ -393,8 +490,10 @@ def secondary(eq, workloads, torch, dev, peaks, fp32_peak):
     for d in (16, 32, 64, 128, 256, 512, 1024, 2048):
         rows = (1 << 30) // (4 * d)
         x = workloads.gaussian_table(rows, d, 7, device=dev)
-        ms, ev = _time_method(eq, torch, dev, x, "greedy", B, n=5, warm=2)
-        sweep[str(d)] = greedy_line(x, d, ms, ev)
+        par = {} if check else None
+        ms, ev = _time_method(eq, torch, dev, x, "greedy", B, n=5, warm=2, parity=par,
+                              parity_sample=1_000_000)
+        sweep[str(d)] = dict(greedy_line(x, d, ms, ev), parity=par)
         del x
     res["greedy_dsweep_1GiB_config5a"] = sweep
     return res
@@ -459,6 +558,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed bytes")
+    ap.add_argument("--parity-rows", type=int, default=-1,
+                    help="rows checked against the oracle (0 = all; default all at N = 1, 1M per rank above)")
     ap.add_argument("--secondary", action=argparse.BooleanOptionalAction, default=True,
                     help="config 2 ASYM, config 3 GREEDY and the SLS lookup, device-timed (rank 0)")
     args = ap.parse_args()

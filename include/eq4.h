@@ -181,6 +181,16 @@ int64_t eq4_kmeans_row_stride(int64_t dim, int aux);
 int eq4_kmeans_rows(const float *x, int64_t rows, int64_t dim, int64_t ld, int aux, uint8_t *out,
                     int32_t *iters, int32_t *status, void *stream);
 
+/* Diagnostics: counters of the GREEDY kernel's rare paths on the current device,
+ * accumulated over launches since the last reset: out[0] = float64 re-decisions
+ * (one per row and loop iteration whose fp32 comparison fell inside the error
+ * band), out[1] = rows whose codes took the float64 codec, out[2] = comparisons
+ * settled by counting the elements within reach of a rounding boundary (inside
+ * the band for d misrounded elements, outside the one for 2), out[3] = of those,
+ * escalated to a float64 re-decision (more than 2 such elements on a side).
+ * reset != 0 zeroes them after the read.  Synchronous (device-wide). */
+int eq4_diag_counters(int64_t *out, int reset);
+
 /* Diagnostics: internal arithmetic self-test on the current device (mismatch
  * count, -1 on CUDA error).  which 0/1: the divide-free float64 w/15 used for
  * scales against the IEEE divide, on float differences / full-range doubles. */

@@ -90,7 +90,10 @@ def lib():
         L.eqo_clip_range_aciq.argtypes = [vp, i64, vp, vp, vp]
         L.eqo_clip_range_gss.argtypes = [vp, i64, i32, vp, vp, vp, vp]
         L.eqo_sls4.argtypes = [vp, i64, i64, i32, vp, i64, vp, i64, vp, vp]
+        L.eqo_quantize_pack_table_gaps.argtypes = [vp, i64, i64, i64, i32, i32, dbl, i32, vp, vp,
+                                                   vp, vp, vp, vp, vp, vp, i32]
         L.eqo_np_extremum.argtypes = [vp, i64, i32]
+        L.eqo_greedy_trace.argtypes = [vp, i64, i32, dbl, i32, vp, vp, vp, vp, vp, vp]
         L.eqo_np_extremum.restype = dbl
         _lib = L
     return _lib
@@ -288,6 +291,41 @@ def quantize_pack_table(x, method: str, b: int = 200, r: float = 0.16, aux: str 
     if rc:
         raise OracleError(rc)
     return TableResult(packed, lo, hi, i0, i1, nv)
+
+
+def greedy_trace(x, b: int = 200, r: float = 0.16, cap: int = 100000):
+    """The reference walk of clip_range_greedy, step by step: (nl, nr, loss_l, loss_r) arrays
+    with one entry per loop iteration (clipping.py:180-192)."""
+    x = _f32(x)
+    cap = min(cap, 2 * b + 2)
+    nl, nr = np.zeros(cap, np.int32), np.zeros(cap, np.int32)
+    ll, lr = np.zeros(cap), np.zeros(cap)
+    it = np.zeros(1, np.int32)
+    scratch = np.empty(max(16, x.size), np.float64)
+    rc = lib().eqo_greedy_trace(_p(x), x.size, b, float(r), cap, _p(it), _p(nl), _p(nr), _p(ll),
+                                _p(lr), _p(scratch))
+    if rc:
+        raise OracleError(rc)
+    n = int(it[0])
+    return nl[:n], nr[:n], ll[:n], lr[:n]
+
+
+def quantize_pack_table_gaps(x, b: int = 200, r: float = 0.16, aux: str = "fp16", nthreads: int = 0):
+    """GREEDY table driver plus, per row, the smallest relative gap of the reference's two
+    competing losses (clipping.py:185) and of candidate vs best (clipping.py:187,191) over
+    the walk.  Returns (TableResult, gap_lr, gap_best)."""
+    x = _f32(x)
+    rows, d = x.shape
+    packed = np.zeros(rows * packed_row_stride(d, aux), np.uint8)
+    lo, hi, nv = np.zeros(rows), np.zeros(rows), np.zeros(rows)
+    i0, i1 = np.zeros(rows, np.int32), np.zeros(rows, np.int32)
+    g1, g2 = np.full(rows, np.inf), np.full(rows, np.inf)
+    rc = lib().eqo_quantize_pack_table_gaps(_p(x), rows, d, d, METHODS["greedy"], b, float(r),
+                                            AUX[aux], _p(packed), _p(lo), _p(hi), _p(i0), _p(i1),
+                                            _p(nv), _p(g1), _p(g2), int(nthreads))
+    if rc:
+        raise OracleError(rc)
+    return TableResult(packed, lo, hi, i0, i1, nv), g1, g2
 
 
 def sparse_lengths_sum4(packed, rows: int, d: int, aux: str, indices, lengths):

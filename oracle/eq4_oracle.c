@@ -264,9 +264,63 @@ int eqo_clip_range_gss(const float *x, long d, int nbits, double *scratch, doubl
  * reference's WorkCounters.loss_evals == 1 + 2*iters (0 for constant rows).
  * *best_i / *best_j receive the step counts of the returned pair:
  * (x0 + i*step, x1 - j*step). */
+static int greedy_impl(const float *x, long d, int nbits, int b, double r, double *lo, double *hi,
+                       int *iters, int *best_i, int *best_j, double *scratch, double *gap_lr,
+                       double *gap_best);
+
 int eqo_clip_range_greedy(const float *x, long d, int nbits, int b, double r,
                           double *lo, double *hi, int *iters, int *best_i, int *best_j,
                           double *scratch) {
+    return greedy_impl(x, d, nbits, b, r, lo, hi, iters, best_i, best_j, scratch, NULL, NULL);
+}
+
+/* Test hook: the walk of clip_range_greedy step by step.  For iteration t (t < *iters):
+ * nl[t], nr[t] before the move, loss_l[t], loss_r[t] (clipping.py:181-184).
+ * cap = capacity of the arrays.  Returns EQO_* (the walk stops at cap). */
+int eqo_greedy_trace(const float *x, long d, int b, double r, int cap, int *iters, int *nl_out,
+                     int *nr_out, double *loss_l_out, double *loss_r_out, double *scratch) {
+    if (b < 1) return EQO_EB;
+    if (!(0.0 < r && r <= 1.0)) return EQO_ER;
+    if (d <= 0) return EQO_EEMPTY;
+    double x0, x1;
+    row_minmax(x, d, &x0, &x1);
+    *iters = 0;
+    if (x0 == x1) return EQO_OK;
+    double stepsize = (x1 - x0) / (double)b;
+    double min_steps = (double)b * (1.0 - r) * stepsize;
+    long nl = 0, nr = 0;
+    int it = 0;
+    while ((x0 + (double)nl * stepsize) + min_steps < (x1 - (double)nr * stepsize) && it < cap) {
+        double lmin = x0 + (double)(nl + 1) * stepsize, lmax = x1 - (double)nr * stepsize;
+        double rmin = x0 + (double)nl * stepsize, rmax = x1 - (double)(nr + 1) * stepsize;
+        double loss_l, loss_r;
+        int rc = eqo_quant_mse(x, d, lmin, lmax, 4, scratch, &loss_l);
+        if (!rc) rc = eqo_quant_mse(x, d, rmin, rmax, 4, scratch, &loss_r);
+        if (rc) return rc;
+        nl_out[it] = (int)nl; nr_out[it] = (int)nr;
+        loss_l_out[it] = loss_l; loss_r_out[it] = loss_r;
+        if (loss_l < loss_r) nl += 1; else nr += 1;
+        it++;
+    }
+    *iters = it;
+    return EQO_OK;
+}
+
+/* Relative gap |a - b| / max(|a|, |b|) of two competing losses (0 when both are 0). */
+static double rel_gap(double a, double b) {
+    const double m = fmax(fabs(a), fabs(b));
+    return m > 0.0 ? fabs(a - b) / m : 0.0;
+}
+
+/* The walk of eqo_clip_range_greedy; gap_lr / gap_best (optional) receive the smallest
+ * relative gap over the walk between the two competing losses (clipping.py:185) and
+ * between the chosen candidate and the best so far (clipping.py:187,191) -- the
+ * reference's own near-ties, which north_star asks to count (INFINITY: no iteration). */
+static int greedy_impl(const float *x, long d, int nbits, int b, double r, double *lo, double *hi,
+                       int *iters, int *best_i, int *best_j, double *scratch, double *gap_lr,
+                       double *gap_best) {
+    if (gap_lr) *gap_lr = INFINITY;
+    if (gap_best) *gap_best = INFINITY;
     if (b < 1) return EQO_EB;                        /* clipping.py:158-159 */
     if (!(0.0 < r && r <= 1.0)) return EQO_ER;       /* clipping.py:160-161 */
     if (d <= 0) return EQO_EEMPTY;                   /* clipping.py:162 */
@@ -292,6 +346,12 @@ int eqo_clip_range_greedy(const float *x, long d, int nbits, int b, double r,
         if (rc) return rc;
         rc = eqo_quant_mse(x, d, rmin, rmax, nbits, scratch, &loss_r);   /* :184 */
         if (rc) return rc;
+        if (gap_lr) {
+            const double g1 = rel_gap(loss_l, loss_r);
+            const double g2 = rel_gap(loss_l < loss_r ? loss_l : loss_r, best_loss);
+            if (g1 < *gap_lr) *gap_lr = g1;
+            if (g2 < *gap_best) *gap_best = g2;
+        }
         if (loss_l < loss_r) {                                           /* :185 */
             nl += 1;
             if (loss_l < best_loss) {
@@ -577,9 +637,31 @@ int eqo_pack_table4(const uint8_t *codes, long rows, long d, int aux, const void
  *   info0/info1  greedy: iterations / -; hist-brute: start_bin / nbins_selected
  *   norm       hist-brute window norm
  * Returns the first error code over rows (rows are independent). */
+static int table_impl(const float *x, long rows, long d, long ld, int method, int b, double r,
+                      int aux, uint8_t *packed, double *lo_out, double *hi_out, int32_t *info0,
+                      int32_t *info1, double *norm_out, double *gap_lr, double *gap_best,
+                      int nthreads);
+
 int eqo_quantize_pack_table(const float *x, long rows, long d, long ld, int method, int b,
                             double r, int aux, uint8_t *packed, double *lo_out, double *hi_out,
                             int32_t *info0, int32_t *info1, double *norm_out, int nthreads) {
+    return table_impl(x, rows, d, ld, method, b, r, aux, packed, lo_out, hi_out, info0, info1,
+                      norm_out, NULL, NULL, nthreads);
+}
+
+/* Same, plus GREEDY's per-row smallest near-tie gaps (greedy_impl) -- the parity report. */
+int eqo_quantize_pack_table_gaps(const float *x, long rows, long d, long ld, int method, int b,
+                                 double r, int aux, uint8_t *packed, double *lo_out,
+                                 double *hi_out, int32_t *info0, int32_t *info1, double *norm_out,
+                                 double *gap_lr, double *gap_best, int nthreads) {
+    return table_impl(x, rows, d, ld, method, b, r, aux, packed, lo_out, hi_out, info0, info1,
+                      norm_out, gap_lr, gap_best, nthreads);
+}
+
+static int table_impl(const float *x, long rows, long d, long ld, int method, int b, double r,
+                      int aux, uint8_t *packed, double *lo_out, double *hi_out, int32_t *info0,
+                      int32_t *info1, double *norm_out, double *gap_lr, double *gap_best,
+                      int nthreads) {
     if (rows < 1 || d < 1) return EQO_EEMPTY;
     if (method < 0 || method > 7) return EQO_EMETHOD;
     if (method == METHOD_GREEDY) {
@@ -629,8 +711,12 @@ int eqo_quantize_pack_table(const float *x, long rows, long d, long ld, int meth
                     rc = eqo_clip_range_asym(row, d, &lo, &hi);
                 } else if (method == METHOD_GREEDY) {
                     int bi, bj;
-                    rc = eqo_clip_range_greedy(row, d, 4, b, r, &lo, &hi, &a0, &bi, &bj, scratch);
+                    double g1 = INFINITY, g2 = INFINITY;
+                    rc = greedy_impl(row, d, 4, b, r, &lo, &hi, &a0, &bi, &bj, scratch,
+                                     gap_lr ? &g1 : NULL, gap_best ? &g2 : NULL);
                     a1 = bi;
+                    if (gap_lr) gap_lr[i] = g1;
+                    if (gap_best) gap_best[i] = g2;
                 } else if (method == METHOD_HIST_BRUTE) {
                     long ce = 0, bv = 0;
                     rc = eqo_hist_brute(row, d, b, &lo, &hi, &a0, &a1, &nv, &ce, &bv, scratch);

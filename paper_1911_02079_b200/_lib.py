@@ -45,6 +45,7 @@ EXPORTS = (
     "eq4_quantize_file",
     "eq4_write_embq",
     "eq4_selftest",
+    "eq4_diag_counters",
 )
 
 _lib = None
@@ -98,6 +99,8 @@ def load() -> ctypes.CDLL:
         L.eq4_write_embq.restype = i32
         L.eq4_selftest.argtypes = [i32, i64, ctypes.c_uint64]
         L.eq4_selftest.restype = ctypes.c_longlong
+        L.eq4_diag_counters.argtypes = [vp, i32]
+        L.eq4_diag_counters.restype = i32
         _lib = L
     return _lib
 
@@ -118,3 +121,13 @@ def check(rc: int) -> None:
 
 def packed_row_stride(dim: int, aux: str) -> int:
     return int(load().eq4_packed_row_stride(int(dim), AUX[aux]))
+
+
+def diag_counters(reset: bool = False) -> dict:
+    """GREEDY rare-path counters of the current device (eq4_diag_counters)."""
+    import numpy as np
+
+    out = np.zeros(4, np.int64)
+    check(load().eq4_diag_counters(out.ctypes.data_as(ctypes.c_void_p), int(bool(reset))))
+    return {"exact_redecisions": int(out[0]), "exact_code_rows": int(out[1]),
+            "near_count_checks": int(out[2]), "near_count_escalations": int(out[3])}

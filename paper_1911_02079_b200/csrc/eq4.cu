@@ -72,6 +72,14 @@ enum { M_ASYM = 0, M_GREEDY = 1 };
 #define G_MINB64 3   // 170 registers: the phase-A loop state stays out of local memory
 #endif
 
+// Diagnostic counters of the GREEDY kernel's rare paths (read by eq4_diag_counters):
+// [0] rows re-decided with the float64 restatement (one per row and iteration),
+// [1] rows whose codes came from the float64 codec (an element near a rounding
+// boundary), [2] comparisons resolved by counting near-boundary elements
+// (near_escalate), [3] of those, escalated to the exact re-decision (more than
+// 2 elements of a side within reach of a boundary).  Only the rare paths touch them.
+__device__ unsigned long long g_diag[4];
+
 struct Params {
   const float* x;
   int64_t rows;
@@ -97,7 +105,8 @@ struct Params {
   double qY, inv_qY;  // Y grid quantum and inverse
   float delta;        // qY / 2
   float tau2;         // relative band coefficient, both sides (incl. reference grid rounding)
-  float kmis;         // misround band per W^2, both sides
+  float kmis;         // misround band per W^2, both sides (<= 2 misrounded elements per side)
+  float kmisx;        // extra band per W^2 when every element of a side may misround
   float c1;           // Yh quantisation band: 4.2 * delta * sqrt(d)
   float c0;           // 2.1 * d * delta^2
 };
@@ -923,6 +932,7 @@ __device__ __forceinline__ void emit_greedy(const Params& p, const float4* ys4, 
   if (!rvalid) near = false;
   if (__any_sync(FULL, near)) {   // rare: float64 codec (uniform.py:77-79) for the whole slice
     if (near) {
+      if (fast && q == 0) atomicAdd(&g_diag[1], 1ull);
       const CodeParams cp = make_code_params(lo, hi);
       for (int c = 0; c < E / 4; ++c) {
         uint32_t w = 0;
@@ -951,6 +961,62 @@ __device__ __forceinline__ void emit_greedy(const Params& p, const float4* ys4, 
   }
 }
 
+// Elements of group g's row whose code under candidate (B, W) lies within nb of
+// a rounding boundary (code argument alpha*s within nb of an integer, strictly
+// inside the clamp range), computed with the search's own arithmetic.  Only
+// those elements can take a different code in the fp32 loss than in the
+// reference's, each moving the loss by <= 2 eta W^2.
+// Warp-cooperative over the row's LPR columns of the slice; every lane
+// returns the count.
+template <int LPR, int E, bool VEC>
+__device__ __noinline__ int near_count(const float* ysf, int g, int d, float B, float W, float nb) {
+  const int lane = threadIdx.x & 31;
+  const float kW = rcp_approx(W * ALPHA), h = 0.5f / ALPHA;
+  int cnt = 0;
+  for (int t = lane; t < LPR * E; t += 32) {
+    const int q = t % LPR, i = t / LPR;
+    if (!VEC && i >= valid_slots<LPR, E, VEC>(q, d)) continue;
+    const float z = __fadd_rn(ysf[((i >> 2) * 32 + g * LPR + q) * 4 + (i & 3)], -B);
+    const float sv = sat_fma(z, kW, h);
+    const float m = __fadd_rn(__fmaf_rd(sv, ALPHA, MAGIC), -MAGIC);
+    const float fr = __fmaf_rn(sv, ALPHA, -m);
+    cnt += (sv > 0.f && sv < 1.f && fabsf(fr - 0.5f) > 0.5f - nb) ? 1 : 0;
+  }
+  return __reduce_add_sync(FULL, cnt);
+}
+
+// Rows whose fast comparison lies outside the error band for <= 2 misrounded
+// elements per side but inside the band for d of them (chk) are resolved by
+// counting the elements that can misround for the candidates involved: more
+// than 2 on any side sends the row to the exact re-decision.  Rows one at a
+// time, the whole warp counting (like exact_block); returns the lane's row's
+// escalation.
+template <int LPR, int E, bool VEC>
+__device__ __forceinline__ bool near_escalate(const Params& p, const float* ysf, bool chk, int q, int gw,
+                                              int d, float BL, float W, int bi, int bj) {
+  unsigned bal = __ballot_sync(FULL, chk && q == 0);
+  bool esc = false;
+  while (bal) {
+    const int leader = __ffs(bal) - 1;
+    bal &= bal - 1;
+    const int lg = leader / LPR;
+    const float bl = __shfl_sync(FULL, BL, leader);
+    const int ri = __shfl_sync(FULL, bi, leader), rj = __shfl_sync(FULL, bj, leader);
+    const float nb = NEAR + p.delta / W;
+    const int cL = near_count<LPR, E, VEC>(ysf, lg, d, bl, W, nb);
+    const int cR = near_count<LPR, E, VEC>(ysf, lg, d, bl - 15.f, W, nb);
+    const float Wb = (float)(p.b - ri - rj);
+    const int cB = near_count<LPR, E, VEC>(ysf, lg, d, (float)(15 * ri), Wb, NEAR + p.delta / Wb);
+    const bool e = cL > 2 || cR > 2 || cB > 2;
+    if (lg == gw) esc = e;
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&g_diag[2], 1ull);
+      if (e) atomicAdd(&g_diag[3], 1ull);
+    }
+  }
+  return esc;
+}
+
 enum : unsigned { F_ACTIVE = 1, F_EXACT_ONLY = 2, F_BEST_EX = 4, F_ERR = 8 };
 
 // The rare path of one loop iteration: rows flagged need_ex are re-decided one
@@ -967,6 +1033,7 @@ __device__ __forceinline__ void exact_block(const Params& p, bool need_ex, int q
     const int leader = __ffs(bal) - 1;
     bal &= bal - 1;
     const int lg = leader / LPR;
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_diag[0], 1ull);
     const ExactOut o = exact_decide<(E <= 16)>(
         &rs[lg], (double)__shfl_sync(FULL, nl, leader), (double)__shfl_sync(FULL, nr, leader),
         __shfl_sync(FULL, bi, leader), __shfl_sync(FULL, bj, leader),
@@ -1141,7 +1208,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
     // the hot loop's registers are not shaped by the calls it makes.
     const int itA = __any_sync(FULL, flags & F_EXACT_ONLY) ? 0 : min(p.it_exact_from, p.b - 1);
     while (it < itA) {
-      bool need_ex = false, goL = false;
+      bool need_ex = false, goL = false, chk = false;
       float SL = 0.f, SR = 0.f, cand = 0.f;
       for (; it < itA; ++it) {
         const float Wf = (float)(p.b - it - 1);
@@ -1159,8 +1226,10 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         cand = goL ? SL : SR;
         const float mall = fmaxf(fmaxf(SL, SR), Lbest);
         const float band = p.tau2 * mall + p.c1 * sqrt_approx(mall) + (p.c0 + p.kmis * Wf * Wf);
-        need_ex = (flags & F_ACTIVE) && (fabsf(SL - SR) <= band || fabsf(cand - Lbest) <= band);
-        if (__any_sync(FULL, need_ex)) break;
+        const float gap = fminf(fabsf(SL - SR), fabsf(cand - Lbest));
+        need_ex = (flags & F_ACTIVE) && gap <= band;
+        chk = (flags & F_ACTIVE) && !need_ex && gap <= __fmaf_rn(p.kmisx * Wf, Wf, band);
+        if (__any_sync(FULL, need_ex || chk)) break;
         const bool upd = (flags & F_ACTIVE) != 0;
         const bool mvL = upd && goL;
         nl += mvL;
@@ -1174,6 +1243,9 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         iters += upd;
       }
       if (it >= itA) break;
+      if (__any_sync(FULL, chk))
+        need_ex |= near_escalate<LPR, E, VEC>(p, reinterpret_cast<const float*>(ys4), chk, q, gw, d, BLf,
+                                              (float)(p.b - it - 1), bi, bj);
       // iteration `it` has rows to re-decide exactly; the others apply the fast decision
       const bool upd = (flags & F_ACTIVE) && !need_ex;
       if (upd) {
@@ -1209,8 +1281,12 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         const float cand = goL ? SL : SR;
         const float mall = fmaxf(fmaxf(SL, SR), Lbest);
         const float band = p.tau2 * mall + p.c1 * sqrt_approx(mall) + (p.c0 + p.kmis * Wf * Wf);
-        need_ex = (flags & F_ACTIVE) &&
-                  ((flags & F_EXACT_ONLY) || fabsf(SL - SR) <= band || fabsf(cand - Lbest) <= band);
+        const float gap = fminf(fabsf(SL - SR), fabsf(cand - Lbest));
+        need_ex = (flags & F_ACTIVE) && ((flags & F_EXACT_ONLY) || gap <= band);
+        const bool chk = (flags & F_ACTIVE) && !need_ex && gap <= __fmaf_rn(p.kmisx * Wf, Wf, band);
+        if (__any_sync(FULL, chk))
+          need_ex |= near_escalate<LPR, E, VEC>(p, reinterpret_cast<const float*>(ys4), chk, q, gw, d, BLf,
+                                                Wf, bi, bj);
         if ((flags & F_ACTIVE) && !need_ex) {
           if (goL) { ++nl; BLf += 15.f; } else { ++nr; }
           if (cand < Lbest) {
@@ -1992,6 +2068,10 @@ static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t
     // boundary, each adding <= 2*eta*W^2 to the loss; allow 2 per side, both
     // sides.
     p.kmis = (float)(2.0 * 2.0 * 2.0 * 4.0 * 5.9604645e-8 * 15.75);
+    // ... and when more than 2 elements of a side could misround (repeated values
+    // parked next to a boundary), the comparison is only trusted after counting
+    // them (near_escalate): up to all d elements per side
+    p.kmisx = p.kmis * (float)std::max<int64_t>(0, dim - 2) * 0.5f;
     // rows with max|x| <= 1e6 (max - min) (others run exact_only): the
     // reference's rounded grid moves its losses by <= 3e-14 * 1e6 relative
     p.tau2 += (float)(2.0 * 3e-14 * 1e6);
@@ -2182,6 +2262,20 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
   if (tkeys) cudaFreeAsync(tkeys, st[0]);
   for (int i = 0; i < NS; i++) cudaStreamSynchronize(st[i]);
   return rc;
+}
+
+// Diagnostics: the GREEDY rare-path counters (g_diag) of the current device;
+// reset != 0 zeroes them after the read.  Synchronous.
+int eq4_diag_counters(int64_t* out, int reset) {
+  unsigned long long h[4] = {0, 0, 0, 0};
+  cudaError_t e = cudaMemcpyFromSymbol(h, g_diag, sizeof h);
+  if (e == cudaSuccess && reset) {
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_diag, z, sizeof z);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "diag counters");
+  for (int i = 0; i < 4; i++) out[i] = (int64_t)h[i];
+  return EQ4_OK;
 }
 
 // Diagnostics: run an internal arithmetic self-test on the current device and

@@ -40,17 +40,19 @@ __device__ __forceinline__ double div15(double w) {
 // bias the row is packed with.  numpy's AVX-512 reduction (restated op by op in
 // oracle/eq4_oracle.c np_reduce_ext) makes the choice a fixed priority over
 // positions p of the row (d elements), the same for min and max:
-//   x[0] lowest; p in 1 .. 8*nv (nv = (d-1)/8 full vectors) by vector lane
-//   k = (p-1) % 8 in the order 1 > 5 > 3 > 7 > 0 > 4 > 2 > 6 (the _mm512_reduce
-//   tree), the later p within a lane; above all the scalar tail p > 8*nv, the
-//   later the higher.  np_zero_key is 0 for a non-zero element, else a key
-//   whose maximum over the row's zeros carries the winner's sign in bit 0.
+//   p in 1 .. 8*nv (nv = (d-1)/8 full vectors) by vector lane k = (p-1) % 8 in
+//   the order 1 > 5 > 3 > 7 > 0 > 4 > 2 > 6 (the _mm512_reduce tree), the later
+//   p within a lane; above all the scalar tail p > 8*nv, the later the higher.
+//   x[0] seeds every lane's accumulator, so a zero x[0] stands in lane 1 (the
+//   top lane) below lane 1's own elements; with no full vector it is lowest.
+//   np_zero_key is 0 for a non-zero element, else a key whose maximum over the
+//   row's zeros carries the winner's sign in bit 0.
 __device__ __forceinline__ unsigned np_zero_key(float v, int p, int d) {
   if (v != 0.f) return 0u;
   const int nv8 = (d - 1) >> 3;
   unsigned prio;
   if (p == 0) {
-    prio = 1u;
+    prio = nv8 >= 1 ? (8u << 24) + 1u : 1u;
   } else if (p > 8 * nv8) {
     prio = (1u << 29) + (unsigned)p;
   } else {
