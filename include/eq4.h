@@ -181,6 +181,43 @@ int64_t eq4_kmeans_row_stride(int64_t dim, int aux);
 int eq4_kmeans_rows(const float *x, int64_t rows, int64_t dim, int64_t ld, int aux, uint8_t *out,
                     int32_t *iters, int32_t *status, void *stream);
 
+/*
+ * Standalone codec and histogram entry points (device pointers, stream-ordered).
+ * x_is_f64 != 0: the rows are float64 (the reference promotes any input to
+ * float64, uniform.py:72 / histclip.py:56 / table.py:94); else float32.
+ *
+ * uniform.py:60-80 quantize_uniform per row / uniform.py:142-167
+ * quantize_table_uniform: codes [rows x dim] (one byte per code, 0..2^nbits-1)
+ * of each row against the float64 range (xmin[i*range_stride],
+ * xmax[i*range_stride]) -- range_stride 0 applies one range to every row --
+ * with scales/biases [rows] written as aux-width bit patterns.  The ranges
+ * must be valid ClipRanges (finite, xmin <= xmax; table.py:70-74).  nbits 4 or 8.
+ */
+int eq4_quantize_rows(const void *x, int x_is_f64, int64_t rows, int64_t dim, int64_t ld,
+                      const double *xmin, const double *xmax, int64_t range_stride, int nbits, int aux,
+                      uint8_t *codes, void *scales, void *biases, void *stream);
+
+/* uniform.py:83-91 dequantize_uniform: out = float32(scale) * float32(code) + float32(bias),
+ * two rounded float32 operations per element. */
+int eq4_dequantize_rows(const uint8_t *codes, int64_t rows, int64_t dim, const void *scales,
+                        const void *biases, int aux, float *out, void *stream);
+
+/* histclip.py:52-67 build_histogram of every row: lo/hi [rows] = np.min / np.max (numpy's
+ * choice among equal extrema included), counts [rows x b] int64 (bins of width
+ * (hi - lo)/b, index clip(floor((x - lo)/w), 0, b-1); a constant row puts d in bin 0). */
+int eq4_build_histogram(const void *x, int x_is_f64, int64_t rows, int64_t dim, int64_t ld, int b,
+                        double *lo, double *hi, int64_t *counts, void *stream);
+
+/* histclip.py:70-82 bin_l2_norm elementwise: density * (de**3 - db**3) / 3.0 with each cube
+ * rounded once (numpy's power may differ in the last bit: host SIMD pow). */
+int eq4_bin_l2_norm(const double *delta_begin, const double *delta_end, const double *density,
+                    int64_t n, double *out, void *stream);
+
+/* table.py:81-103 quant_mse per row for nbits 4 or 8 and float32 or float64 rows (one
+ * lane per row, numpy pairwise sum, bit-exact). */
+int eq4_quant_mse_rows(const void *x, int x_is_f64, int64_t rows, int64_t dim, int64_t ld,
+                       const double *xmin, const double *xmax, int nbits, double *out, void *stream);
+
 /* Diagnostics: counters of the GREEDY kernel's rare paths on the current device,
  * accumulated over launches since the last reset: out[0] = float64 re-decisions
  * (one per row and loop iteration whose fp32 comparison fell inside the error

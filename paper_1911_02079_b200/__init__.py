@@ -38,6 +38,9 @@ from .api import (  # noqa: F401
     quantize_table,
     row_clip_range,
 )
+from .codec import (Histogram, UniformRowQuant, bin_l2_norm, build_histogram,  # noqa: F401
+                    dequantize_uniform, quantize_table_uniform, quantize_uniform, unpack_row,
+                    unpack_row_codes)
 from .codebook import (CodebookQuantTable, CodebookRowQuant, quantize_row_kmeans,  # noqa: F401
                        quantize_table_kmeans)
 from .pooled import PooledQuery, bytes_per_pooled_row, sparse_lengths_sum_4bit  # noqa: F401

@@ -46,6 +46,11 @@ EXPORTS = (
     "eq4_write_embq",
     "eq4_selftest",
     "eq4_diag_counters",
+    "eq4_quantize_rows",
+    "eq4_dequantize_rows",
+    "eq4_build_histogram",
+    "eq4_bin_l2_norm",
+    "eq4_quant_mse_rows",
 )
 
 _lib = None
@@ -101,6 +106,16 @@ def load() -> ctypes.CDLL:
         L.eq4_selftest.restype = ctypes.c_longlong
         L.eq4_diag_counters.argtypes = [vp, i32]
         L.eq4_diag_counters.restype = i32
+        L.eq4_quantize_rows.argtypes = [vp, i32, i64, i64, i64, vp, vp, i64, i32, i32, vp, vp, vp, vp]
+        L.eq4_quantize_rows.restype = i32
+        L.eq4_dequantize_rows.argtypes = [vp, i64, i64, vp, vp, i32, vp, vp]
+        L.eq4_dequantize_rows.restype = i32
+        L.eq4_build_histogram.argtypes = [vp, i32, i64, i64, i64, i32, vp, vp, vp, vp]
+        L.eq4_build_histogram.restype = i32
+        L.eq4_bin_l2_norm.argtypes = [vp, vp, vp, i64, vp, vp]
+        L.eq4_bin_l2_norm.restype = i32
+        L.eq4_quant_mse_rows.argtypes = [vp, i32, i64, i64, i64, vp, vp, i32, vp, vp]
+        L.eq4_quant_mse_rows.restype = i32
         _lib = L
     return _lib
 

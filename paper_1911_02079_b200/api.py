@@ -53,6 +53,26 @@ def _is_cuda(x) -> bool:
     return torch is not None and isinstance(x, torch.Tensor) and x.is_cuda
 
 
+def _rows_on_device(x):
+    """(device tensor rows x d, is_f64) of an array-like promoted like np.asarray(x, float64).
+
+    float32 inputs (EmbeddingTable rows, float32 arrays/tensors) stay float32 -- promoting
+    them to float64 is exact; anything else becomes a float64 tensor."""
+    if isinstance(x, EmbeddingTable):
+        x = x.device_values if x.on_device else x.values
+    if _is_cuda(x):
+        t = x if x.dtype in (torch.float32, torch.float64) else x.double()
+    else:
+        a = np.asarray(x)
+        if a.dtype != np.float32:
+            a = np.asarray(x, dtype=np.float64)
+        t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    if t.dim() == 1:
+        t = t.reshape(1, -1)
+    t = t.contiguous()
+    return t, t.dtype == torch.float64
+
+
 # ---------------------------------------------------------------------------
 # containers (table.py)
 # ---------------------------------------------------------------------------
@@ -645,12 +665,18 @@ def quant_mse_rows(x, xmin, xmax):
 
 
 def quant_mse(x, clip_range: ClipRange, nbits: int) -> float:
-    """table.py:81-103 (4-bit on the GPU)."""
+    """table.py:81-103 on the GPU (eq4_quant_mse_rows): float32 or float64 values, nbits 4
+    or 8, numpy's pairwise float64 sum -- bit-exact."""
     if nbits not in (4, 8):
         raise ValueError(f"nbits must be 4 or 8, got {nbits}")
-    if nbits != 4:
-        raise ValueError("nbits=8 is not on the B200 hot path (4-bit only)")
-    row = _one_row(x)
-    if not _is_cuda(row):
-        row = torch.from_numpy(np.ascontiguousarray(row)).cuda()
-    return float(quant_mse_rows(row, [clip_range.xmin], [clip_range.xmax])[0].item())
+    flat = x.reshape(-1) if _is_cuda(x) else np.asarray(x).reshape(-1)
+    n = int(flat.numel() if _is_cuda(x) else flat.size)
+    if n == 0:
+        return 0.0   # np.sum of an empty array
+    t, f64 = _rows_on_device(flat)
+    lo = torch.tensor([float(clip_range.xmin)], dtype=torch.float64, device=t.device)
+    hi = torch.tensor([float(clip_range.xmax)], dtype=torch.float64, device=t.device)
+    out = torch.empty(1, dtype=torch.float64, device=t.device)
+    _lib.check(_lib.load().eq4_quant_mse_rows(_vp(t), int(f64), 1, n, n, _vp(lo), _vp(hi), int(nbits),
+                                              _vp(out), _stream_handle()))
+    return float(out.item())

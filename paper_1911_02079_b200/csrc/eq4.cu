@@ -2072,6 +2072,7 @@ static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t
     // parked next to a boundary), the comparison is only trusted after counting
     // them (near_escalate): up to all d elements per side
     p.kmisx = p.kmis * (float)std::max<int64_t>(0, dim - 2) * 0.5f;
+    if (const char* ev = getenv("EQ4_DEV_KMISX_SCALE")) p.kmisx *= (float)atof(ev);   // development A/B only
     // rows with max|x| <= 1e6 (max - min) (others run exact_only): the
     // reference's rounded grid moves its losses by <= 3e-14 * 1e6 relative
     p.tau2 += (float)(2.0 * 3e-14 * 1e6);
@@ -2262,6 +2263,62 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
   if (tkeys) cudaFreeAsync(tkeys, st[0]);
   for (int i = 0; i < NS; i++) cudaStreamSynchronize(st[i]);
   return rc;
+}
+
+int eq4_quantize_rows(const void* x, int x_is_f64, int64_t rows, int64_t dim, int64_t ld,
+                      const double* xmin, const double* xmax, int64_t range_stride, int nbits, int aux,
+                      uint8_t* codes, void* scales, void* biases, void* stream) {
+  if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "table must be at least 1x1");
+  if (ld < dim) return fail(EQ4_EINVAL, "ld must be >= dim");
+  if (nbits != 4 && nbits != 8) return fail(EQ4_EINVAL, "nbits must be 4 or 8, got " + std::to_string(nbits));
+  if (aux != EQ4_AUX_FP16 && aux != EQ4_AUX_FP32) return fail(EQ4_EINVAL, "aux must be fp32 or fp16");
+  if (range_stride < 0) return fail(EQ4_EINVAL, "range_stride must be >= 0");
+  if (!x || !xmin || !xmax || !codes || !scales || !biases) return fail(EQ4_EINVAL, "null buffer");
+  std::string err;
+  const int rc = eq4_codec_quantize_rows(x, x_is_f64, rows, dim, ld, xmin, xmax, range_stride, nbits, aux,
+                                         codes, scales, biases, (cudaStream_t)stream, err);
+  return rc == EQ4_OK ? rc : fail(rc, err);
+}
+
+int eq4_dequantize_rows(const uint8_t* codes, int64_t rows, int64_t dim, const void* scales,
+                        const void* biases, int aux, float* out, void* stream) {
+  if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "table must be at least 1x1");
+  if (aux != EQ4_AUX_FP16 && aux != EQ4_AUX_FP32) return fail(EQ4_EINVAL, "aux must be fp32 or fp16");
+  if (!codes || !scales || !biases || !out) return fail(EQ4_EINVAL, "null buffer");
+  std::string err;
+  const int rc = eq4_codec_dequantize_rows(codes, rows, dim, scales, biases, aux, out, (cudaStream_t)stream, err);
+  return rc == EQ4_OK ? rc : fail(rc, err);
+}
+
+int eq4_build_histogram(const void* x, int x_is_f64, int64_t rows, int64_t dim, int64_t ld, int b,
+                        double* lo, double* hi, int64_t* counts, void* stream) {
+  if (b < 1) return fail(EQ4_EINVAL, "b must be >= 1, got " + std::to_string(b));   // histclip.py:54-55
+  if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "input vector is empty");          // histclip.py:57-58
+  if (ld < dim) return fail(EQ4_EINVAL, "ld must be >= dim");
+  if (!x || !lo || !hi || !counts) return fail(EQ4_EINVAL, "null buffer");
+  std::string err;
+  const int rc = eq4_codec_build_histogram(x, x_is_f64, rows, dim, ld, b, lo, hi, counts, (cudaStream_t)stream, err);
+  return rc == EQ4_OK ? rc : fail(rc, err);
+}
+
+int eq4_bin_l2_norm(const double* delta_begin, const double* delta_end, const double* density, int64_t n,
+                    double* out, void* stream) {
+  if (n < 0) return fail(EQ4_EINVAL, "n must be >= 0");
+  if (n == 0) return EQ4_OK;
+  if (!delta_begin || !delta_end || !density || !out) return fail(EQ4_EINVAL, "null buffer");
+  std::string err;
+  const int rc = eq4_codec_bin_l2_norm(delta_begin, delta_end, density, n, out, (cudaStream_t)stream, err);
+  return rc == EQ4_OK ? rc : fail(rc, err);
+}
+
+int eq4_quant_mse_rows(const void* x, int x_is_f64, int64_t rows, int64_t dim, int64_t ld,
+                       const double* xmin, const double* xmax, int nbits, double* out, void* stream) {
+  if (nbits != 4 && nbits != 8) return fail(EQ4_EINVAL, "nbits must be 4 or 8, got " + std::to_string(nbits));
+  if (rows < 1 || dim < 1 || ld < dim) return fail(EQ4_EINVAL, "bad shape");
+  if (!x || !xmin || !xmax || !out) return fail(EQ4_EINVAL, "null buffer");
+  std::string err;
+  const int rc = eq4_codec_quant_mse_rows(x, x_is_f64, rows, dim, ld, xmin, xmax, nbits, out, (cudaStream_t)stream, err);
+  return rc == EQ4_OK ? rc : fail(rc, err);
 }
 
 // Diagnostics: the GREEDY rare-path counters (g_diag) of the current device;

@@ -39,3 +39,18 @@ int eq4_internal_table_accumulate(const float* x, int64_t rows, int64_t dim, int
 int eq4_internal_quantize_pack_keys(const float* x, int64_t rows, int64_t dim, int method, int b,
                                     double r, int aux, uint8_t* packed, int32_t* info0,
                                     int32_t* status, cudaStream_t s, const int* keys);
+
+// Standalone codec / histogram helpers (eq4_codec.cu).  x_f64: rows are float64.
+int eq4_codec_quantize_rows(const void* x, int x_f64, int64_t rows, int64_t dim, int64_t ld,
+                            const double* xmin, const double* xmax, int64_t range_stride, int nbits,
+                            int aux, uint8_t* codes, void* scales, void* biases, cudaStream_t s,
+                            std::string& err);
+int eq4_codec_dequantize_rows(const uint8_t* codes, int64_t rows, int64_t dim, const void* scales,
+                              const void* biases, int aux, float* out, cudaStream_t s, std::string& err);
+int eq4_codec_build_histogram(const void* x, int x_f64, int64_t rows, int64_t dim, int64_t ld, int b,
+                              double* lo, double* hi, int64_t* counts, cudaStream_t s, std::string& err);
+int eq4_codec_bin_l2_norm(const double* db, const double* de, const double* rho, int64_t n, double* out,
+                          cudaStream_t s, std::string& err);
+int eq4_codec_quant_mse_rows(const void* x, int x_f64, int64_t rows, int64_t dim, int64_t ld,
+                             const double* xmin, const double* xmax, int nbits, double* out,
+                             cudaStream_t s, std::string& err);
