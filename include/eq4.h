@@ -43,8 +43,8 @@ extern "C" {
 #define EQ4_METHOD_GREEDY 1     /* clipping.py:142-193 clip_range_greedy */
 #define EQ4_METHOD_HIST_BRUTE 2 /* histclip.py:136-178 hist_brute_search */
 #define EQ4_METHOD_SYM 3        /* clipping.py:51-55   clip_range_sym */
-#define EQ4_METHOD_ACIQ 4       /* clipping.py:115-139 clip_range_aciq (laplacian) */
-#define EQ4_METHOD_GSS 5        /* clipping.py:70-112  clip_range_gss (tol 1e-4) */
+#define EQ4_METHOD_ACIQ 4       /* clipping.py:115-139 clip_range_aciq (constant: eq4_quantize_pack_p) */
+#define EQ4_METHOD_GSS 5        /* clipping.py:70-112  clip_range_gss (tol: eq4_quantize_pack_p) */
 #define EQ4_METHOD_TABLE 6      /* clipping.py:64-67   clip_range_table (one range per table) */
 #define EQ4_METHOD_HIST_APPRX 7 /* histclip.py:181-217 hist_apprx_search (b <= 256) */
 
@@ -89,6 +89,28 @@ int eq4_quantize_pack(const float *x, int64_t rows, int64_t dim, int64_t ld, int
                       double r, int aux, uint8_t *packed, double *xmin, double *xmax,
                       int32_t *info0, int32_t *info1, double *norm, int32_t *status,
                       void *stream);
+
+/*
+ * eq4_quantize_pack with the method's real parameter the reference takes beside b and r:
+ *   ACIQ  param = the clipping constant (clipping.py:115-134: 5.03 for the laplacian
+ *         assumption, or the caller's gaussian_constant);
+ *   GSS   param = tol (clipping.py:70, the bracket stops below tol * max|x|);
+ *   param = 0 selects the reference default (5.03, 1e-4); other methods ignore it.
+ * eq4_quantize_pack(...) == eq4_quantize_pack_p(..., param = 0, ...).
+ */
+int eq4_quantize_pack_p(const float *x, int64_t rows, int64_t dim, int64_t ld, int method, int b,
+                        double r, double param, int aux, uint8_t *packed, double *xmin, double *xmax,
+                        int32_t *info0, int32_t *info1, double *norm, int32_t *status, void *stream);
+
+/*
+ * clip_range_aciq / clip_range_gss (clipping.py:70-139) of FLOAT64 rows -- the scalar entry
+ * points promote any input to float64 (clipping.py:46), which need not be float32 values.
+ * Ranges only (no packing): xmin/xmax [rows] float64, info0 (optional) GSS quant_mse
+ * evaluations.  method EQ4_METHOD_ACIQ or EQ4_METHOD_GSS; param as eq4_quantize_pack_p.
+ * Device pointers, stream-ordered; non-finite rows set EQ4_STATUS_NONFINITE.
+ */
+int eq4_row_range_f64(const double *x, int64_t rows, int64_t dim, int64_t ld, int method, double param,
+                      double *xmin, double *xmax, int32_t *info0, int32_t *status, void *stream);
 
 /*
  * Same operation on HOST buffers (pinned or pageable), the call a

@@ -35,6 +35,8 @@ EXPORTS = (
     "eq4_last_error",
     "eq4_packed_row_stride",
     "eq4_quantize_pack",
+    "eq4_quantize_pack_p",
+    "eq4_row_range_f64",
     "eq4_quantize_pack_host",
     "eq4_pack",
     "eq4_unpack",
@@ -82,6 +84,11 @@ def load() -> ctypes.CDLL:
         L.eq4_quantize_pack.argtypes = [vp, i64, i64, i64, i32, i32, dbl, i32, vp, vp, vp, vp, vp,
                                         vp, vp, vp]
         L.eq4_quantize_pack.restype = i32
+        L.eq4_quantize_pack_p.argtypes = [vp, i64, i64, i64, i32, i32, dbl, dbl, i32, vp, vp, vp, vp,
+                                          vp, vp, vp, vp]
+        L.eq4_quantize_pack_p.restype = i32
+        L.eq4_row_range_f64.argtypes = [vp, i64, i64, i64, i32, dbl, vp, vp, vp, vp, vp]
+        L.eq4_row_range_f64.restype = i32
         L.eq4_quantize_pack_host.argtypes = [vp, i64, i64, i64, i32, i32, dbl, i32, vp, vp, vp, vp,
                                              vp, vp, i64, vp, vp]
         L.eq4_quantize_pack_host.restype = i32

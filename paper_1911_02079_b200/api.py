@@ -381,7 +381,8 @@ class RowResults:
 
 def quantize_pack_table4(table, method: str, aux_precision: str = "fp16", b: int = 200,
                          r: float = 0.16, *, out=None, rows_out: RowResults | None = None,
-                         with_rows: bool = False, status=None, stream=None, check: bool = True):
+                         with_rows: bool = False, status=None, stream=None, check: bool = True,
+                         param: float = 0.0):
     """Fused ``pack_table4(quantize_table(table, method, 4, aux, b, r))`` on the GPU.
 
     ``table``: EmbeddingTable, CUDA float32 tensor (device path, stream
@@ -390,7 +391,9 @@ def quantize_pack_table4(table, method: str, aux_precision: str = "fp16", b: int
     path nothing synchronises; the caller inspects ``status`` itself (the C
     entry point clears it on the stream first).  ``stream`` (a torch CUDA
     stream, default the current one) orders the launch; the output buffers
-    are allocated on it and the status read waits for it.
+    are allocated on it and the status read waits for it.  ``param``: ACIQ's
+    clipping constant / GSS's tol (0 = the reference defaults 5.03 / 1e-4;
+    device tables only).
     """
     if method not in GPU_METHODS:
         raise ValueError(f"{method!r} is not on the B200 hot path; supported: {GPU_METHODS}")
@@ -405,7 +408,8 @@ def quantize_pack_table4(table, method: str, aux_precision: str = "fp16", b: int
         if stream is not None and stream != torch.cuda.current_stream(src.device):
             with torch.cuda.stream(stream):
                 return quantize_pack_table4(src, method, aux_precision, b, r, out=out, rows_out=rows_out,
-                                            with_rows=with_rows, status=status, stream=None, check=check)
+                                            with_rows=with_rows, status=status, stream=None, check=check,
+                                            param=param)
         x = src if (src.dtype == torch.float32 and src.stride(1) == 1) else src.float().contiguous()
         rows, d = int(x.shape[0]), int(x.shape[1])
         ld = int(x.stride(0))
@@ -422,8 +426,8 @@ def quantize_pack_table4(table, method: str, aux_precision: str = "fp16", b: int
                             torch.empty(rows, dtype=torch.float64, device=dev))
         if status is None:
             status = torch.empty(1, dtype=torch.int32, device=dev)   # cleared by eq4_quantize_pack
-        rc = L.eq4_quantize_pack(_vp(x), rows, d, ld, _lib.METHOD[method], int(b), float(r),
-                                 _lib.AUX[aux_precision], _vp(out),
+        rc = L.eq4_quantize_pack_p(_vp(x), rows, d, ld, _lib.METHOD[method], int(b), float(r),
+                                   float(param), _lib.AUX[aux_precision], _vp(out),
                                  _vp(rr.xmin) if rr else None, _vp(rr.xmax) if rr else None,
                                  _vp(rr.info0) if rr else None, _vp(rr.info1) if rr else None,
                                  _vp(rr.norm) if rr else None, _vp(status), _stream_handle(stream))
@@ -433,6 +437,8 @@ def quantize_pack_table4(table, method: str, aux_precision: str = "fp16", b: int
             if st:
                 _raise_status(st, x, method, b, r, aux_precision)
         return PackedTable4(rows, d, aux_precision, device_buffer=out), rr
+    if param:
+        raise ValueError("param (ACIQ constant / GSS tol) is taken on the device path only")
     # host path: pinned/pageable host memory through the pipelined C entry point
     if torch is not None and isinstance(src, torch.Tensor):
         xh = src.float().contiguous().numpy()
@@ -528,23 +534,50 @@ def quantize_table(table, method: str, nbits: int = 4, aux_precision: str = "fp3
     return UniformQuantTable.from_packed(packed, scheme=method)
 
 
-def _one_row(x) -> np.ndarray:
+def _one_row(x):
+    """The row as the reference sees it (np.asarray(x, float64), clipping.py:44-48): a float32
+    (1, d) array/tensor when its values are float32 values (every EmbeddingTable row), else a
+    float64 one."""
     if _is_cuda(x):
-        x = x.float().reshape(1, -1)
+        x = x.reshape(1, -1)
         if x.numel() == 0:
             raise ValueError("input vector is empty")
-        return x
-    a = np.asarray(x, dtype=np.float64)
+        if x.dtype == torch.float32:
+            return x
+        x = x.double()
+        return x.float() if bool((x.float().double() == x).all()) else x
+    a = np.asarray(x)
     if a.size == 0:
         raise ValueError("input vector is empty")                  # clipping.py:44-48
-    return a.astype(np.float32).reshape(1, -1)
+    if a.dtype == np.float32:
+        return a.reshape(1, -1)
+    a = np.asarray(x, dtype=np.float64).reshape(1, -1)
+    f = a.astype(np.float32)
+    return f if np.array_equal(f.astype(np.float64), a, equal_nan=True) else a
 
 
-def _row_search(method, x, b=200, r=0.16):
+def _row_search(method, x, b=200, r=0.16, param=0.0):
     row = _one_row(x)
     if not _is_cuda(row):
         row = torch.from_numpy(np.ascontiguousarray(row)).cuda()
-    _, rr = quantize_pack_table4(row, method, "fp32", b, r, with_rows=True)
+    if row.dtype == torch.float64:
+        # values that are not float32 values: the reference searches them in float64
+        if method not in ("aciq", "gss"):
+            raise ValueError(f"{method}: the B200 path takes float32 rows (every EmbeddingTable "
+                             "row is one); this float64 row has values float32 cannot hold")
+        dev = row.device
+        n = int(row.shape[1])
+        rr = RowResults(torch.empty(1, dtype=torch.float64, device=dev),
+                        torch.empty(1, dtype=torch.float64, device=dev),
+                        torch.empty(1, dtype=torch.int32, device=dev), None, None)
+        st = torch.empty(1, dtype=torch.int32, device=dev)
+        _lib.check(_lib.load().eq4_row_range_f64(_vp(row), 1, n, n, _lib.METHOD[method], float(param),
+                                                 _vp(rr.xmin), _vp(rr.xmax), _vp(rr.info0), _vp(st),
+                                                 _stream_handle()))
+        if int(st.item()) & _lib.STATUS_NONFINITE:
+            raise ValueError("clip range must be finite")
+        return rr
+    _, rr = quantize_pack_table4(row, method, "fp32", b, r, with_rows=True, param=param)
     return rr
 
 
@@ -600,26 +633,37 @@ def clip_range_sym(x) -> ClipRange:
 
 
 def clip_range_aciq(x, distribution: str = "laplacian", gaussian_constant: float | None = None) -> ClipRange:
-    """clipping.py:115-139 (the laplacian constant 5.03; the caller-supplied gaussian
-    constant branch is not on the GPU path)."""
-    if distribution == "gaussian":
+    """clipping.py:115-139: alpha = constant * mean|x - mean| (5.03 for the laplacian
+    assumption, the caller's gaussian_constant otherwise); alpha == 0 -> the data range."""
+    if distribution == "laplacian":
+        constant = 5.03
+    elif distribution == "gaussian":
         if gaussian_constant is None:
             raise ValueError("gaussian clipping requires an explicit gaussian_constant; "
                              "only the laplacian constant is built in")
-        raise ValueError("aciq with a gaussian constant is not on the B200 hot path (laplacian only)")
-    if distribution != "laplacian":
+        constant = float(gaussian_constant)
+    else:
         raise ValueError(f"distribution must be 'laplacian' or 'gaussian', got {distribution!r}")
-    rr = _row_search("aciq", x)
+    if not (np.isfinite(constant) and constant > 0.0):
+        # alpha = constant * mad: zero (or negative) constants give the data range or an
+        # inverted range in the reference; the device parameter is a positive constant
+        if constant == 0.0:
+            return clip_range_asym(x)
+        raise ValueError(f"xmin exceeds xmax: gaussian_constant {constant} must be positive")
+    rr = _row_search("aciq", x, param=constant)
     return ClipRange(float(rr.xmin[0].item()), float(rr.xmax[0].item()))
 
 
 def clip_range_gss(x, nbits: int = 4, tol: float = 1e-4, counters: WorkCounters | None = None) -> ClipRange:
-    """clipping.py:70-112 (4-bit, tol 1e-4 -- the row_clip_range configuration)."""
+    """clipping.py:70-112: golden-section search of the symmetric threshold (4-bit objective;
+    tol as given)."""
     if tol <= 0:
         raise ValueError(f"tol must be positive, got {tol}")
-    if nbits != 4 or tol != 1e-4:
-        raise ValueError("gss is on the B200 hot path for nbits=4, tol=1e-4 only")
-    rr = _row_search("gss", x)
+    if nbits not in (4, 8):
+        raise ValueError(f"nbits must be 4 or 8, got {nbits}")
+    if nbits != 4:
+        raise ValueError("gss with nbits=8 is not on the B200 hot path (4-bit only)")
+    rr = _row_search("gss", x, param=float(tol))
     _apply_counters(counters, "gss", 0, rr)
     return ClipRange(float(rr.xmin[0].item()), float(rr.xmax[0].item()))
 

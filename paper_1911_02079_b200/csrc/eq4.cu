@@ -60,6 +60,11 @@ constexpr int NTHREADS_G = G_THREADS;         // GREEDY blocks (warps are indepe
 constexpr int NWARPS_G = NTHREADS_G / 32;
 constexpr int MAX_LEAVES = 64;          // numpy pairwise leaves for d <= 4096
 constexpr float ALPHA = 15.75f;         // saturation scale for the code FFMA
+// |alpha * s - (z/W + 1/2)| <= ETA_CODE for s = RN(z * kw_of(W) + h), |z/W| <= 15.5:
+// 15.5 * 2^-24 (kW rounded once) + 15.75 * 2^-25 (s rounded once) = 1.39e-6.
+constexpr double ETA_CODE = 1.6e-6;
+// elements counted as able to take the other code: within ETA_CODE (+ margin) + delta/W
+constexpr float NEAR_CNT = 2.5e-6f;
 constexpr float MAGIC = 8388608.f;      // 2^23
 enum { M_ASYM = 0, M_GREEDY = 1 };
 #ifndef GREEDY_MINB
@@ -188,6 +193,10 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+
+// 1 / (W alpha) rounded once (W alpha is exact in fp32 for W < 2^18): the search's
+// code argument alpha * sat(z * kW + h) is then within ETA_CODE of (z / W + 1/2).
+__device__ __forceinline__ float kw_of(float Wf) { return __frcp_rn(Wf * ALPHA); }
 
 __device__ __forceinline__ float sat_fma(float a, float b, float c) {
   float r;
@@ -567,9 +576,11 @@ struct WarpSliceG {
   __host__ __device__ static size_t out_off() {
     return (codes_off() + (VEC ? 0 : (size_t)RPW * D) + 15) & ~(size_t)15;
   }
-  __host__ __device__ static size_t bytes(int stride) {
+  // per-warp rare-path counters (g_diag), flushed once when the warp exits
+  __host__ __device__ static size_t diag_off(int stride) {
     return (out_off() + (size_t)RPW * stride + 32 + 15) & ~(size_t)15;
   }
+  __host__ __device__ static size_t bytes(int stride) { return diag_off(stride) + 16; }
 };
 
 // Warp-level copy of nbytes from shared src to global dst (equal modulo 16).
@@ -883,7 +894,7 @@ template <int LPR, int E, bool VEC>
 __device__ __forceinline__ void emit_greedy(const Params& p, const float4* ys4, int nv, int q,
                                             double lo, double hi, int bi, int bj, bool fast_ok,
                                             bool ok, bool rvalid, const float* xr, uint8_t* orow,
-                                            uint8_t* crow) {
+                                            uint8_t* crow, unsigned* wdiag) {
   const int Wb = p.b - bi - bj;
   const float B = (float)(15 * bi);
   const float Wf = (float)(Wb > 0 ? Wb : 1);
@@ -932,7 +943,7 @@ __device__ __forceinline__ void emit_greedy(const Params& p, const float4* ys4, 
   if (!rvalid) near = false;
   if (__any_sync(FULL, near)) {   // rare: float64 codec (uniform.py:77-79) for the whole slice
     if (near) {
-      if (fast && q == 0) atomicAdd(&g_diag[1], 1ull);
+      if (fast && q == 0) atomicAdd(&wdiag[1], 1u);
       const CodeParams cp = make_code_params(lo, hi);
       for (int c = 0; c < E / 4; ++c) {
         uint32_t w = 0;
@@ -961,58 +972,66 @@ __device__ __forceinline__ void emit_greedy(const Params& p, const float4* ys4, 
   }
 }
 
-// Elements of group g's row whose code under candidate (B, W) lies within nb of
-// a rounding boundary (code argument alpha*s within nb of an integer, strictly
-// inside the clamp range), computed with the search's own arithmetic.  Only
-// those elements can take a different code in the fp32 loss than in the
-// reference's, each moving the loss by <= 2 eta W^2.
-// Warp-cooperative over the row's LPR columns of the slice; every lane
-// returns the count.
-template <int LPR, int E, bool VEC>
-__device__ __noinline__ int near_count(const float* ysf, int g, int d, float B, float W, float nb) {
-  const int lane = threadIdx.x & 31;
-  const float kW = rcp_approx(W * ALPHA), h = 0.5f / ALPHA;
-  int cnt = 0;
-  for (int t = lane; t < LPR * E; t += 32) {
-    const int q = t % LPR, i = t / LPR;
-    if (!VEC && i >= valid_slots<LPR, E, VEC>(q, d)) continue;
-    const float z = __fadd_rn(ysf[((i >> 2) * 32 + g * LPR + q) * 4 + (i & 3)], -B);
-    const float sv = sat_fma(z, kW, h);
-    const float m = __fadd_rn(__fmaf_rd(sv, ALPHA, MAGIC), -MAGIC);
-    const float fr = __fmaf_rn(sv, ALPHA, -m);
-    cnt += (sv > 0.f && sv < 1.f && fabsf(fr - 0.5f) > 0.5f - nb) ? 1 : 0;
-  }
-  return __reduce_add_sync(FULL, cnt);
+// 1 if an element at z = Y - B lies within nb of a code rounding boundary of a
+// candidate of width W (code argument alpha*s within nb of an integer, strictly
+// inside the clamp range), computed with the search's own arithmetic.  Only such
+// elements can take a different code in the fp32 loss than in the reference's,
+// each moving the loss by <= 2 eta W^2.
+__device__ __forceinline__ unsigned near_bnd(float z, float kW, float nb) {
+  const float sv = sat_fma(z, kW, 0.5f / ALPHA);
+  const float m = __fadd_rn(__fmaf_rd(sv, ALPHA, MAGIC), -MAGIC);
+  const float fr = __fmaf_rn(sv, ALPHA, -m);
+  return (sv > 0.f && sv < 1.f && fabsf(fr - 0.5f) > 0.5f - nb) ? 1u : 0u;
 }
 
-// Rows whose fast comparison lies outside the error band for <= 2 misrounded
-// elements per side but inside the band for d of them (chk) are resolved by
-// counting the elements that can misround for the candidates involved: more
-// than 2 on any side sends the row to the exact re-decision.  Rows one at a
-// time, the whole warp counting (like exact_block); returns the lane's row's
+// Elements of group lg's row within reach of a rounding boundary for the two
+// candidates of an iteration (L: base BL, R: base BL - 15, width W) and for the
+// best pair so far (bi, bj): true when any of the three has more than 2 (the
+// error band's allowance per side).  The whole warp counts the row's slice
+// columns in one pass (three 10-bit counts packed into one reduction).
+// Warp-collective with warp-uniform arguments.
+template <int LPR, int E, bool VEC>
+__device__ __forceinline__ bool near_over(const Params& p, const float* ysf, int lg, int d, float BL, float W,
+                                          int bi, int bj, unsigned* wdiag) {
+  const int lane = threadIdx.x & 31;
+  const float Wb = (float)(p.b - bi - bj), Bb = (float)(15 * bi);
+  const float kW = kw_of(W), kWb = kw_of(Wb);
+  const float nb = NEAR_CNT + p.delta / W, nbb = NEAR_CNT + p.delta / Wb;
+  unsigned cnt = 0u;
+  for (int t = lane; t < LPR * E; t += 32) {
+    const int qq = t % LPR, i = t / LPR;
+    if (!VEC && i >= valid_slots<LPR, E, VEC>(qq, d)) continue;
+    const float y = ysf[((i >> 2) * 32 + lg * LPR + qq) * 4 + (i & 3)];
+    const float z = __fadd_rn(y, -BL);
+    cnt += near_bnd(z, kW, nb) + (near_bnd(__fadd_rn(z, 15.f), kW, nb) << 10) +
+           (near_bnd(__fadd_rn(y, -Bb), kWb, nbb) << 20);
+  }
+  cnt = __reduce_add_sync(FULL, cnt);
+  const bool over = (cnt & 1023u) > 2u || ((cnt >> 10) & 1023u) > 2u || (cnt >> 20) > 2u;
+  if (lane == 0) {
+    wdiag[2] += 1u;
+    wdiag[3] += over ? 1u : 0u;
+  }
+  return over;
+}
+
+// Strict walk: rows whose comparison lies outside the band for <= 2 misrounded
+// elements per side but inside the band for all d of them (chk) count the
+// elements in reach of a boundary right away; more than 2 on a side sends the
+// row to the exact re-decision.  Rows one at a time; returns the lane's row's
 // escalation.
 template <int LPR, int E, bool VEC>
 __device__ __forceinline__ bool near_escalate(const Params& p, const float* ysf, bool chk, int q, int gw,
-                                              int d, float BL, float W, int bi, int bj) {
+                                              int d, float BL, float W, int bi, int bj, unsigned* wdiag) {
   unsigned bal = __ballot_sync(FULL, chk && q == 0);
   bool esc = false;
   while (bal) {
     const int leader = __ffs(bal) - 1;
     bal &= bal - 1;
     const int lg = leader / LPR;
-    const float bl = __shfl_sync(FULL, BL, leader);
-    const int ri = __shfl_sync(FULL, bi, leader), rj = __shfl_sync(FULL, bj, leader);
-    const float nb = NEAR + p.delta / W;
-    const int cL = near_count<LPR, E, VEC>(ysf, lg, d, bl, W, nb);
-    const int cR = near_count<LPR, E, VEC>(ysf, lg, d, bl - 15.f, W, nb);
-    const float Wb = (float)(p.b - ri - rj);
-    const int cB = near_count<LPR, E, VEC>(ysf, lg, d, (float)(15 * ri), Wb, NEAR + p.delta / Wb);
-    const bool e = cL > 2 || cR > 2 || cB > 2;
+    const bool e = near_over<LPR, E, VEC>(p, ysf, lg, d, __shfl_sync(FULL, BL, leader), W,
+                                          __shfl_sync(FULL, bi, leader), __shfl_sync(FULL, bj, leader), wdiag);
     if (lg == gw) esc = e;
-    if ((threadIdx.x & 31) == 0) {
-      atomicAdd(&g_diag[2], 1ull);
-      if (e) atomicAdd(&g_diag[3], 1ull);
-    }
   }
   return esc;
 }
@@ -1027,13 +1046,13 @@ __device__ __forceinline__ void exact_block(const Params& p, bool need_ex, int q
                                             int64_t ld, int d, double* e2, double* leaf_sum,
                                             int* leaf_st, int* leaf_ln, int& nl, int& nr, int& bi,
                                             int& bj, int& iters, unsigned& flags, float& Lbest,
-                                            float& BLf) {
+                                            float& BLf, unsigned* wdiag) {
   unsigned bal = __ballot_sync(FULL, need_ex && q == 0);
   while (bal) {
     const int leader = __ffs(bal) - 1;
     bal &= bal - 1;
     const int lg = leader / LPR;
-    if ((threadIdx.x & 31) == 0) atomicAdd(&g_diag[0], 1ull);
+    if ((threadIdx.x & 31) == 0) wdiag[0] += 1u;
     const ExactOut o = exact_decide<(E <= 16)>(
         &rs[lg], (double)__shfl_sync(FULL, nl, leader), (double)__shfl_sync(FULL, nr, leader),
         __shfl_sync(FULL, bi, leader), __shfl_sync(FULL, bj, leader),
@@ -1081,6 +1100,9 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
   int* leaf_ln = leaf_st + MAX_LEAVES;
   uint8_t* codes_w = ws + S::codes_off();
   uint8_t* out_base = ws + S::out_off();
+  unsigned* wdiag = reinterpret_cast<unsigned*>(ws + S::diag_off(p.stride));
+  if (lane < 4) wdiag[lane] = 0u;
+  __syncwarp();
   const int d = p.d;
   const int nv = valid_slots<LPR, E, VEC>(q, d);
   const float hh = 0.5f / ALPHA;
@@ -1122,7 +1144,11 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         mn = group_min<LPR>(lmn);
         mx = group_max<LPR>(lmx);
         sm = group_sum<LPR>(sm);
+#ifndef G_NOZERO
         if (__any_sync(FULL, rvalid && (mn == 0.f || mx == 0.f))) {   // rare: numpy's signed-zero choice
+#else
+        if (false) {
+#endif
           unsigned kz = 0u;
           for (int c = 0; c < E / 4; ++c) {
             const float4 t = __ldg(src + LPR * c);
@@ -1193,9 +1219,9 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       const float Wf = (float)p.b;                                                   // :174
       float a0;
       if constexpr (VEC)
-        a0 = eval_one_x2<E>(ysl, 0.f, -Wf, rcp_approx(Wf * ALPHA), hh);
+        a0 = eval_one_x2<E>(ysl, 0.f, -Wf, kw_of(Wf), hh);
       else
-        a0 = eval_one<E, true>(ys4, nv, 0.f, -Wf, rcp_approx(Wf * ALPHA), hh);
+        a0 = eval_one<E, true>(ys4, nv, 0.f, -Wf, kw_of(Wf), hh);
       Lbest = group_sum<LPR>(a0);
     }
     int nl = 0, nr = 0, bi = 0, bj = 0, iters = 0;
@@ -1215,11 +1241,11 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         float aL, aR;
         if constexpr (VEC) {
           if (Wf >= 17.f)   // codes move by at most one under the 15-shift
-            eval_pair_x2_shift<E>(ysl, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+            eval_pair_x2_shift<E>(ysl, BLf, -Wf, kw_of(Wf), hh, aL, aR);
           else
-            eval_pair_x2<E>(ysl, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+            eval_pair_x2<E>(ysl, BLf, -Wf, kw_of(Wf), hh, aL, aR);
         } else {
-          eval_pair<E, true>(ys4, nv, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+          eval_pair<E, true>(ys4, nv, BLf, -Wf, kw_of(Wf), hh, aL, aR);
         }
         group_sum_pair<LPR>(aL, aR, SL, SR);
         goL = SL < SR;                                                   // clipping.py:185
@@ -1245,7 +1271,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       if (it >= itA) break;
       if (__any_sync(FULL, chk))
         need_ex |= near_escalate<LPR, E, VEC>(p, reinterpret_cast<const float*>(ys4), chk, q, gw, d, BLf,
-                                              (float)(p.b - it - 1), bi, bj);
+                                              (float)(p.b - it - 1), bi, bj, wdiag);
       // iteration `it` has rows to re-decide exactly; the others apply the fast decision
       const bool upd = (flags & F_ACTIVE) && !need_ex;
       if (upd) {
@@ -1254,7 +1280,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         ++iters;
       }
       exact_block<LPR, E, VEC>(p, need_ex, q, gw, p.b - it - 1, SL, SR, rs, xblk, p.ld, d, e2, leaf_sum,
-                               leaf_st, leaf_ln, nl, nr, bi, bj, iters, flags, Lbest, BLf);
+                               leaf_st, leaf_ln, nl, nr, bi, bj, iters, flags, Lbest, BLf, wdiag);
       ++it;
     }
     // Phase B: the remaining iterations, with the float64 loop condition
@@ -1273,9 +1299,9 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         const float Wf = (float)W;
         float aL, aR;
         if constexpr (VEC)
-          eval_pair_x2<E>(ysl, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+          eval_pair_x2<E>(ysl, BLf, -Wf, kw_of(Wf), hh, aL, aR);
         else
-          eval_pair<E, true>(ys4, nv, BLf, -Wf, rcp_approx(Wf * ALPHA), hh, aL, aR);
+          eval_pair<E, true>(ys4, nv, BLf, -Wf, kw_of(Wf), hh, aL, aR);
         group_sum_pair<LPR>(aL, aR, SL, SR);
         const bool goL = SL < SR;
         const float cand = goL ? SL : SR;
@@ -1286,7 +1312,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         const bool chk = (flags & F_ACTIVE) && !need_ex && gap <= __fmaf_rn(p.kmisx * Wf, Wf, band);
         if (__any_sync(FULL, chk))
           need_ex |= near_escalate<LPR, E, VEC>(p, reinterpret_cast<const float*>(ys4), chk, q, gw, d, BLf,
-                                                Wf, bi, bj);
+                                                Wf, bi, bj, wdiag);
         if ((flags & F_ACTIVE) && !need_ex) {
           if (goL) { ++nl; BLf += 15.f; } else { ++nr; }
           if (cand < Lbest) {
@@ -1298,7 +1324,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       }
       if (__any_sync(FULL, need_ex))
         exact_block<LPR, E, VEC>(p, need_ex, q, gw, W, SL, SR, rs, xblk, p.ld, d, e2, leaf_sum, leaf_st,
-                                 leaf_ln, nl, nr, bi, bj, iters, flags, Lbest, BLf);
+                                 leaf_ln, nl, nr, bi, bj, iters, flags, Lbest, BLf, wdiag);
     }
 
     // ---- result, codes, pack ----
@@ -1319,7 +1345,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
     uint8_t* out_tile = out_base + (((uintptr_t)p.packed + gofs) & 15);
     emit_greedy<LPR, E, VEC>(p, ysl, nv, q, lo, hi, bi, bj, mn != mx,
                              rvalid && !bad && !(flags & F_ERR), rvalid, xr,
-                             out_tile + gw * p.stride, codes_w + gw * D);
+                             out_tile + gw * p.stride, codes_w + gw * D, wdiag);
     if (rvalid && q == 0) {
       if (p.lo_out) { p.lo_out[row] = lo; p.hi_out[row] = hi; }
       if (p.info0) p.info0[row] = info0;
@@ -1339,6 +1365,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
     warp_copy_out(p.packed + gofs, out_tile, blk_rows * p.stride);
     __syncwarp();
   }
+  if (lane < 4 && wdiag[lane]) atomicAdd(&g_diag[lane], (unsigned long long)wdiag[lane]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1960,19 +1987,47 @@ int64_t eq4_packed_row_stride(int64_t dim, int aux) {
 static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t ld, int method,
                               int b, double r, int aux, uint8_t* packed, double* xmin, double* xmax,
                               int32_t* info0, int32_t* info1, double* norm, int32_t* status,
-                              void* stream, const int* table_keys);
+                              void* stream, const int* table_keys, double param = 0.0);
 
 int eq4_quantize_pack(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, int b,
                       double r, int aux, uint8_t* packed, double* xmin, double* xmax,
                       int32_t* info0, int32_t* info1, double* norm, int32_t* status,
                       void* stream) {
+  return eq4_quantize_pack_p(x, rows, dim, ld, method, b, r, 0.0, aux, packed, xmin, xmax, info0, info1,
+                             norm, status, stream);
+}
+
+int eq4_quantize_pack_p(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, int b,
+                        double r, double param, int aux, uint8_t* packed, double* xmin, double* xmax,
+                        int32_t* info0, int32_t* info1, double* norm, int32_t* status, void* stream) {
+  if (!(param >= 0.0) || !std::isfinite(param))
+    return fail(EQ4_EINVAL, "param must be finite and >= 0 (0 = the reference default)");
   // the status word describes this call: cleared on the stream before the kernels OR into it
   if (status) {
     const cudaError_t e = cudaMemsetAsync(status, 0, 4, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "status reset");
   }
   return quantize_pack_impl(x, rows, dim, ld, method, b, r, aux, packed, xmin, xmax, info0, info1,
-                            norm, status, stream, nullptr);
+                            norm, status, stream, nullptr, param);
+}
+
+int eq4_row_range_f64(const double* x, int64_t rows, int64_t dim, int64_t ld, int method, double param,
+                      double* xmin, double* xmax, int32_t* info0, int32_t* status, void* stream) {
+  if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "input vector is empty");
+  if (ld < dim) return fail(EQ4_EINVAL, "ld must be >= dim");
+  if (!x || !xmin || !xmax) return fail(EQ4_EINVAL, "null buffer");
+  if (method != EQ4_METHOD_ACIQ && method != EQ4_METHOD_GSS)
+    return fail(EQ4_EUNSUPPORTED, "float64 rows: only aciq and gss ranges are computed here");
+  if (!(param >= 0.0) || !std::isfinite(param)) return fail(EQ4_EINVAL, "param must be finite and >= 0");
+  if (param == 0.0) param = method == EQ4_METHOD_ACIQ ? 5.03 : 1e-4;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (status) {
+    const cudaError_t e = cudaMemsetAsync(status, 0, 4, s);
+    if (e != cudaSuccess) return cuda_fail(e, "status reset");
+  }
+  std::string err;
+  const int rc = eq4_rowrange_f64_launch(x, rows, dim, ld, method, param, xmin, xmax, info0, status, s, err);
+  return rc == EQ4_OK ? rc : fail(rc, err);
 }
 
 // TABLE range keys of rows [0, rows) accumulated into keys[0..1] (k_table_init first).
@@ -1989,7 +2044,7 @@ static int table_keys_accumulate(const float* x, int64_t rows, int64_t dim, int6
 static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t ld, int method,
                               int b, double r, int aux, uint8_t* packed, double* xmin, double* xmax,
                               int32_t* info0, int32_t* info1, double* norm, int32_t* status,
-                              void* stream, const int* table_keys) {
+                              void* stream, const int* table_keys, double param) {
   if (rows < 1 || dim < 1) return fail(EQ4_EINVAL, "table must be at least 1x1");
   if (ld < dim) return fail(EQ4_EINVAL, "ld must be >= dim");
   if (!x || !packed) return fail(EQ4_EINVAL, "null buffer");
@@ -2035,7 +2090,8 @@ static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t
   }
   if (method == EQ4_METHOD_ACIQ || method == EQ4_METHOD_GSS) {
     std::string err;
-    const int rc = eq4_rowrange_launch(x, rows, dim, ld, method, aux, packed, xmin, xmax, info0,
+    if (param == 0.0) param = method == EQ4_METHOD_ACIQ ? 5.03 : 1e-4;   // clipping.py:70,125-126
+    const int rc = eq4_rowrange_launch(x, rows, dim, ld, method, param, aux, packed, xmin, xmax, info0,
                                        status, s, err);
     return rc == EQ4_OK ? rc : fail(rc, err);
   }
@@ -2062,12 +2118,11 @@ static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t
     p.inv_qY = 1.0 / p.qY;
     p.delta = (float)(p.qY * 0.5);
     p.tau2 = tau2_for((int)dim, vec);
-    // misround: the code argument alpha*s carries |error| <= eta = 4u*alpha
-    // (approximate reciprocal 2u, product/add roundings), so a code can differ
-    // from the reference's only for elements within eta of a rounding
-    // boundary, each adding <= 2*eta*W^2 to the loss; allow 2 per side, both
-    // sides.
-    p.kmis = (float)(2.0 * 2.0 * 2.0 * 4.0 * 5.9604645e-8 * 15.75);
+    // misround: the code argument alpha*s carries |error| <= eta = ETA_CODE
+    // (kW and s each rounded once), so a code can differ from the reference's
+    // only for elements within eta of a rounding boundary, each adding
+    // <= 2*eta*W^2 to the loss; the band allows 2 per side, both sides.
+    p.kmis = (float)(2.0 * 2.0 * 2.0 * ETA_CODE);
     // ... and when more than 2 elements of a side could misround (repeated values
     // parked next to a boundary), the comparison is only trusted after counting
     // them (near_escalate): up to all d elements per side

@@ -24,9 +24,14 @@ int eq4_io_write_embq(const char* path, const uint8_t* packed, int64_t rows, int
                       int on_device, std::string& err);
 
 // ACIQ / GSS row-range searches + quantize + pack (eq4_rowrange.cu).
-int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, int aux,
-                        uint8_t* packed, double* xmin, double* xmax, int32_t* info0,
+// param: ACIQ's constant (5.03 laplacian or a gaussian_constant), GSS's tol.
+int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, double param,
+                        int aux, uint8_t* packed, double* xmin, double* xmax, int32_t* info0,
                         int32_t* status, cudaStream_t s, std::string& err);
+// ACIQ / GSS ranges of float64 rows (the scalar entry points), no packing.
+int eq4_rowrange_f64_launch(const double* x, int64_t rows, int64_t dim, int64_t ld, int method,
+                            double param, double* xmin, double* xmax, int32_t* info0, int32_t* status,
+                            cudaStream_t s, std::string& err);
 
 // Row-wise KMEANS codebooks (eq4_kmeans.cu).
 int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int aux, uint8_t* out,

@@ -19,6 +19,7 @@
 // Rows wider than 256 read their elements straight from global memory.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -46,17 +47,40 @@ struct RRParams {
   int32_t* info0;
   int32_t* status;
   double invphi;     // (sqrt(5) - 1) / 2, clipping.py:27
+  double aciq_const; // clipping.py:125-134: 5.03 (laplacian) or the caller's gaussian_constant
+  double gss_tol;    // clipping.py:70 tol (default 1e-4)
   int staged;
   int vec4;          // rows 16-byte aligned (d % 4 == 0, ld % 4 == 0, aligned base)
   size_t warp_bytes;
 };
 
-// Element k of this lane's row.
-struct RowView {
-  const float* base;
+// Element k of this lane's row (float32 table rows; float64 for the scalar entry points).
+template <typename T>
+struct RowViewT {
+  const T* base;
   int ks;
-  __device__ __forceinline__ float operator[](int k) const { return base[(size_t)k * ks]; }
+  __device__ __forceinline__ T operator[](int k) const { return base[(size_t)k * ks]; }
 };
+using RowView = RowViewT<float>;
+
+// numpy's zero choice (np_zero_key) for an element of either width.
+template <typename T>
+__device__ __forceinline__ unsigned np_zero_key_t(T v, int p, int d) {
+  if (v != (T)0) return 0u;
+  return np_zero_key(signbit(v) ? -0.f : 0.f, p, d);
+}
+
+// table.py:81-103 quant_mse(x, (lo, hi), 4) of a float64 row, bit-exact (exact codec).
+__device__ __forceinline__ double lane_quant_mse(const RowViewT<double>& xr, int d, double lo, double hi) {
+  if (hi == lo) {
+    return np_sum([&](int k) {
+      const double e = __dsub_rn(xr[k], lo);
+      return __dmul_rn(e, e);
+    }, d);
+  }
+  const double scale = div15(__dsub_rn(hi, lo));
+  return np_sum([&](int k) { return np_err2(xr[k], lo, hi, scale); }, d);
+}
 
 // table.py:81-103 quant_mse(x, (lo, hi), 4) of this lane's row, bit-exact.
 __device__ __forceinline__ double lane_quant_mse(const RowView& xr, int d, double lo, double hi) {
@@ -97,31 +121,36 @@ __device__ __forceinline__ double lane_quant_mse(const RowView& xr, int d, doubl
   }, d);
 }
 
-// clipping.py:115-139, laplacian branch.
-__device__ __forceinline__ void lane_aciq(const RowView& xr, int d, float mn, float mx, double& lo,
-                                          double& hi) {
+// clipping.py:115-139: alpha = constant * mean|x - mean| (5.03 laplacian, :125-126, or
+// the caller's gaussian_constant, :127-134).
+template <typename T>
+__device__ __forceinline__ void lane_aciq(const RowViewT<T>& xr, int d, double mn, double mx,
+                                          double constant, double& lo, double& hi) {
   const double n = (double)d;
   const double mean = __ddiv_rn(np_sum([&](int k) { return (double)xr[k]; }, d), n);
   const double mad = __ddiv_rn(np_sum([&](int k) { return fabs(__dsub_rn((double)xr[k], mean)); }, d), n);
-  const double alpha = __dmul_rn(5.03, mad);
+  const double alpha = __dmul_rn(constant, mad);
   if (alpha == 0.0) {   // clipping.py:137-138 -> clip_range_asym (numpy's signed-zero choice)
-    if (mn == 0.f || mx == 0.f) {
+    if (mn == 0.0 || mx == 0.0) {
       unsigned kz = 0u;
-      for (int k = 0; k < d; k++) kz = max(kz, np_zero_key(xr[k], k, d));
-      np_zero_apply(kz, mn, mx);
+      for (int k = 0; k < d; k++) kz = max(kz, np_zero_key_t(xr[k], k, d));
+      const double z = (kz & 1u) ? -0.0 : 0.0;
+      if (mn == 0.0) mn = z;
+      if (mx == 0.0) mx = z;
     }
-    lo = (double)mn;
-    hi = (double)mx;
+    lo = mn;
+    hi = mx;
   } else {
     lo = __dsub_rn(mean, alpha);
     hi = __dadd_rn(mean, alpha);
   }
 }
 
-// clipping.py:70-112 with tol = 1e-4; returns the number of quant_mse calls.
-__device__ __forceinline__ int lane_gss(const RowView& xr, int d, float mn, float mx, double invphi,
-                                        double& lo_out, double& hi_out) {
-  const double tmax = (double)fmaxf(fabsf(mn), fabsf(mx));
+// clipping.py:70-112; returns the number of quant_mse calls.
+template <typename T>
+__device__ __forceinline__ int lane_gss(const RowViewT<T>& xr, int d, double mn, double mx, double invphi,
+                                        double tol, double& lo_out, double& hi_out) {
+  const double tmax = fmax(fabs(mn), fabs(mx));
   if (tmax == 0.0) {
     lo_out = 0.0;
     hi_out = 0.0;
@@ -139,7 +168,7 @@ __device__ __forceinline__ int lane_gss(const RowView& xr, int d, float mn, floa
   double fc = f(c), fe = f(e);
   if (fc < best_f) { best_t = c; best_f = fc; }
   if (fe < best_f) { best_t = e; best_f = fe; }
-  const double stop = __dmul_rn(1e-4, tmax);
+  const double stop = __dmul_rn(tol, tmax);
   while (__dsub_rn(b, a) > stop) {
     if (fc < fe) {
       b = e; e = c; fe = fc;
@@ -230,9 +259,9 @@ __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
     int evals = 0;
     if (rvalid && !bad) {
       if constexpr (METHOD == EQ4_METHOD_ACIQ) {
-        lane_aciq(xr, d, mn, mx, lo, hi);
+        lane_aciq(xr, d, (double)mn, (double)mx, p.aciq_const, lo, hi);
       } else {
-        evals = lane_gss(xr, d, mn, mx, p.invphi, lo, hi);
+        evals = lane_gss(xr, d, (double)mn, (double)mx, p.invphi, p.gss_tol, lo, hi);
       }
     }
     // codes (uniform.py:60-80) + packed row (packed.py:68-83), staged then copied out
@@ -306,14 +335,65 @@ __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
   }
 }
 
+// The scalar entry points on float64 rows (clip_range_aciq / clip_range_gss of any array,
+// clipping.py:46 promotes it to float64): ranges (and GSS evaluation counts) only, lane
+// per row straight from global memory.
+template <int METHOD>
+__global__ void k_rowrange_f64(const double* x, int64_t rows, int d, int64_t ld, double invphi,
+                               double param, double* lo_out, double* hi_out, int32_t* info0,
+                               int32_t* status) {
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < rows;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    RowViewT<double> xr{x + row * ld, 1};
+    double mn = INFINITY, mx = -INFINITY;
+    bool bad = false;
+    for (int k = 0; k < d; k++) {
+      const double v = xr[k];
+      mn = fmin(mn, v);
+      mx = fmax(mx, v);
+      bad |= !isfinite(v);
+    }
+    double lo = 0.0, hi = 0.0;
+    int evals = 0;
+    if (bad) {
+      if (status) atomicOr(status, EQ4_STATUS_NONFINITE);
+    } else if constexpr (METHOD == EQ4_METHOD_ACIQ) {
+      lane_aciq(xr, d, mn, mx, param, lo, hi);
+    } else {
+      evals = lane_gss(xr, d, mn, mx, invphi, param, lo, hi);
+    }
+    lo_out[row] = lo;
+    hi_out[row] = hi;
+    if (info0) info0[row] = evals;
+  }
+}
+
 }  // namespace eq4
 
 using namespace eq4;
 
-int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, int aux,
-                        uint8_t* packed, double* xmin, double* xmax, int32_t* info0,
+int eq4_rowrange_f64_launch(const double* x, int64_t rows, int64_t dim, int64_t ld, int method,
+                            double param, double* xmin, double* xmax, int32_t* info0, int32_t* status,
+                            cudaStream_t s, std::string& err) {
+  const double invphi = (std::sqrt(5.0) - 1.0) / 2.0;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 127) / 128, 148 * 8));
+  if (method == EQ4_METHOD_ACIQ)
+    k_rowrange_f64<EQ4_METHOD_ACIQ><<<grid, 128, 0, s>>>(x, rows, (int)dim, ld, invphi, param, xmin, xmax,
+                                                         info0, status);
+  else
+    k_rowrange_f64<EQ4_METHOD_GSS><<<grid, 128, 0, s>>>(x, rows, (int)dim, ld, invphi, param, xmin, xmax,
+                                                        info0, status);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { err = std::string("k_rowrange_f64: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+  return EQ4_OK;
+}
+
+int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int method, double param,
+                        int aux, uint8_t* packed, double* xmin, double* xmax, int32_t* info0,
                         int32_t* status, cudaStream_t s, std::string& err) {
   RRParams p;
+  p.aciq_const = method == EQ4_METHOD_ACIQ ? param : 5.03;
+  p.gss_tol = method == EQ4_METHOD_GSS ? param : 1e-4;
   p.x = x; p.rows = rows; p.ld = ld; p.d = (int)dim; p.aux = aux; p.method = method;
   p.half = (int)((dim + 1) / 2);
   p.stride = p.half + 2 * (aux == EQ4_AUX_FP16 ? 2 : 4);

@@ -39,6 +39,9 @@ def test_signed_zero_golden_device_and_host(method):
                 for i in np.nonzero(~keep)[0]:
                     assert oracle.hist_apprx_gap(x[i], b)[1] <= 1e-12, (d, i)
                 assert keep.sum() >= x.shape[0] - 2, d
+            if method == "hist-brute":
+                keep = (_bits(lo) == _bits(glo)) & (_bits(hi) == _bits(ghi))
+                _excuse_hist_ties(x, b, ~keep, rr, f"golden d={d}")
             got = p.buffer.reshape(-1, st)
             assert np.array_equal(got[keep], want[keep]), (d, aux, np.nonzero((got != want).any(1))[0])
             assert np.array_equal(_bits(lo)[keep], _bits(glo)[keep]), (d, aux)
@@ -71,7 +74,25 @@ def test_signed_zero_random_vs_oracle(method, d):
         want = oracle.quantize_pack_table(x, method, b, 0.16, aux)
         st = eq.packed_row_stride(d, aux)
         got = p.buffer.reshape(-1, st)
-        bad = np.nonzero((got != want.packed.reshape(-1, st)).any(1))[0]
+        lo, hi = rr.xmin.cpu().numpy(), rr.xmax.cpu().numpy()
+        badm = ((got != want.packed.reshape(-1, st)).any(1) | (_bits(lo) != _bits(want.xmin))
+                | (_bits(hi) != _bits(want.xmax)))
+        if method == "hist-brute":
+            badm &= ~_excuse_hist_ties(x, b, badm, rr, f"random d={d}")
+        bad = np.nonzero(badm)[0]
         assert bad.size == 0, (aux, bad[:8])
-        assert np.array_equal(_bits(rr.xmin.cpu().numpy()), _bits(want.xmin))
-        assert np.array_equal(_bits(rr.xmax.cpu().numpy()), _bits(want.xmax))
+
+
+def _excuse_hist_ties(x, b, rows_mask, rr, what):
+    """HIST-BRUTE rows whose window differs from the reference's / the oracle's: excused only
+    when the two windows' norms tie to 1e-12 relative (the reference's norms come from BLAS
+    dot products whose rounding order is CPU specific; rows of a few distinct values tie
+    exactly in exact arithmetic).  Returns the excused-row mask."""
+    i0, i1 = rr.info0.cpu().numpy(), rr.info1.cpu().numpy()
+    exc = np.zeros(len(rows_mask), bool)
+    for i in np.nonzero(rows_mask)[0]:
+        o = oracle.hist_brute_search(x[i], b)
+        ng = oracle.hist_window_norm(x[i], b, int(i0[i]), int(i1[i]))
+        assert abs(ng - o.norm) <= 1e-12 * max(abs(ng), abs(o.norm)), (what, i, ng, o.norm)
+        exc[i] = True
+    return exc
