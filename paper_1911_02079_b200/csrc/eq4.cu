@@ -61,10 +61,10 @@ constexpr int NWARPS_G = NTHREADS_G / 32;
 constexpr int MAX_LEAVES = 64;          // numpy pairwise leaves for d <= 4096
 constexpr float ALPHA = 15.75f;         // saturation scale for the code FFMA
 // |alpha * s - (z/W + 1/2)| <= ETA_CODE for s = RN(z * kw_of(W) + h), |z/W| <= 15.5:
-// 15.5 * 2^-24 (kW rounded once) + 15.75 * 2^-25 (s rounded once) = 1.39e-6.
-constexpr double ETA_CODE = 1.6e-6;
+// 15.5 * 2^-23 (kW within 1 ulp) + 15.75 * 2^-25 (s rounded once) = 2.32e-6.
+constexpr double ETA_CODE = 2.6e-6;
 // elements counted as able to take the other code: within ETA_CODE (+ margin) + delta/W
-constexpr float NEAR_CNT = 2.5e-6f;
+constexpr float NEAR_CNT = 3.5e-6f;
 constexpr float MAGIC = 8388608.f;      // 2^23
 enum { M_ASYM = 0, M_GREEDY = 1 };
 #ifndef GREEDY_MINB
@@ -194,9 +194,10 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   return r;
 }
 
-// 1 / (W alpha) rounded once (W alpha is exact in fp32 for W < 2^18): the search's
-// code argument alpha * sat(z * kW + h) is then within ETA_CODE of (z / W + 1/2).
-__device__ __forceinline__ float kw_of(float Wf) { return __frcp_rn(Wf * ALPHA); }
+// 1 / (W alpha) by rcp.approx (max error 1 ulp; W alpha is exact in fp32 for
+// W < 2^18): the search's code argument alpha * sat(z * kW + h) is then within
+// ETA_CODE of (z / W + 1/2).
+__device__ __forceinline__ float kw_of(float Wf) { return rcp_approx(Wf * ALPHA); }
 
 __device__ __forceinline__ float sat_fma(float a, float b, float c) {
   float r;
@@ -2119,7 +2120,7 @@ static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t
     p.delta = (float)(p.qY * 0.5);
     p.tau2 = tau2_for((int)dim, vec);
     // misround: the code argument alpha*s carries |error| <= eta = ETA_CODE
-    // (kW and s each rounded once), so a code can differ from the reference's
+    // (kW within 1 ulp, s rounded once), so a code can differ from the reference's
     // only for elements within eta of a rounding boundary, each adding
     // <= 2*eta*W^2 to the loss; the band allows 2 per side, both sides.
     p.kmis = (float)(2.0 * 2.0 * 2.0 * ETA_CODE);
