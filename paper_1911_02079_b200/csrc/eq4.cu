@@ -1704,6 +1704,49 @@ __global__ void k_selftest_div15(int which, int64_t n, uint64_t seed, unsigned l
 using namespace eq4;
 
 static thread_local std::string g_err;
+
+// Python's repr(float) (shortest round-trip digits; fixed notation for decimal
+// exponents -4..15 with at least one fractional digit, else d.ddde+XX), so the
+// C ABI's messages carry the reference's exact ValueError texts (table.py:73-74
+// formats the floats with str()).
+std::string py_float_repr(double v) {
+  if (v != v) return "nan";
+  if (v == INFINITY) return "inf";
+  if (v == -INFINITY) return "-inf";
+  char buf[64];
+  int prec = 1;
+  for (; prec <= 17; ++prec) {
+    snprintf(buf, sizeof buf, "%.*e", prec - 1, v);
+    if (strtod(buf, nullptr) == v) break;
+  }
+  // buf = [-]d.ddde[+-]XX with prec significant digits
+  std::string m(buf);
+  const size_t epos = m.find('e');
+  const int exp10 = atoi(m.c_str() + epos + 1);
+  std::string digits;
+  for (size_t i = 0; i < epos; ++i)
+    if (m[i] >= '0' && m[i] <= '9') digits += m[i];
+  const bool neg = v < 0 || (v == 0 && std::signbit(v));
+  std::string out = neg ? "-" : "";
+  if (exp10 >= -4 && exp10 < 16) {
+    if (exp10 < 0) {
+      out += "0." + std::string(-exp10 - 1, '0') + digits;
+    } else {
+      if ((int)digits.size() <= exp10 + 1) {
+        out += digits + std::string(exp10 + 1 - digits.size(), '0') + ".0";
+      } else {
+        out += digits.substr(0, exp10 + 1) + "." + digits.substr(exp10 + 1);
+      }
+    }
+  } else {
+    out += digits.substr(0, 1);
+    if (digits.size() > 1) out += "." + digits.substr(1);
+    char e[16];
+    snprintf(e, sizeof e, "e%c%02d", exp10 < 0 ? '-' : '+', exp10 < 0 ? -exp10 : exp10);
+    out += e;
+  }
+  return out;
+}
 static int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
@@ -2308,9 +2351,7 @@ int eq4_quantize_pack_host(const float* x, int64_t rows, int64_t dim, int64_t ld
       if (code == EQ4_EDATA) {
         rc = fail(EQ4_EDATA, "table contains non-finite values (NaN/Inf)");
       } else if (code == EQ4_ERANGE) {
-        char buf[128];
-        snprintf(buf, sizeof buf, "xmin %.17g exceeds xmax %.17g", elo, ehi);
-        rc = fail(EQ4_ERANGE, buf);
+        rc = fail(EQ4_ERANGE, "xmin " + py_float_repr(elo) + " exceeds xmax " + py_float_repr(ehi));
         if (bad_lohi) { bad_lohi[0] = elo; bad_lohi[1] = ehi; }
       }
       if (bad_row && first >= 0) *bad_row = r0 + first;

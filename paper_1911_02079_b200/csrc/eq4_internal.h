@@ -59,3 +59,6 @@ int eq4_codec_bin_l2_norm(const double* db, const double* de, const double* rho,
 int eq4_codec_quant_mse_rows(const void* x, int x_f64, int64_t rows, int64_t dim, int64_t ld,
                              const double* xmin, const double* xmax, int nbits, double* out,
                              cudaStream_t s, std::string& err);
+
+// Python's repr(float) text (eq4.cu), for the reference's ValueError messages.
+std::string py_float_repr(double v);

@@ -271,7 +271,7 @@ int eq4_io_quantize_file(const char* in_path, const char* out_path, int method, 
         if (dhi) cudaFree(dhi);
         if (bad_row) *bad_row = found >= 0 ? r0 + found : -1;
         if (bad_lohi) { bad_lohi[0] = lohi[0]; bad_lohi[1] = lohi[1]; }
-        err = "xmin exceeds xmax";
+        err = "xmin " + py_float_repr(lohi[0]) + " exceeds xmax " + py_float_repr(lohi[1]);
         rc = EQ4_ERANGE;
       }
       break;
