@@ -608,7 +608,7 @@ def hist_brute_search(x, b: int = 200, counters: WorkCounters | None = None) -> 
 
 
 def hist_apprx_search(x, b: int = 200, counters: WorkCounters | None = None) -> HistWindow:
-    """histclip.py:181-217 (b <= 256 on the GPU path)."""
+    """histclip.py:181-217."""
     _check_method_params("hist-apprx", b, 0.16)
     rr = _row_search("hist-apprx", x, b)
     _apply_counters(counters, "hist-apprx", b, rr)

@@ -569,11 +569,13 @@ struct WarpSliceG {
   static constexpr int RPW = 32 / LPR;
   static constexpr int D = LPR * E;
   static constexpr int E2CAP = D < 512 ? D : 512;
+  // numpy pairwise leaves of a row of <= D elements (leaves hold 64..128 above 128)
+  static constexpr int LEAVES = D / 64 + 2 > MAX_LEAVES ? D / 64 + 2 : MAX_LEAVES;
   __host__ __device__ static size_t ys_off() { return 0; }                            // E/4 x 32 float4
   __host__ __device__ static size_t rs_off() { return ys_off() + (size_t)E * 32 * 4; }
   __host__ __device__ static size_t e2_off() { return rs_off() + RPW * sizeof(RowShared); }
   __host__ __device__ static size_t leaf_off() { return e2_off() + (size_t)E2CAP * 8; }
-  __host__ __device__ static size_t codes_off() { return leaf_off() + (size_t)MAX_LEAVES * 16; }
+  __host__ __device__ static size_t codes_off() { return leaf_off() + (size_t)LEAVES * 16; }
   __host__ __device__ static size_t out_off() {
     return (codes_off() + (VEC ? 0 : (size_t)RPW * D) + 15) & ~(size_t)15;
   }
@@ -835,7 +837,7 @@ struct ExactOut {
   int flags;  // 1 = range error, 2 = move left, 4 = candidate better than best
 };
 
-template <bool INLINE_LEAF>
+template <bool INLINE_LEAF, int LEAVES>
 __device__ __forceinline__ ExactOut exact_decide(RowShared* R, double nl, double nr, int bi, int bj,
                                                  bool bvalid, const float* xs, int d, double* e2,
                                                  double* leaf_sum, int* leaf_st, int* leaf_ln) {
@@ -862,7 +864,7 @@ __device__ __forceinline__ ExactOut exact_decide(RowShared* R, double nl, double
     o.flags = (goL ? 2 : 0) | ((goL ? o.vL : o.vR) < o.vb ? 4 : 0);   // clipping.py:187,191
     return o;
   }
-  if (!errL) o.vL = warp_np_loss(xs, d, lmin, lmax, e2, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
+  if (!errL) o.vL = warp_np_loss(xs, d, lmin, lmax, e2, leaf_sum, leaf_st, leaf_ln, LEAVES);
   if (errL || errR) {
     if ((threadIdx.x & 31) == 0) {
       R->elo = errL ? lmin : rmin;
@@ -871,13 +873,13 @@ __device__ __forceinline__ ExactOut exact_decide(RowShared* R, double nl, double
     o.flags = 1;
     return o;
   }
-  o.vR = warp_np_loss(xs, d, rmin, rmax, e2, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
+  o.vR = warp_np_loss(xs, d, rmin, rmax, e2, leaf_sum, leaf_st, leaf_ln, LEAVES);
   const bool goL = o.vL < o.vR;                             // clipping.py:185
   const double vc = goL ? o.vL : o.vR;
   if (!bvalid) {
     const double blo = bi == 0 ? x0 : __dadd_rn(x0, __dmul_rn((double)bi, st));
     const double bhi = bj == 0 ? x1 : __dsub_rn(x1, __dmul_rn((double)bj, st));
-    o.vb = warp_np_loss(xs, d, blo, bhi, e2, leaf_sum, leaf_st, leaf_ln, MAX_LEAVES);
+    o.vb = warp_np_loss(xs, d, blo, bhi, e2, leaf_sum, leaf_st, leaf_ln, LEAVES);
   }
   o.flags = (goL ? 2 : 0) | (vc < o.vb ? 4 : 0);            // clipping.py:187,191
   return o;
@@ -1054,7 +1056,7 @@ __device__ __forceinline__ void exact_block(const Params& p, bool need_ex, int q
     bal &= bal - 1;
     const int lg = leader / LPR;
     if ((threadIdx.x & 31) == 0) wdiag[0] += 1u;
-    const ExactOut o = exact_decide<(E <= 16)>(
+    const ExactOut o = exact_decide<(E <= 16), WarpSliceG<LPR, E, VEC>::LEAVES>(
         &rs[lg], (double)__shfl_sync(FULL, nl, leader), (double)__shfl_sync(FULL, nr, leader),
         __shfl_sync(FULL, bi, leader), __shfl_sync(FULL, bj, leader),
         (__shfl_sync(FULL, flags, leader) & F_BEST_EX) != 0, xblk + lg * ld, d, e2, leaf_sum, leaf_st,
@@ -1097,8 +1099,8 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
   RowShared* rs = reinterpret_cast<RowShared*>(ws + S::rs_off());
   double* e2 = reinterpret_cast<double*>(ws + S::e2_off());
   double* leaf_sum = reinterpret_cast<double*>(ws + S::leaf_off());
-  int* leaf_st = reinterpret_cast<int*>(leaf_sum + MAX_LEAVES);
-  int* leaf_ln = leaf_st + MAX_LEAVES;
+  int* leaf_st = reinterpret_cast<int*>(leaf_sum + S::LEAVES);
+  int* leaf_ln = leaf_st + S::LEAVES;
   uint8_t* codes_w = ws + S::codes_off();
   uint8_t* out_base = ws + S::out_off();
   unsigned* wdiag = reinterpret_cast<unsigned*>(ws + S::diag_off(p.stride));
@@ -1108,9 +1110,10 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
   const int nv = valid_slots<LPR, E, VEC>(q, d);
   const float hh = 0.5f / ALPHA;
   const int64_t nblocks = (p.rows + RPW - 1) / RPW;
-  const int64_t wstride = (int64_t)gridDim.x * NWARPS_G;
+  const int nwb = (int)(blockDim.x >> 5);   // warps per block (fewer for wide rows)
+  const int64_t wstride = (int64_t)gridDim.x * nwb;
 
-  for (int64_t blk = (int64_t)blockIdx.x * NWARPS_G + warp; blk < nblocks; blk += wstride) {
+  for (int64_t blk = (int64_t)blockIdx.x * nwb + warp; blk < nblocks; blk += wstride) {
     const int64_t row0 = blk * RPW, row = row0 + gw;
     const bool rvalid = row < p.rows;
     RowShared& R = rs[gw];
@@ -1180,6 +1183,47 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const double Y = __dmul_rn(__dsub_rn((double)tv[k], x0), kY);
+            y[k] = (float)__dsub_rn(__dadd_rn(Y, cY), cY);
+          }
+          ys4[c * 32 + lane] = make_float4(y[0], y[1], y[2], y[3]);
+        }
+      } else if constexpr (E > 64) {
+        // wide masked rows (d > 2048): the lane's slots q + LPR*i are streamed from
+        // global memory twice (L1/L2 hits the second time) -- no E-sized register array
+        const float* src = xr + q;
+        float lmn = INFINITY, lmx = -INFINITY, sm = 0.f;
+        for (int i = 0; i < nv; ++i) {
+          const float t = rvalid ? __ldg(src + LPR * i) : 0.f;
+          lmn = fminf(lmn, t);
+          lmx = fmaxf(lmx, t);
+          sm = __fadd_rn(sm, t);
+        }
+        mn = group_min<LPR>(lmn);
+        mx = group_max<LPR>(lmx);
+        sm = group_sum<LPR>(sm);
+        if (__any_sync(FULL, rvalid && (mn == 0.f || mx == 0.f))) {   // rare: numpy's signed-zero choice
+          unsigned kz = 0u;
+          for (int i = 0; i < nv; ++i)
+            kz = max(kz, np_zero_key(rvalid ? __ldg(src + LPR * i) : 1.f, q + LPR * i, d));
+          np_zero_apply(group_umax<LPR>(kz), mn, mx);
+        }
+        bad = false;
+        if (__any_sync(FULL, !isfinite(sm) && rvalid)) {
+          bool lb = false;
+          for (int i = 0; i < nv; ++i) lb |= rvalid && !isfinite(__ldg(src + LPR * i));
+          bad = group_any<LPR>(lb) && rvalid;
+          if (bad && q == 0 && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
+        }
+        x0 = (double)mn; x1 = (double)mx;
+        step = __ddiv_rn(__dsub_rn(x1, x0), (double)p.b);                           // :172
+        kY = (x0 != x1) ? __ddiv_rn(15.0, step) : 0.0;
+        for (int c = 0; c < E / 4; ++c) {
+          float y[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int i = 4 * c + k;
+            const float t = (rvalid && i < nv) ? __ldg(src + LPR * i) : 0.f;
+            const double Y = __dmul_rn(__dsub_rn((double)t, x0), kY);
             y[k] = (float)__dsub_rn(__dadd_rn(Y, cY), cY);
           }
           ys4[c * 32 + lane] = make_float4(y[0], y[1], y[2], y[3]);
@@ -1604,6 +1648,90 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_asym_bulk(const Params p) {
 }
 
 // ---------------------------------------------------------------------------
+// ASYM family on wide rows (d > 2048): one warp per row, two streaming passes
+// (min / max / finiteness, then codes; the second pass hits L1/L2), nibbles
+// written straight to the packed row.  Bandwidth-class like k_asym; no
+// E-sized register arrays, so any d.
+// ---------------------------------------------------------------------------
+template <int RM>
+__global__ void __launch_bounds__(256) k_asym_wide(const Params p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int d = p.d;
+  const bool vec = (d % 4 == 0) && (p.ld % 4 == 0) && (((uintptr_t)p.x & 15) == 0);
+  for (int64_t row = w0; row < p.rows; row += ws) {
+    const float* xr = p.x + row * p.ld;
+    float mn = INFINITY, mx = -INFINITY, sm = 0.f;
+    if (vec) {
+      const float4* x4 = reinterpret_cast<const float4*>(xr);
+      for (int c = lane; c < d / 4; c += 32) {
+        const float4 t = __ldcs(x4 + c);
+        mn = fminf(mn, fminf(fminf(t.x, t.y), fminf(t.z, t.w)));
+        mx = fmaxf(mx, fmaxf(fmaxf(t.x, t.y), fmaxf(t.z, t.w)));
+        sm = __fadd_rn(sm, __fadd_rn(__fadd_rn(t.x, t.y), __fadd_rn(t.z, t.w)));
+      }
+    } else {
+      for (int k = lane; k < d; k += 32) {
+        const float t = __ldcs(xr + k);
+        mn = fminf(mn, t);
+        mx = fmaxf(mx, t);
+        sm = __fadd_rn(sm, t);
+      }
+    }
+    mn = group_min<32>(mn);
+    mx = group_max<32>(mx);
+    sm = group_sum<32>(sm);
+    if (mn == 0.f || mx == 0.f) {   // rare: numpy's signed-zero choice
+      unsigned kz = 0u;
+      for (int k = lane; k < d; k += 32) kz = max(kz, np_zero_key(xr[k], k, d));
+      np_zero_apply(__reduce_max_sync(FULL, kz), mn, mx);
+    }
+    bool bad = false;
+    if (!isfinite(sm)) {
+      bool lb = false;
+      for (int k = lane; k < d; k += 32) lb |= !isfinite(xr[k]);
+      bad = __any_sync(FULL, lb);
+      if (bad && lane == 0 && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
+    }
+    apply_range_mode<RM>(p, mn, mx);
+    const double lo = (double)mn, hi = (double)mx;          // clipping.py:51-67
+    const CodeParams cp = make_code_params(bad ? 0.0 : lo, bad ? 0.0 : hi);
+    uint8_t* orow = p.packed + row * (int64_t)p.stride;
+    // codes (uniform.py:77-79) of element pairs -> packed bytes (packed.py:75-77)
+    for (int m = lane; m < p.half; m += 32) {
+      unsigned c0 = 0u, c1 = 0u;
+      if (!bad) {
+        bool n0, n1 = false;
+        const float a = xr[2 * m];
+        c0 = code_of(a, cp, n0);
+        if (n0) c0 = code_exact(a, cp);
+        if (2 * m + 1 < d) {
+          const float bb = xr[2 * m + 1];
+          c1 = code_of(bb, cp, n1);
+          if (n1) c1 = code_exact(bb, cp);
+        }
+      }
+      orow[m] = (uint8_t)(c0 | (c1 << 4));
+    }
+    if (lane == 0) {
+      const double sc = (!bad && hi != lo) ? cp.scale : 0.0;   // uniform.py:74-80
+      uint8_t* a = orow + p.half;
+      if (p.aux == EQ4_AUX_FP16) {
+        const uint32_t s16 = aux_bits_f16(sc), b16 = aux_bits_f16(lo);
+        a[0] = s16 & 0xff; a[1] = s16 >> 8; a[2] = b16 & 0xff; a[3] = b16 >> 8;
+      } else {
+        const uint32_t s32 = aux_bits_f32(sc), b32 = aux_bits_f32(lo);
+        for (int k = 0; k < 4; ++k) { a[k] = (s32 >> (8 * k)) & 0xff; a[4 + k] = (b32 >> (8 * k)) & 0xff; }
+      }
+      if (p.lo_out) { p.lo_out[row] = lo; p.hi_out[row] = hi; }
+      if (p.info0) p.info0[row] = 0;
+      if (p.info1) p.info1[row] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // pack / unpack / quant_mse utility kernels
 // ---------------------------------------------------------------------------
 __global__ void k_pack(const uint8_t* codes, int64_t rows, int d, int aux, const uint8_t* sc,
@@ -1807,9 +1935,12 @@ static int launch_rq(const Params& p, cudaStream_t s) {
     return launch_persistent(k_asym<LPR, E, VEC, 0>, L::total(p.stride), nt, p, s, "k_asym");
   } else {
     using S = WarpSliceG<LPR, E, VEC>;
-    return launch_persistent(k_greedy<LPR, E, VEC>, NWARPS_G * S::bytes(p.stride),
-                             (p.rows + S::RPW * NWARPS_G - 1) / (S::RPW * NWARPS_G), p, s, "k_greedy",
-                             NTHREADS_G);
+    // wide rows: as many warps per block as the per-warp slices fit in shared memory
+    int nw = NWARPS_G;
+    while (nw > 1 && (size_t)nw * S::bytes(p.stride) > 220 * 1024) nw >>= 1;
+    if (S::bytes(p.stride) > 220 * 1024) return fail(EQ4_EUNSUPPORTED, "GREEDY row does not fit in shared memory");
+    return launch_persistent(k_greedy<LPR, E, VEC>, nw * S::bytes(p.stride),
+                             (p.rows + S::RPW * nw - 1) / (S::RPW * nw), p, s, "k_greedy", 32 * nw);
   }
 }
 
@@ -1839,7 +1970,11 @@ static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
     if (d <= 512) return launch_rq<METHOD, 32, 16, false>(p, s);
     if (d <= 1024) return launch_rq<METHOD, 32, 32, false>(p, s);
     if (d <= 2048) return launch_rq<METHOD, 32, 64, false>(p, s);
-    return fail(EQ4_EUNSUPPORTED, "dim > 2048 is not supported by the B200 path");
+    // wide rows: warp per row, two streaming passes
+    const int64_t nt = (p.rows + 7) / 8;
+    if (p.range_mode == 1) return launch_persistent(k_asym_wide<1>, 0, nt, p, s, "k_asym_wide");
+    if (p.range_mode == 2) return launch_persistent(k_asym_wide<2>, 0, nt, p, s, "k_asym_wide");
+    return launch_persistent(k_asym_wide<0>, 0, nt, p, s, "k_asym_wide");
   } else {
   // GREEDY: 64 elements per lane amortise the per-iteration decision work best
   // (measured on 20M x 64 and the 1 GiB d-sweep against 32 per lane; the row
@@ -1854,6 +1989,9 @@ static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
       case 512: return launch_rq<METHOD, 8, 64, true>(p, s);
       case 1024: return launch_rq<METHOD, 16, 64, true>(p, s);
       case 2048: return launch_rq<METHOD, 32, 64, true>(p, s);
+      case 4096: return launch_rq<METHOD, 32, 128, true>(p, s);
+      case 8192: return launch_rq<METHOD, 32, 256, true>(p, s);
+      case 16384: return launch_rq<METHOD, 32, 512, true>(p, s);
       default: break;
     }
   }
@@ -1866,7 +2004,11 @@ static int dispatch_rq(const Params& p, bool vec, cudaStream_t s) {
   if (d <= 512) return launch_rq<METHOD, 8, 64, false>(p, s);
   if (d <= 1024) return launch_rq<METHOD, 16, 64, false>(p, s);
   if (d <= 2048) return launch_rq<METHOD, 32, 64, false>(p, s);
-  return fail(EQ4_EUNSUPPORTED, "dim > 2048 is not supported by the B200 path");
+  // wide rows: one warp per row, 128..512 elements per lane (row slice in shared memory)
+  if (d <= 4096) return launch_rq<METHOD, 32, 128, false>(p, s);
+  if (d <= 8192) return launch_rq<METHOD, 32, 256, false>(p, s);
+  if (d <= 16384) return launch_rq<METHOD, 32, 512, false>(p, s);
+  return fail(EQ4_EUNSUPPORTED, "GREEDY with dim > 16384 is not supported by the B200 path");
   }
 }
 
@@ -1883,9 +2025,10 @@ static float tau2_for(int d, bool vec) {
   if (d <= 8) { lpr = 1; e = 8; }
   else if (d <= 16) { lpr = 1; e = 16; }
   else if (d <= 32) { lpr = 1; e = 32; }
-  else { lpr = 1; while (lpr * 64 < d) lpr *= 2; e = 64; }
+  else if (d <= 2048) { lpr = 1; while (lpr * 64 < d) lpr *= 2; e = 64; }
+  else { lpr = 32; e = d <= 4096 ? 128 : (d <= 8192 ? 256 : 512); }
   const bool packed = vec && (d == 16 || d == 32 || d == 64 || d == 128 || d == 256 || d == 512 ||
-                              d == 1024 || d == 2048);
+                              d == 1024 || d == 2048 || d == 4096 || d == 8192 || d == 16384);
   int lg = 0;
   while ((1 << lg) < lpr) lg++;
   const int h = (packed ? e / 2 + 1 : e) + lg + 1;

@@ -432,13 +432,15 @@ __device__ __forceinline__ double apprx_term(int c, int j, double w, int s, doub
 }
 
 // histclip.py:110-121 window_norm = np.sum over the b bins of density * unit norm, in
-// numpy's pairwise order (b <= 256: one or two leaves of 8 accumulator chains, the
-// fixed ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree, then the remainder in order).
-// Warp-collective: lanes compute the bins' terms into t[0..b) (empty bins give the
-// +0.0 numpy adds, which leave every partial sum unchanged), lanes 8l..8l+7 run
-// leaf l's chains.  Every lane returns the value.
+// numpy's pairwise order (the leaves of np_leaves, 8 accumulator chains each, the
+// fixed ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree, the remainder in order, then the
+// leaves combined in the recursion's association, np_combine).  Warp-collective:
+// lanes compute the bins' terms into t[0..b) (empty bins give the +0.0 numpy adds,
+// which leave every partial sum unchanged), lanes 8l..8l+7 run leaf l's chains.
+// Every lane returns the value.
 static __device__ __noinline__ double apprx_norm_np_warp(const int* cnt, int b, double w, int s, int n,
-                                                  double* t, int lane) {
+                                                  double* t, int lane, double* leaf_sum, int* leaf_st,
+                                                  int* leaf_ln, int max_leaves) {
   const double dst_w = __ddiv_rn(__dmul_rn(w, (double)n), 15.0);
   const double half = __dmul_rn(0.5, dst_w);
   const double cw = l2u(-half, half);
@@ -446,26 +448,38 @@ static __device__ __noinline__ double apprx_norm_np_warp(const int* cnt, int b, 
     const int c = cnt[j];
     t[j] = c ? apprx_term(c, j, w, s, dst_w, half, cw) : 0.0;
   }
+  int nl = 0;
+  if (lane == 0) nl = np_leaves(b, leaf_st, leaf_ln, max_leaves);
+  nl = __shfl_sync(0xffffffffu, nl, 0);
   __syncwarp();
-  const int nleaves = b > 128 ? 2 : 1;
-  int n2 = b;
-  if (b > 128) { n2 = b / 2; n2 -= n2 % 8; }
-  const int leaf = (lane >> 3) & 1, k = lane & 7;
-  const int ls = leaf ? n2 : 0, ln = leaf ? b - n2 : n2;
-  const int nfull = ln < 8 ? 0 : ln - (ln % 8);
-  double r = 0.0;
-  if (lane < 8 * nleaves)
-    for (int jj = k; jj < nfull; jj += 8) r = __dadd_rn(r, t[ls + jj]);
-  double rr[8];
-#pragma unroll
-  for (int q = 0; q < 8; q++) rr[q] = __shfl_sync(0xffffffffu, r, (lane & 8) + q);
-  double res = 0.0;
-  if (ln >= 8)
-    res = __dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
-                    __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7])));
-  for (int jj = nfull; jj < ln; jj++) res = __dadd_rn(res, t[ls + jj]);
-  const double leaf1 = __shfl_sync(0xffffffffu, res, 8);
-  const double total = nleaves == 2 ? __dadd_rn(res, leaf1) : res;   // lane 0: leaf 0 + leaf 1
+  // four leaves per pass: lanes 8l..8l+7 run leaf l's 8 accumulator chains
+  const int g = lane >> 3, m = lane & 7;
+  for (int base = 0; base < nl; base += 4) {
+    const int li = base + g;
+    const bool ok = li < nl;
+    const int a = ok ? leaf_st[li] : 0, len = ok ? leaf_ln[li] : 8;
+    const int nfull = len - (len % 8);
+    double r = (ok && len >= 8) ? t[a + m] : 0.0;
+    for (int i = 8 + m; i < nfull; i += 8) r = __dadd_rn(r, t[a + i]);
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    if (ok && m == 0) {
+      if (len < 8) {   // numpy: res = 0.; res += a[i] for n < 8
+        r = 0.0;
+        for (int i = 0; i < len; i++) r = __dadd_rn(r, t[a + i]);
+      } else {
+        for (int i = nfull; i < len; i++) r = __dadd_rn(r, t[a + i]);
+      }
+      leaf_sum[li] = r;
+    }
+    __syncwarp();
+  }
+  double total = 0.0;
+  if (lane == 0) {
+    int li = 0;
+    total = np_combine(b, leaf_sum, &li);
+  }
   __syncwarp();
   return __shfl_sync(0xffffffffu, __dadd_rn(0.0, total), 0);
 }

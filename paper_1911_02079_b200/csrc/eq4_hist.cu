@@ -74,6 +74,7 @@ struct HistParams {
   double *lo_out, *hi_out, *norm_out;
   int32_t *info0, *info1, *status;
   const double* U;
+  int wide;   // rows read from global memory (too wide to stage)
 };
 
 // codes (uniform.py:60-80) + packed row (packed.py:68-83) + per-row outputs.  Warp-collective.
@@ -82,18 +83,34 @@ __device__ __forceinline__ void hist_emit(const HistParams& p, int64_t row, int 
                                           int best_s, int best_n, double norm) {
   const bool ok = !bad;
   const CodeParams cp = make_code_params(ok ? wlo : 0.0, ok ? whi : 0.0);
-  for (int k = lane; k < d; k += 32) {
-    bool ne;
-    unsigned c = code_of(xs[k], cp, ne);
-    if (ne) c = code_exact(xs[k], cp);
-    codes[k] = ok ? (uint8_t)c : 0;
-  }
-  __syncwarp();
   uint8_t* orow = p.packed + row * (int64_t)p.stride;
-  for (int m = lane; m < p.half; m += 32) {
-    const unsigned c0 = codes[2 * m];
-    const unsigned c1 = (2 * m + 1 < d) ? codes[2 * m + 1] : 0u;
-    orow[m] = (uint8_t)(c0 | (c1 << 4));
+  if (p.wide) {   // element pairs straight to packed bytes (no staging)
+    for (int m = lane; m < p.half; m += 32) {
+      unsigned c0 = 0u, c1 = 0u;
+      if (ok) {
+        bool ne;
+        c0 = code_of(xs[2 * m], cp, ne);
+        if (ne) c0 = code_exact(xs[2 * m], cp);
+        if (2 * m + 1 < d) {
+          c1 = code_of(xs[2 * m + 1], cp, ne);
+          if (ne) c1 = code_exact(xs[2 * m + 1], cp);
+        }
+      }
+      orow[m] = (uint8_t)(c0 | (c1 << 4));
+    }
+  } else {
+    for (int k = lane; k < d; k += 32) {
+      bool ne;
+      unsigned c = code_of(xs[k], cp, ne);
+      if (ne) c = code_exact(xs[k], cp);
+      codes[k] = ok ? (uint8_t)c : 0;
+    }
+    __syncwarp();
+    for (int m = lane; m < p.half; m += 32) {
+      const unsigned c0 = codes[2 * m];
+      const unsigned c1 = (2 * m + 1 < d) ? codes[2 * m + 1] : 0u;
+      orow[m] = (uint8_t)(c0 | (c1 << 4));
+    }
   }
   if (lane == 0) {
     const double sc = (ok && whi != wlo) ? div15(__dsub_rn(whi, wlo)) : 0.0;
@@ -143,9 +160,14 @@ struct HistSlice {
   __host__ __device__ size_t cnt_off() const { return nz_off() + (size_t)m * 16; }          // int[b]
   __host__ __device__ size_t lb_off() const { return cnt_off() + (size_t)b * 4; }           // int[b+1]
   __host__ __device__ size_t xs_off() const { return lb_off() + (size_t)(b + 1) * 4; }      // float[d]
-  __host__ __device__ size_t codes_off() const { return xs_off() + (size_t)d * 4; }         // u8[d]
-  __host__ __device__ size_t wq_off() const { return (codes_off() + (size_t)d + 15) & ~(size_t)15; }   // int[64]
-  __host__ __device__ size_t bytes() const { return wq_off() + 64 * 4; }
+  __host__ __device__ size_t codes_off() const { return xs_off() + (wide ? 0 : (size_t)d * 4); }   // u8[d]
+  __host__ __device__ size_t wq_off() const {                                                // int[64]
+    return (codes_off() + (wide ? 0 : (size_t)d) + 15) & ~(size_t)15;
+  }
+  __host__ __device__ int leaves() const { return b / 64 + 2; }                             // numpy leaves of b terms
+  __host__ __device__ size_t leaf_off() const { return wq_off() + 64 * 4; }                  // double + 2 int per leaf
+  __host__ __device__ size_t bytes() const { return leaf_off() + (size_t)leaves() * 16; }
+  bool wide;   // the row stays in global memory (xs / codes not staged)
 };
 
 __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
@@ -179,8 +201,11 @@ constexpr double APPRX_TOL = 1e-11;   // relative gap below which the walk re-de
 __device__ __forceinline__ void hist_apprx_walk(const double* Us, const double* A3, const double* R3,
                                                 const NzBin* nz, const int* cnt,
                                                 double* tmp, int m, int b, double w, int lane, int& best_s,
-                                                int& best_n, double& norm) {
-  auto exact = [&](int s0, int n0) -> double { return apprx_norm_np_warp(cnt, b, w, s0, n0, tmp, lane); };
+                                                int& best_n, double& norm, double* leaf_sum, int* leaf_st,
+                                                int* leaf_ln, int max_leaves) {
+  auto exact = [&](int s0, int n0) -> double {
+    return apprx_norm_np_warp(cnt, b, w, s0, n0, tmp, lane, leaf_sum, leaf_st, leaf_ln, max_leaves);
+  };
   int st = 0, en = b;
   double bestF;
   {
@@ -251,7 +276,7 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = p.b, d = p.d;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const HistSlice S{b, d, min(b, d)};
+  const HistSlice S{b, d, min(b, d), p.wide != 0};
   const double* Us = p.U;   // L1/L2-resident (160 KB at b = 200)
   unsigned char* ws = smem + (size_t)warp * S.bytes();
   double* A3 = reinterpret_cast<double*>(ws + S.a3_off());
@@ -259,17 +284,22 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
   NzBin* nz = reinterpret_cast<NzBin*>(ws + S.nz_off());
   int* cnt = reinterpret_cast<int*>(ws + S.cnt_off());
   int* lb = reinterpret_cast<int*>(ws + S.lb_off());
-  float* xs = reinterpret_cast<float*>(ws + S.xs_off());
+  float* xs_s = reinterpret_cast<float*>(ws + S.xs_off());
   uint8_t* codes = ws + S.codes_off();
   int* wq = reinterpret_cast<int*>(ws + S.wq_off());
+  double* leaf_sum = reinterpret_cast<double*>(ws + S.leaf_off());
+  int* leaf_st = reinterpret_cast<int*>(leaf_sum + S.leaves());
+  int* leaf_ln = leaf_st + S.leaves();
 
   for (int64_t row = (int64_t)blockIdx.x * nw + warp; row < p.rows; row += (int64_t)gridDim.x * nw) {
     // ---- row, min/max, finiteness ----
     float mn = INFINITY, mx = -INFINITY;
     bool bad = false;
+    // the row: staged in shared memory, or read from global memory when it is too wide
+    const float* xs = S.wide ? p.x + row * p.ld : xs_s;
     for (int k = lane; k < d; k += 32) {
       const float v = p.x[row * p.ld + k];
-      xs[k] = v;
+      if (!S.wide) xs_s[k] = v;
       mn = fminf(mn, v);
       mx = fmaxf(mx, v);
       bad |= !isfinite(v);
@@ -337,7 +367,7 @@ __global__ void __launch_bounds__(32 * HIST_NW) k_hist(const HistParams p) {
       __syncwarp();
       if constexpr (APPRX) {
         hist_apprx_walk(Us, A3, R3, nz, cnt, reinterpret_cast<double*>(ws + S.tmp_off()), m, b, w, lane,
-                        best_s, best_n, norm);
+                        best_s, best_n, norm, leaf_sum, leaf_st, leaf_ln, S.leaves());
         wlo = __dadd_rn(lo, __dmul_rn(w, (double)best_s));          // histclip.py:214-219
         whi = __dadd_rn(lo, __dmul_rn(w, (double)(best_s + best_n)));
       } else {
@@ -481,8 +511,7 @@ static const double* hist_table(int b, cudaStream_t s, std::string& err) {
 int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b, int aux,
                     uint8_t* packed, double* xmin, double* xmax, int32_t* info0, int32_t* info1,
                     double* norm, int32_t* status, cudaStream_t s, std::string& err, bool apprx) {
-  if (b > 4096) { err = "hist-brute with b > 4096 is not supported by the B200 path"; return EQ4_EUNSUPPORTED; }
-  if (apprx && b > 256) { err = "hist-apprx with b > 256 is not supported by the B200 path"; return EQ4_EUNSUPPORTED; }
+  if (b > 65535) { err = "hist with b > 65535 is not supported by the B200 path"; return EQ4_EUNSUPPORTED; }
   const double* U = hist_table(b, s, err);
   if (!U) return EQ4_ECUDA;
   HistParams p;
@@ -495,9 +524,14 @@ int eq4_hist_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int b
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const HistSlice SS{b, (int)dim, (int)std::min<int64_t>(b, dim)};
+  HistSlice SS{b, (int)dim, (int)std::min<int64_t>(b, dim), false};
+  if (SS.bytes() > (size_t)max_optin / 2) SS.wide = true;   // wide rows stay in global memory
+  p.wide = SS.wide ? 1 : 0;
   const size_t per = SS.bytes();
-  if (per > (size_t)max_optin) { err = "hist-brute: row does not fit in shared memory"; return EQ4_EUNSUPPORTED; }
+  if (per > (size_t)max_optin) {
+    err = "hist: the b-bin tables of a row do not fit in shared memory (b too large)";
+    return EQ4_EUNSUPPORTED;
+  }
   const int nw = (int)std::max<size_t>(1, std::min<size_t>(HIST_NW, max_optin / per));
   const size_t smem = (size_t)nw * per;
   auto kern = apprx ? k_hist<true> : k_hist<false>;

@@ -23,6 +23,7 @@
 #include "../../include/eq4.h"
 #include "eq4_device.cuh"
 #include "eq4_internal.h"
+#include "eq4_np.cuh"
 
 namespace eq4 {
 
@@ -30,7 +31,6 @@ constexpr int KM_THREADS = 128;
 constexpr int KM_WARPS = KM_THREADS / 32;
 constexpr int KM_K = 16;
 constexpr int KM_COL = 33;
-constexpr int KM_MAX_D = 256;
 
 struct KMParams {
   const float* x;
@@ -48,75 +48,19 @@ struct KMLane {
   __device__ __forceinline__ double v(int k) const { return (double)xs[k * KM_COL]; }
 };
 
-// numpy leaf over members [s0, s0 + n) of the cluster-sorted index column perm
-// (perm holds each cluster's members in element order: a stable counting sort)
-__device__ __forceinline__ double km_sorted_leaf(const KMLane& L, const uint8_t* perm, int s0, int n) {
-  auto f = [&](int i) { return L.v(perm[(s0 + i) * 32]); };
-  if (n < 8) {
-    double res = 0.0;
-    for (int i = 0; i < n; i++) res = __dadd_rn(res, f(i));
-    return res;
-  }
-  double r0 = f(0), r1 = f(1), r2 = f(2), r3 = f(3), r4 = f(4), r5 = f(5), r6 = f(6), r7 = f(7);
-  const int nf = n - (n % 8);
-  int i = 8;
-  for (; i < nf; i += 8) {
-    r0 = __dadd_rn(r0, f(i));     r1 = __dadd_rn(r1, f(i + 1));
-    r2 = __dadd_rn(r2, f(i + 2)); r3 = __dadd_rn(r3, f(i + 3));
-    r4 = __dadd_rn(r4, f(i + 4)); r5 = __dadd_rn(r5, f(i + 5));
-    r6 = __dadd_rn(r6, f(i + 6)); r7 = __dadd_rn(r7, f(i + 7));
-  }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
-                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
-  for (; i < n; i++) res = __dadd_rn(res, f(i));
-  return res;
-}
-
-// members.mean() of the m members at perm[s0 ..]: 0.0 + pairwise sum / m
-__device__ __forceinline__ double km_sorted_mean(const KMLane& L, const uint8_t* perm, int s0, int m) {
-  double s;
-  if (m <= 128) {
-    s = km_sorted_leaf(L, perm, s0, m);
-  } else {
-    int n2 = m / 2;
-    n2 -= n2 % 8;
-    s = __dadd_rn(km_sorted_leaf(L, perm, s0, n2), km_sorted_leaf(L, perm, s0 + n2, m - n2));
-  }
+// members.mean() of the m members at perm[s0 ..] (perm holds each cluster's members in
+// element order: a stable counting sort): 0.0 + numpy pairwise sum / m (eq4_np.cuh)
+__device__ __forceinline__ double km_sorted_mean(const KMLane& L, const uint16_t* perm, int s0, int m) {
+  const double s = np_pw([&](int i) { return L.v(perm[(s0 + i) * 32]); }, 0, m);
   return __ddiv_rn(__dadd_rn(0.0, s), (double)m);
 }
 
-// np.sum((v - c[a])**2): pairwise over the d squared errors (d <= 256: two leaves max)
-__device__ __forceinline__ double km_sse_leaf(const KMLane& L, const double* cl, int a0, int n) {
-  auto f = [&](int k) {
+// np.sum((v - c[a])**2): numpy's pairwise order over the d squared errors (eq4_np.cuh)
+__device__ __forceinline__ double km_sse(const KMLane& L, const double* cl, int d) {
+  return np_sum([&](int k) {
     const double e = __dsub_rn(L.v(k), cl[L.a[k * 32]]);
     return __dmul_rn(e, e);
-  };
-  if (n < 8) {
-    double res = 0.0;
-    for (int i = 0; i < n; i++) res = __dadd_rn(res, f(a0 + i));
-    return res;
-  }
-  double r0 = f(a0), r1 = f(a0 + 1), r2 = f(a0 + 2), r3 = f(a0 + 3);
-  double r4 = f(a0 + 4), r5 = f(a0 + 5), r6 = f(a0 + 6), r7 = f(a0 + 7);
-  const int nf = n - (n % 8);
-  int i = 8;
-  for (; i < nf; i += 8) {
-    r0 = __dadd_rn(r0, f(a0 + i));     r1 = __dadd_rn(r1, f(a0 + i + 1));
-    r2 = __dadd_rn(r2, f(a0 + i + 2)); r3 = __dadd_rn(r3, f(a0 + i + 3));
-    r4 = __dadd_rn(r4, f(a0 + i + 4)); r5 = __dadd_rn(r5, f(a0 + i + 5));
-    r6 = __dadd_rn(r6, f(a0 + i + 6)); r7 = __dadd_rn(r7, f(a0 + i + 7));
-  }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
-                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
-  for (; i < n; i++) res = __dadd_rn(res, f(a0 + i));
-  return res;
-}
-
-__device__ __forceinline__ double km_sse(const KMLane& L, const double* cl, int d) {
-  if (d <= 128) return __dadd_rn(0.0, km_sse_leaf(L, cl, 0, d));
-  int n2 = d / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(0.0, __dadd_rn(km_sse_leaf(L, cl, 0, n2), km_sse_leaf(L, cl, n2, d - n2)));
+  }, d);
 }
 
 // argmin_j |v - c_j| (first minimum), assignments to L.a, per-cluster counts (counted in
@@ -149,8 +93,8 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
   const int d = p.d;
   float* xs = reinterpret_cast<float*>(ws);
   uint8_t* abuf = ws + (((size_t)d * KM_COL * 4 + 15) & ~(size_t)15);
-  uint8_t* pbuf = abuf + (size_t)d * 32;                                     // cluster-sorted indices
-  int* obuf = reinterpret_cast<int*>(pbuf + (((size_t)d * 32 + 15) & ~(size_t)15));   // [16][32] offsets
+  uint16_t* pbuf = reinterpret_cast<uint16_t*>(abuf + (((size_t)d * 32 + 15) & ~(size_t)15));   // sorted indices
+  int* obuf = reinterpret_cast<int*>(pbuf + (((size_t)d * 32 + 7) & ~(size_t)7));      // [16][32] offsets
   uint8_t* out_base = reinterpret_cast<uint8_t*>(obuf + KM_K * 32);
   const int ab = p.aux == EQ4_AUX_FP16 ? 2 : 4;
   const int64_t nblk = (p.rows + 31) / 32;
@@ -167,7 +111,7 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
     KMLane L;
     L.xs = xs + lane;
     L.a = abuf + lane;
-    uint8_t* perm = pbuf + lane;
+    uint16_t* perm = pbuf + lane;
     int* offs = obuf + lane;
     double c[KM_K];
     int iters = -1;
@@ -235,7 +179,7 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
             for (int k = 0; k < d; k++) {
               const int j = L.a[k * 32];
               const int pos = offs[j * 32];
-              perm[pos * 32] = (uint8_t)k;
+              perm[pos * 32] = (uint16_t)k;
               offs[j * 32] = pos + 1;
             }
           }
@@ -329,18 +273,14 @@ using namespace eq4;
 
 int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int aux, uint8_t* out,
                       int32_t* iters, int32_t* status, cudaStream_t s, std::string& err) {
-  if (dim > KM_MAX_D) {
-    err = "kmeans with dim > 256 is not supported by the B200 path";
-    return EQ4_EUNSUPPORTED;
-  }
   KMParams p;
   p.x = x; p.rows = rows; p.ld = ld; p.d = (int)dim; p.aux = aux;
   p.half = (int)((dim + 1) / 2);
   p.stride = KM_K * (aux == EQ4_AUX_FP16 ? 2 : 4) + p.half;
   p.out = out; p.iters = iters; p.status = status;
   // staged rows, assignments, cluster-sorted indices, offsets, packed tile
-  size_t wb = (((size_t)dim * KM_COL * 4 + 15) & ~(size_t)15) + (size_t)dim * 32 +
-              (((size_t)dim * 32 + 15) & ~(size_t)15) + (size_t)KM_K * 32 * 4 + (size_t)32 * p.stride + 32;
+  size_t wb = (((size_t)dim * KM_COL * 4 + 15) & ~(size_t)15) + (((size_t)dim * 32 + 15) & ~(size_t)15) +
+              (((size_t)dim * 32 * 2 + 15) & ~(size_t)15) + (size_t)KM_K * 32 * 4 + (size_t)32 * p.stride + 32;
   p.warp_bytes = (wb + 15) & ~(size_t)15;
   int dev = 0, sms = 0, per_sm = 0, max_optin = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -359,6 +299,10 @@ int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_kmeans_rows, w * 32, sm_w);
     if (e != cudaSuccess) { err = std::string("k_kmeans_rows setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
     if (blocks * w > best_warps) { best_warps = blocks * w; nw = w; per_sm = blocks; }
+  }
+  if (best_warps == 0) {
+    err = "kmeans: a warp's 32 staged rows of dim " + std::to_string(dim) + " do not fit in shared memory";
+    return EQ4_EUNSUPPORTED;
   }
   const size_t smem = p.warp_bytes * nw;
   e = cudaFuncSetAttribute(k_kmeans_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

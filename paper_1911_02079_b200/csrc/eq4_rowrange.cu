@@ -50,6 +50,7 @@ struct RRParams {
   double aciq_const; // clipping.py:125-134: 5.03 (laplacian) or the caller's gaussian_constant
   double gss_tol;    // clipping.py:70 tol (default 1e-4)
   int staged;
+  int direct;        // wide rows: packed rows written straight to global (no staging tile)
   int vec4;          // rows 16-byte aligned (d % 4 == 0, ld % 4 == 0, aligned base)
   size_t warp_bytes;
 };
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
     // codes (uniform.py:60-80) + packed row (packed.py:68-83), staged then copied out
     uint8_t* out_tile = out_base + (((uintptr_t)p.packed + (size_t)row0 * p.stride) & 15);
     if (rvalid) {
-      uint8_t* orow = out_tile + (size_t)lane * p.stride;
+      uint8_t* orow = p.direct ? p.packed + (size_t)row * p.stride : out_tile + (size_t)lane * p.stride;
       const bool degenerate = bad || hi == lo;
       const CodeParams cp = make_code_params(degenerate ? 0.0 : lo, degenerate ? 0.0 : hi);
       // Branch-free fp32 codes: s = sat((x - lo) / (hi - lo)) clamps below lo / above hi
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
     }
     __syncwarp();
     // warp copy of the staged packed rows (16-byte stores where aligned)
-    {
+    if (!p.direct) {
       uint8_t* dst = p.packed + (size_t)row0 * p.stride;
       const int nbytes = nrows * p.stride;
       int head = (int)((16 - ((uintptr_t)dst & 15)) & 15);
@@ -402,7 +403,9 @@ int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, i
   p.staged = dim <= RR_MAX_STAGED;
   p.vec4 = (dim % 4 == 0) && (ld % 4 == 0) && (((uintptr_t)x & 15) == 0);
   const size_t xs_bytes = p.staged ? (size_t)dim * RR_COL * 4 : 0;
-  p.warp_bytes = ((xs_bytes + 15) & ~(size_t)15) + (((size_t)32 * p.stride + 32 + 15) & ~(size_t)15);
+  p.direct = (size_t)32 * p.stride > 24 * 1024;   // wide rows: no per-warp staging tile
+  p.warp_bytes = ((xs_bytes + 15) & ~(size_t)15) +
+                 (p.direct ? 0 : (((size_t)32 * p.stride + 32 + 15) & ~(size_t)15));
   p.warp_bytes = (p.warp_bytes + 15) & ~(size_t)15;
   const size_t smem = p.warp_bytes * RR_WARPS;
   auto kern = method == EQ4_METHOD_ACIQ ? k_rowrange<EQ4_METHOD_ACIQ> : k_rowrange<EQ4_METHOD_GSS>;

@@ -69,5 +69,22 @@ def test_hist_apprx_api_and_counters():
     c = eq.WorkCounters()
     eq.row_clip_range("hist-apprx", np.full(9, 2.5, np.float32), b=40, counters=c)
     assert (c.candidate_evals, c.bin_visits) == (1, 40)
-    with pytest.raises(ValueError, match="not supported"):
-        eq.hist_apprx_search(x[0], 300)
+    h = eq.hist_apprx_search(x[0], 300)          # b > 256: numpy leaves beyond two
+    o = oracle.hist_apprx_search(x[0], 300)
+    assert (h.start_bin, h.nbins_selected) == (o.start_bin, o.nbins_selected)
+
+
+@pytest.mark.parametrize("b", [249, 250, 253, 255, 257, 300, 400, 1000])
+def test_hist_apprx_pairwise_leaves(b):
+    """b in 249..255 (the right half of 129..135 terms splits again), and b > 256: windows
+    identical to the oracle's except where its walk meets a 1e-12 near-tie, norms within
+    1e-12."""
+    x = rng.mixed_table(300, 64, b)
+    p, rr = eq.quantize_pack_table4(torch.from_numpy(x).cuda(), "hist-apprx", "fp16", b, with_rows=True)
+    st, ns, nm = rr.info0.cpu().numpy(), rr.info1.cpu().numpy(), rr.norm.cpu().numpy()
+    for i, row in enumerate(x):
+        o, gap = oracle.hist_apprx_gap(row, b)
+        if (st[i], ns[i]) != (o.start_bin, o.nbins_selected):
+            assert gap <= 1e-12, (b, i)
+            continue
+        assert nm[i] == pytest.approx(o.norm, rel=1e-12, abs=1e-300), (b, i)

@@ -50,12 +50,30 @@ def test_kmeans_random_vs_oracle(rows, d, gen, aux):
     assert np.array_equal(it.cpu().numpy(), its)
 
 
-def test_kmeans_wide_rows_unsupported_and_nonfinite():
-    with pytest.raises(ValueError, match="not supported"):
-        eq.quantize_table(np.ones((2, 300), np.float32) * np.arange(300, dtype=np.float32), "kmeans")
+def test_kmeans_nonfinite():
     from paper_1911_02079_b200.codebook import kmeans_rows
 
     x = torch.randn(64, 32, device="cuda")
     x[5, 3] = float("nan")
     with pytest.raises(ValueError, match="non-finite"):
         kmeans_rows(x, "fp16")
+
+
+@pytest.mark.parametrize("d,rows", [(249, 64), (250, 64), (255, 40), (257, 40), (300, 40), (640, 16), (1000, 8)])
+def test_kmeans_pairwise_leaves_and_wide_rows(d, rows):
+    """Rows whose SSE / cluster-mean sums split into more than two numpy leaves (d or a
+    cluster of 249..255 elements: the right half of 129..135 splits again) and rows wider
+    than 256: codebooks, indices and Lloyd rounds bit-exact against the oracle."""
+    from paper_1911_02079_b200.codebook import kmeans_rows
+
+    x = rng.mixed_table(rows, d, d)
+    x[0, : d - 3] = x[0, 0]            # one cluster holding all but 3 elements
+    x[1, : d // 2] = 1.0 + np.arange(d // 2, dtype=np.float32) * 1e-6
+    for aux in ("fp16", "fp32"):
+        it = torch.empty(rows, dtype=torch.int32, device="cuda")
+        payload = kmeans_rows(torch.from_numpy(x).cuda(), aux, iters=it).cpu().numpy()
+        q = CodebookQuantTable.from_payload(payload, rows, d, aux)
+        books, idx, its = oracle.kmeans_table(x, aux)
+        assert np.array_equal(q.codebooks.view(np.uint8), books.view(np.uint8)), (d, aux)
+        assert np.array_equal(q.indices, idx), (d, aux)
+        assert np.array_equal(it.cpu().numpy(), its), (d, aux)
