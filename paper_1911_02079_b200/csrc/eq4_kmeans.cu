@@ -40,12 +40,14 @@ struct KMParams {
   int32_t* iters;
   int32_t* status;
   size_t warp_bytes;
+  int staged;   // rows staged in shared memory as a [d][33] tile
 };
 
 struct KMLane {
-  const float* xs;   // this lane's column: element k at xs[k * KM_COL]
+  const float* xs;   // this lane's row: element k at xs[k * ks] (staged column or global row)
+  int ks;
   uint8_t* a;        // assignments, element k at a[k * 32]
-  __device__ __forceinline__ double v(int k) const { return (double)xs[k * KM_COL]; }
+  __device__ __forceinline__ double v(int k) const { return (double)xs[(size_t)k * ks]; }
 };
 
 // members.mean() of the m members at perm[s0 ..] (perm holds each cluster's members in
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
   unsigned char* ws = smem + (size_t)warp * p.warp_bytes;
   const int d = p.d;
   float* xs = reinterpret_cast<float*>(ws);
-  uint8_t* abuf = ws + (((size_t)d * KM_COL * 4 + 15) & ~(size_t)15);
+  uint8_t* abuf = ws + (p.staged ? (((size_t)d * KM_COL * 4 + 15) & ~(size_t)15) : 0);
   uint16_t* pbuf = reinterpret_cast<uint16_t*>(abuf + (((size_t)d * 32 + 15) & ~(size_t)15));   // sorted indices
   int* obuf = reinterpret_cast<int*>(pbuf + (((size_t)d * 32 + 7) & ~(size_t)7));      // [16][32] offsets
   uint8_t* out_base = reinterpret_cast<uint8_t*>(obuf + KM_K * 32);
@@ -105,11 +107,18 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
     const int nrows = (int)min((int64_t)32, p.rows - row0);
     for (int r = 0; r < nrows; r++) {
       const float* src = p.x + (row0 + r) * p.ld;
-      for (int k = lane; k < d; k += 32) xs[k * KM_COL + r] = __ldcs(src + k);
+      if (p.staged)
+        for (int k = lane; k < d; k += 32) xs[k * KM_COL + r] = __ldcs(src + k);
     }
     __syncwarp();
     KMLane L;
-    L.xs = xs + lane;
+    if (p.staged) {
+      L.xs = xs + lane;
+      L.ks = KM_COL;
+    } else {   // wide rows: read the row from global memory (L1/L2)
+      L.xs = p.x + (rvalid ? row : row0) * p.ld;
+      L.ks = 1;
+    }
     L.a = abuf + lane;
     uint16_t* perm = pbuf + lane;
     int* offs = obuf + lane;
@@ -119,7 +128,7 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
     if (rvalid) {
       double lo = L.v(0), hi = lo;
       for (int k = 0; k < d; k++) {
-        const float f = L.xs[k * KM_COL];
+        const float f = L.xs[(size_t)k * L.ks];
         bad |= !isfinite(f);
         const double x = (double)f;
         lo = x < lo ? x : lo;
@@ -279,7 +288,10 @@ int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int
   p.stride = KM_K * (aux == EQ4_AUX_FP16 ? 2 : 4) + p.half;
   p.out = out; p.iters = iters; p.status = status;
   // staged rows, assignments, cluster-sorted indices, offsets, packed tile
-  size_t wb = (((size_t)dim * KM_COL * 4 + 15) & ~(size_t)15) + (((size_t)dim * 32 + 15) & ~(size_t)15) +
+  // rows whose staged [d][33] tile would take more than half the shared memory are read
+  // from global memory instead
+  p.staged = (size_t)dim * KM_COL * 4 <= 96 * 1024;
+  size_t wb = (p.staged ? (((size_t)dim * KM_COL * 4 + 15) & ~(size_t)15) : 0) + (((size_t)dim * 32 + 15) & ~(size_t)15) +
               (((size_t)dim * 32 * 2 + 15) & ~(size_t)15) + (size_t)KM_K * 32 * 4 + (size_t)32 * p.stride + 32;
   p.warp_bytes = (wb + 15) & ~(size_t)15;
   int dev = 0, sms = 0, per_sm = 0, max_optin = 0;

@@ -72,6 +72,8 @@ def test_kmeans_pairwise_leaves_and_wide_rows(d, rows):
     for aux in ("fp16", "fp32"):
         it = torch.empty(rows, dtype=torch.int32, device="cuda")
         payload = kmeans_rows(torch.from_numpy(x).cuda(), aux, iters=it).cpu().numpy()
+        from paper_1911_02079_b200.codebook import CodebookQuantTable
+
         q = CodebookQuantTable.from_payload(payload, rows, d, aux)
         books, idx, its = oracle.kmeans_table(x, aux)
         assert np.array_equal(q.codebooks.view(np.uint8), books.view(np.uint8)), (d, aux)
