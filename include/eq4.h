@@ -81,7 +81,8 @@ int64_t eq4_packed_row_stride(int64_t dim, int aux);
  *               -1 constant row, -2 range error; HIST-BRUTE: start_bin;
  *               GSS: quant_mse evaluations (WorkCounters.loss_evals);
  *               HIST-APPRX: start_bin (info1 nbins_selected, norm the window norm)
- *   info1       GREEDY: (best_i << 16) | best_j; HIST-BRUTE: nbins_selected
+ *   info1       GREEDY: (best_i << 16) | best_j (best_i alone for b > 65535);
+ *               HIST-BRUTE: nbins_selected
  *   norm        HIST-BRUTE window norm (HistWindow.norm); unused otherwise
  *   status      device int32, EQ4_STATUS_* bits OR-ed in by the kernels
  */

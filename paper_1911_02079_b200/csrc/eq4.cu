@@ -1383,7 +1383,8 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       // candidate's xmin is x0 + nl*step, which is +0.0 for nl = 0 and x0 = -0.0
       lo = (bi == 0 && bj == 0) ? R.x0 : __dadd_rn(R.x0, __dmul_rn((double)bi, R.step));
       hi = bj == 0 ? R.x1 : __dsub_rn(R.x1, __dmul_rn((double)bj, R.step));
-      if (rvalid && !bad && mn != mx) { info0 = iters; info1 = (bi << 16) | bj; }
+      // (best_i << 16) | best_j; best_i alone when b > 65535 (it would not fit)
+      if (rvalid && !bad && mn != mx) { info0 = iters; info1 = p.b > 65535 ? bi : ((bi << 16) | bj); }
     }
     const int blk_rows = (int)min((int64_t)RPW, p.rows - row0);
     const size_t gofs = (size_t)row0 * p.stride;
@@ -2289,7 +2290,8 @@ static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t
     return rc == EQ4_OK ? rc : fail(rc, err);
   }
   if (method == EQ4_METHOD_GREEDY) {
-    if (b > 65535) return fail(EQ4_EUNSUPPORTED, "b > 65535 is not supported by the B200 path");
+    // W * alpha must stay exact in fp32 (kw_of) and 15 b representable on the Y grid
+    if (b > 262143) return fail(EQ4_EUNSUPPORTED, "GREEDY with b > 262143 is not supported by the B200 path");
     // Loop condition (clipping.py:180) at iteration it, i.e. after it moves
     // (nl + nr == it): exactly  (it + b(1-r)) * step < x1 - x0  <=>  it < T with
     // T = b - b(1-r).  For it <= T - 1 the two sides differ by >= one step,

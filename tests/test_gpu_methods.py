@@ -128,3 +128,14 @@ def test_method_api_single_rows_and_counters():
     c = eq.WorkCounters()
     eq.quantize_table(x, "gss", counters=c)
     assert c.loss_evals == sum(oracle.clip_range_rowwise(r, "gss")[2] for r in x)
+
+
+def test_sharded_table_default_device_path():
+    """sharding.quantize_pack_sharded(..., "table") on one rank: the device range + the
+    given-range codec (eq4_quantize_rows) + eq4_pack equal the fused TABLE launch / oracle."""
+    from paper_1911_02079_b200.sharding import quantize_pack_sharded
+
+    x = rng.mixed_table(2000, 40, 5)
+    for aux in ("fp16", "fp32"):
+        got = quantize_pack_sharded(x, "table", aux).cpu().numpy()
+        assert np.array_equal(got, oracle.quantize_pack_table(x, "table", aux=aux).packed), aux

@@ -70,3 +70,11 @@ def test_hist_wide_rows_and_many_bins(method, b, d):
             o, gap = oracle.hist_apprx_gap(row, b)
             if (st[i], ns[i]) != (o.start_bin, o.nbins_selected):
                 assert gap <= 1e-12, i
+
+
+@pytest.mark.parametrize("b,r", [(70000, 0.001), (100000, 0.0004)])
+def test_greedy_many_bins(b, r):
+    """b beyond 16 bits (round 1 refused b > 65535): a walk of ~b*r steps on the fine grid."""
+    x = rng.mixed_table(64, 32, b)
+    rr, want = _check(x, "greedy", "fp16", b=b, r=r)
+    assert np.array_equal(rr.info0.cpu().numpy(), want.info0)

@@ -186,6 +186,58 @@ def test_row_sharded_quantization_over_gloo():
     assert tmax == float(world)
 
 
+def _sharded_table_worker(rank, world, port, x, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1911_02079_b200.sharding import quantize_pack_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def cpu_range(rows):          # the shard's own min / max (the oracle's TABLE range)
+            t = oracle.quantize_pack_table(rows, "table", aux="fp16")
+            return float(t.xmin[0]), float(t.xmax[0])
+
+        def cpu_quantize(rows, lo, hi, aux):   # quantize_table_uniform against one ClipRange
+            rows = np.ascontiguousarray(rows, np.float32)
+            out = []
+            for row in rows:
+                c, s, b = oracle.quantize_uniform(row, lo, hi, 4, aux)
+                out.append(oracle.pack_table4(c[None], [s], [b], aux))
+            return torch.from_numpy(np.concatenate(out))
+
+        full = quantize_pack_sharded(x, "table", "fp16", table_range=cpu_range, compute_range=cpu_quantize)
+        if rank == 0:
+            q.put(full.numpy().tobytes())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_sharded_table_uses_the_global_range_over_gloo():
+    """TABLE (clipping.py:64-67) spans the whole table: the shards all-reduce their ranges and
+    quantize against the global one -- the gathered bytes equal the unsharded oracle's."""
+    import torch.multiprocessing as mp
+
+    from oracle import rng
+
+    x = rng.mixed_table(301, 24, 9)
+    x[5, 3] = 40.0        # the global max sits in rank 0's shard,
+    x[250, 7] = -35.0     # the global min in rank 1's
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_table_worker, args=(r, world, port, x, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == oracle.quantize_pack_table(x, "table", aux="fp16").packed.tobytes()
+
+
 def test_pooled_query_validation_matches_reference(ref):
     from embquant.packed import PooledQuery as RefQuery
 
