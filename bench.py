@@ -126,6 +126,60 @@ def cpu_reference_rate(rows_sample: int, seed: int = 1911, steps: int = 1, warmu
     return rows_sample / t, nthreads, t
 
 
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _ref_chunk(args):
+    """One chunk through the unmodified reference package (baseline/_ref): packed bytes."""
+    path, x, method = args
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import embquant
+
+    t = embquant.EmbeddingTable(x)
+    q = embquant.quantize_table(t, method, 4, AUX, b=B, r=R)
+    return embquant.pack_table4(q).buffer.tobytes()
+
+
+def python_reference_rate(rows: int = 10_000, seed: int = 1911):
+    """Context only: the UNMODIFIED Python reference -- the reference
+    package pip-installed into baseline/_ref from the reference tree -- timed on the bench's
+    mixed generator, GREEDY b=200 r=0.16 fp16, one process per host core over row chunks.
+    Its bytes are checked against the oracle.  None when baseline/_ref is absent."""
+    import multiprocessing as mp
+
+    import oracle
+    from oracle import rng
+
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "embquant")):
+        return None
+    x = rng.mixed_table(rows, DIM, seed)
+    procs = os.cpu_count() or 1
+    chunks = [(path, x[i::procs].copy(), "greedy") for i in range(procs)]
+    with mp.get_context("spawn").Pool(procs) as pool:
+        pool.map(_ref_chunk, [(path, x[:procs], "greedy")] * procs)   # warm the workers
+        t0 = time.perf_counter()
+        parts = pool.map(_ref_chunk, chunks)
+        t = time.perf_counter() - t0
+    want = oracle.quantize_pack_table(x, "greedy", B, R, AUX)
+    stride = (DIM + 1) // 2 + 4
+    got = np.empty((rows, stride), np.uint8)
+    for i, part in enumerate(parts):
+        got[i::procs] = np.frombuffer(part, np.uint8).reshape(-1, stride)
+    return {"value": rows / t, "unit": "rows/s", "cores": procs, "kind": "reference",
+            "sample": f"{rows} rows x {DIM} mixed, GREEDY b=200 r=0.16 fp16, unmodified reference "
+                      f"package (baseline/_ref) in {procs} processes, {t:.2f} s",
+            "bytes_match_oracle": bool(np.array_equal(got.reshape(-1), want.packed))}
+
+
 def parity_report(eq, torch, dev, x, out, method, b, sample=0, x_host=None, nthreads=0):
     """Check a timed launch's packed bytes against the CPU oracle on the same table.
 
@@ -219,6 +273,7 @@ def run_reference(args, rank: int):
                                f"each step a {sample}-row sample on the host",
                    "rows": ROWS, "dim": DIM, "b": B, "r": R, "aux": AUX},
         "cpu_baseline": {"value": rate, "unit": "rows/s", "cores": cores, "kind": "port",
+                         "cpu_model": _cpu_model(),
                          "sample": f"{sample} rows x {DIM} of the mixed generator "
                                    "(oracle/eq4_oracle.c restatement of the reference, "
                                    f"{cores} OpenMP threads)"},
@@ -340,6 +395,13 @@ def run_ours(args, rank: int, world: int):
     props = torch.cuda.get_device_properties(dev)
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     fp32_peak = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
+    peak_source = ("derived: SMs x 128 FP32 lanes x 2 x sm_max_mhz (no measured FP32 figure found)")
+    mp = os.path.join(ROOT, "profiles", "r02_fp32_peak.json")
+    if os.path.exists(mp):
+        with open(mp) as f:
+            fp32_peak = float(json.load(f)["peak_used"])
+        peak_source = ("measured: profiles/r02_fp32_peak.json, FFMA2 throughput of this B200 model "
+                       "(tools/microbench/fp32_peak.cu; MEASURED_PEAKS.json has no FP32 figure)")
     achieved = flop_per_step / (ms * 1e-3) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -350,8 +412,13 @@ def run_ours(args, rank: int, world: int):
     if not args.no_cpu and world == 1:   # the reported CPU baseline: rank 0 at N = 1 only
         rate, cores, t = cpu_reference_rate(args.cpu_rows)
         cpu = {"value": rate, "unit": "rows/s", "cores": cores, "kind": "port",
+               "cpu_model": _cpu_model(),
                "sample": f"{args.cpu_rows} rows x {DIM} mixed, GREEDY b=200 r=0.16 fp16 "
                          f"(oracle C restatement, {cores} threads, {t:.1f} s)"}
+        try:
+            cpu["python_reference_context"] = python_reference_rate()
+        except Exception as ex:   # context only: never fails the bench
+            cpu["python_reference_context"] = {"error": str(ex).splitlines()[0][:200]}
     line = {
         "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -365,8 +432,7 @@ def run_ours(args, rank: int, world: int):
         "input_GBps": world * rows * DIM * 4 / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp32_peak, "traffic": traffic,
-                     "peak_source": "derived: SMs x 128 FP32 lanes x 2 x sm_max_mhz "
-                                    "(MEASURED_PEAKS.json has no FP32 figure)",
+                     "peak_source": peak_source,
                      "work": f"13 FLOP x d x loss evaluations ({evals} evals/step)",
                      "hbm_floor_ms": bytes_per_step / (float(peaks.get('hbm_gbs', 6546.9)) * 1e9) * 1e3},
         "cpu_baseline": cpu,
@@ -487,7 +553,7 @@ def secondary(eq, workloads, torch, dev, peaks, fp32_peak, check=True):
     del x, kout, kit
     # config 5a: GREEDY d-sweep, rows = 2^30 / (4 d): 1 GiB of fp32 per table
     sweep = {}
-    for d in (16, 32, 64, 128, 256, 512, 1024, 2048):
+    for d in (16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192):
         rows = (1 << 30) // (4 * d)
         x = workloads.gaussian_table(rows, d, 7, device=dev)
         par = {} if check else None
