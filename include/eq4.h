@@ -247,7 +247,9 @@ int eq4_quant_mse_rows(const void *x, int x_is_f64, int64_t rows, int64_t dim, i
  * band), out[1] = rows whose codes took the float64 codec, out[2] = comparisons
  * settled by counting the elements within reach of a rounding boundary (inside
  * the band for d misrounded elements, outside the one for 2), out[3] = of those,
- * escalated to a float64 re-decision (more than 2 such elements on a side).
+ * escalated to a float64 re-decision (more than 2 such elements on a side),
+ * out[4] = rows the GREEDY screening kernel deferred to the exact kernel
+ * (vector rows: d % 4 == 0 and 16-byte aligned).  out holds 5 entries.
  * reset != 0 zeroes them after the read.  Synchronous (device-wide). */
 int eq4_diag_counters(int64_t *out, int reset);
 

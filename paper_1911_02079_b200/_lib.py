@@ -149,7 +149,8 @@ def diag_counters(reset: bool = False) -> dict:
     """GREEDY rare-path counters of the current device (eq4_diag_counters)."""
     import numpy as np
 
-    out = np.zeros(4, np.int64)
+    out = np.zeros(5, np.int64)
     check(load().eq4_diag_counters(out.ctypes.data_as(ctypes.c_void_p), int(bool(reset))))
     return {"exact_redecisions": int(out[0]), "exact_code_rows": int(out[1]),
-            "near_count_checks": int(out[2]), "near_count_escalations": int(out[3])}
+            "near_count_checks": int(out[2]), "near_count_escalations": int(out[3]),
+            "deferred_rows": int(out[4])}

@@ -83,7 +83,8 @@ enum { M_ASYM = 0, M_GREEDY = 1 };
 // boundary), [2] comparisons resolved by counting near-boundary elements
 // (near_escalate), [3] of those, escalated to the exact re-decision (more than
 // 2 elements of a side within reach of a boundary).  Only the rare paths touch them.
-__device__ unsigned long long g_diag[4];
+// [4] rows the screening kernel deferred to the exact kernel (k_greedy_fast).
+__device__ unsigned long long g_diag[5];
 
 struct Params {
   const float* x;
@@ -114,6 +115,12 @@ struct Params {
   float kmisx;        // extra band per W^2 when every element of a side may misround
   float c1;           // Yh quantisation band: 4.2 * delta * sqrt(d)
   float c0;           // 2.1 * d * delta^2
+  // GREEDY two-pass scheme (vector rows): the screening kernel appends the rows it
+  // defers to dlist (indices into this launch's rows) and counts them in *dcount;
+  // k_greedy with list != 0 then runs exactly those rows
+  uint32_t* dlist;
+  int* dcount;
+  int list;
 };
 
 // Copy nbytes from shared src to global dst; src and dst agree modulo 16.
@@ -558,7 +565,8 @@ k_asym(const Params p) {
 // Rarely-touched float64 state of one row's walk, kept in shared memory so the
 // hot loop holds only the row slice (Yh) and a few scalars in registers.
 struct RowShared {
-  double x0, x1, step, min_steps, kY, kY2, best_ex, elo, ehi, pad;
+  double x0, x1, step, min_steps, kY, kY2, best_ex, elo, ehi;
+  int64_t rid;   // list mode: the row's index in the table
 };
 
 // Per-warp shared-memory slice of the GREEDY kernel.  Warps run independently
@@ -641,7 +649,7 @@ __device__ __forceinline__ f2_t fma2_rm(f2_t a, f2_t b, f2_t c) {
 }
 
 #ifndef G_UNROLL
-#define G_UNROLL 4
+#define G_UNROLL 16
 #endif
 constexpr int kGUnroll = G_UNROLL;   // float4 chunks per trip of the element loop
 
@@ -1045,8 +1053,8 @@ enum : unsigned { F_ACTIVE = 1, F_EXACT_ONLY = 2, F_BEST_EX = 4, F_ERR = 8 };
 // at a time by the whole warp with the bit-exact float64 restatement.
 template <int LPR, int E, bool VEC>
 __device__ __forceinline__ void exact_block(const Params& p, bool need_ex, int q, int gw, int W,
-                                            float SL, float SR, RowShared* rs, const float* xblk,
-                                            int64_t ld, int d, double* e2, double* leaf_sum,
+                                            float SL, float SR, RowShared* rs, const float* xr,
+                                            int d, double* e2, double* leaf_sum,
                                             int* leaf_st, int* leaf_ln, int& nl, int& nr, int& bi,
                                             int& bj, int& iters, unsigned& flags, float& Lbest,
                                             float& BLf, unsigned* wdiag) {
@@ -1059,7 +1067,9 @@ __device__ __forceinline__ void exact_block(const Params& p, bool need_ex, int q
     const ExactOut o = exact_decide<(E <= 16), WarpSliceG<LPR, E, VEC>::LEAVES>(
         &rs[lg], (double)__shfl_sync(FULL, nl, leader), (double)__shfl_sync(FULL, nr, leader),
         __shfl_sync(FULL, bi, leader), __shfl_sync(FULL, bj, leader),
-        (__shfl_sync(FULL, flags, leader) & F_BEST_EX) != 0, xblk + lg * ld, d, e2, leaf_sum, leaf_st,
+        (__shfl_sync(FULL, flags, leader) & F_BEST_EX) != 0,
+        reinterpret_cast<const float*>(__shfl_sync(FULL, reinterpret_cast<unsigned long long>(xr), leader)),
+        d, e2, leaf_sum, leaf_st,
         leaf_ln);
     if (lg == gw) {
       if (o.flags & 1) {
@@ -1109,18 +1119,22 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
   const int d = p.d;
   const int nv = valid_slots<LPR, E, VEC>(q, d);
   const float hh = 0.5f / ALPHA;
-  const int64_t nblocks = (p.rows + RPW - 1) / RPW;
+  // list mode: the rows the screening kernel deferred (dlist[0 .. *dcount)), each
+  // written on its own; otherwise blocks of RPW consecutive rows
+  const int64_t nlist = p.list ? (int64_t)*reinterpret_cast<volatile const int*>(p.dcount) : 0;
+  const int64_t nunits = p.list ? nlist : p.rows;
+  const int64_t nblocks = (nunits + RPW - 1) / RPW;
   const int nwb = (int)(blockDim.x >> 5);   // warps per block (fewer for wide rows)
   const int64_t wstride = (int64_t)gridDim.x * nwb;
 
   for (int64_t blk = (int64_t)blockIdx.x * nwb + warp; blk < nblocks; blk += wstride) {
-    const int64_t row0 = blk * RPW, row = row0 + gw;
-    const bool rvalid = row < p.rows;
+    const int64_t row0 = blk * RPW;
+    const bool rvalid = row0 + gw < nunits;
+    const int64_t row = p.list ? (rvalid ? (int64_t)p.dlist[row0 + gw] : 0) : row0 + gw;
     RowShared& R = rs[gw];
     // the raw rows stay in global memory (L1/L2-resident while the block is
     // searched): only the rare exact decisions and code fix-ups read them
-    const float* xblk = p.x + row0 * p.ld;
-    const float* xr = xblk + (rvalid ? gw : 0) * p.ld;
+    const float* xr = p.x + (rvalid ? row : (p.list ? 0 : row0)) * p.ld;
 
     float mn, mx;
     bool bad;
@@ -1249,7 +1263,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       if (q == 0) {
         R.x0 = x0; R.x1 = x1; R.step = step;
         R.min_steps = __dmul_rn(__dmul_rn((double)p.b, __dsub_rn(1.0, p.r)), step);  // :173
-        R.kY = kY; R.kY2 = kY * kY; R.best_ex = 0.0; R.elo = 0.0; R.ehi = 0.0;
+        R.kY = kY; R.kY2 = kY * kY; R.best_ex = 0.0; R.elo = 0.0; R.ehi = 0.0; R.rid = row;
       }
     }
     __syncwarp();
@@ -1324,7 +1338,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         if (cand < Lbest) { Lbest = cand; bi = nl; bj = nr; flags &= ~F_BEST_EX; }
         ++iters;
       }
-      exact_block<LPR, E, VEC>(p, need_ex, q, gw, p.b - it - 1, SL, SR, rs, xblk, p.ld, d, e2, leaf_sum,
+      exact_block<LPR, E, VEC>(p, need_ex, q, gw, p.b - it - 1, SL, SR, rs, xr, d, e2, leaf_sum,
                                leaf_st, leaf_ln, nl, nr, bi, bj, iters, flags, Lbest, BLf, wdiag);
       ++it;
     }
@@ -1368,7 +1382,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         }
       }
       if (__any_sync(FULL, need_ex))
-        exact_block<LPR, E, VEC>(p, need_ex, q, gw, W, SL, SR, rs, xblk, p.ld, d, e2, leaf_sum, leaf_st,
+        exact_block<LPR, E, VEC>(p, need_ex, q, gw, W, SL, SR, rs, xr, d, e2, leaf_sum, leaf_st,
                                  leaf_ln, nl, nr, bi, bj, iters, flags, Lbest, BLf, wdiag);
     }
 
@@ -1386,9 +1400,9 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       // (best_i << 16) | best_j; best_i alone when b > 65535 (it would not fit)
       if (rvalid && !bad && mn != mx) { info0 = iters; info1 = p.b > 65535 ? bi : ((bi << 16) | bj); }
     }
-    const int blk_rows = (int)min((int64_t)RPW, p.rows - row0);
+    const int blk_rows = (int)min((int64_t)RPW, nunits - row0);
     const size_t gofs = (size_t)row0 * p.stride;
-    uint8_t* out_tile = out_base + (((uintptr_t)p.packed + gofs) & 15);
+    uint8_t* out_tile = p.list ? out_base : out_base + (((uintptr_t)p.packed + gofs) & 15);
     emit_greedy<LPR, E, VEC>(p, ysl, nv, q, lo, hi, bi, bj, mn != mx,
                              rvalid && !bad && !(flags & F_ERR), rvalid, xr,
                              out_tile + gw * p.stride, codes_w + gw * D, wdiag);
@@ -1408,10 +1422,314 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       }
       __syncwarp();
     }
-    warp_copy_out(p.packed + gofs, out_tile, blk_rows * p.stride);
+    if (p.list) {   // scattered rows: each row's bytes to its own place
+      for (int t = lane; t < blk_rows * p.stride; t += 32) {
+        const int rr = t / p.stride;
+        p.packed[(size_t)rs[rr].rid * p.stride + (t - rr * p.stride)] = out_tile[t];
+      }
+    } else {
+      warp_copy_out(p.packed + gofs, out_tile, blk_rows * p.stride);
+    }
     __syncwarp();
   }
   if (lane < 4 && wdiag[lane]) atomicAdd(&g_diag[lane], (unsigned long long)wdiag[lane]);
+}
+
+// ---------------------------------------------------------------------------
+// GREEDY screening kernel (vector rows: d % 4 == 0, 16-byte aligned).
+// The same fp32 walk as k_greedy's phase A/B -- Y slice in shared memory,
+// packed pair evaluation, the error band on both sides of every comparison --
+// but without the float64 tier: a row whose walk meets a comparison inside the
+// band (after the near-boundary count of near_escalate), whose codes need the
+// float64 codec, or that the fast walk does not take at all (non-finite values,
+// a zero at its min or max -- numpy's signed-zero choice --, constant rows, rows
+// the reference's grid rounds coarsely, W < 1) is DEFERRED: its index goes to
+// p.dlist and k_greedy (list mode) redoes the whole row with the exact tier
+// right after on the same stream.  About 2% of the rows of the bench tables
+// are deferred.  Without the exact tier's calls, stack and float64 state the
+// kernel fits 4 warps per SMSP (k_greedy: 3 at 168 registers).
+// ---------------------------------------------------------------------------
+struct RowFast {
+  double x0, x1, step, min_steps;
+};
+
+template <int LPR, int E>
+struct FastSlice {
+  static constexpr int RPW = 32 / LPR;
+  __host__ __device__ static size_t rf_off() { return (size_t)E * 32 * 4; }   // after the E/4 x 32 float4 slice
+  __host__ __device__ static size_t out_off() { return (rf_off() + RPW * sizeof(RowFast) + 15) & ~(size_t)15; }
+  __host__ __device__ static size_t diag_off(int stride) {
+    return (out_off() + (size_t)RPW * stride + 32 + 15) & ~(size_t)15;
+  }
+  __host__ __device__ static size_t bytes(int stride) { return diag_off(stride) + 16; }
+};
+
+#ifdef EQ4_DBG
+#define GF_CHECK(cond, tag, v)                                                                  \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("GF_CHECK %s failed: blk %d thr %d val %lld\n", tag, blockIdx.x, threadIdx.x, (long long)(v)); \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define GF_CHECK(cond, tag, v) do {} while (0)
+#endif
+
+#ifndef GF_MINB
+#define GF_MINB 5
+#endif
+
+template <int LPR, int E>
+__global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fast(const Params p) {
+  using S = FastSlice<LPR, E>;
+  constexpr int RPW = S::RPW;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = lane / LPR, q = lane % LPR;
+  unsigned char* ws = smem + warp * S::bytes(p.stride);
+  float4* ys4 = reinterpret_cast<float4*>(ws);
+  const float4* ysl = ys4 + lane;
+  RowFast* rf = reinterpret_cast<RowFast*>(ws + S::rf_off());
+  uint8_t* out_base = ws + S::out_off();
+  unsigned* wdiag = reinterpret_cast<unsigned*>(ws + S::diag_off(p.stride));
+  if (lane < 4) wdiag[lane] = 0u;
+  __syncwarp();
+  const float hh = 0.5f / ALPHA;
+  const int64_t nblocks = (p.rows + RPW - 1) / RPW;
+  const int nwb = (int)(blockDim.x >> 5);
+  const int64_t wstride = (int64_t)gridDim.x * nwb;
+  unsigned ndefer = 0u;
+
+  for (int64_t blk = (int64_t)blockIdx.x * nwb + warp; blk < nblocks; blk += wstride) {
+    const int64_t row0 = blk * RPW, row = row0 + gw;
+    const bool rvalid = row < p.rows;
+    const float* xr = p.x + (row0 + (rvalid ? gw : 0)) * p.ld;
+    bool defer, active;
+    {
+      const float4* src = reinterpret_cast<const float4*>(xr) + q;
+      float lmn = INFINITY, lmx = -INFINITY;
+      f2_t sm2 = pk2(0.f, 0.f);   // NaN / Inf detector: a packed running sum
+#pragma unroll
+      for (int c = 0; c < E / 4; ++c) {
+        const float4 t = __ldg(src + LPR * c);
+        lmn = fminf(lmn, fminf(fminf(t.x, t.y), fminf(t.z, t.w)));
+        lmx = fmaxf(lmx, fmaxf(fmaxf(t.x, t.y), fmaxf(t.z, t.w)));
+        sm2 = add2(sm2, add2(pk2(t.x, t.y), pk2(t.z, t.w)));
+      }
+      float s0, s1;
+      upk2(sm2, s0, s1);
+      const float mn = group_min<LPR>(lmn), mx = group_max<LPR>(lmx);
+      const float sm = group_sum<LPR>(__fadd_rn(s0, s1));
+      // rows the fp32 walk does not take (clipping.py:163-165 and the band's premises)
+      const float M = fmaxf(fabsf(mn), fabsf(mx));
+      defer = rvalid && (!isfinite(sm) || mn == 0.f || mx == 0.f || !(mn < mx) || !(M <= 1e6f * (mx - mn)));
+      active = rvalid && !defer;
+      const double x0 = (double)mn, x1 = (double)mx;
+      const double step = __ddiv_rn(__dsub_rn(x1, x0), (double)p.b);                  // clipping.py:172
+      const double kY = active ? __ddiv_rn(15.0, step) : 0.0;
+      const double cY = 6755399441055744.0 * p.qY;   // Y + cY rounds Y to the qY grid
+#pragma unroll 4
+      for (int c = 0; c < E / 4; ++c) {
+        const float4 t = __ldg(src + LPR * c);
+        const float tv[4] = {t.x, t.y, t.z, t.w};
+        float y[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double Y = __dmul_rn(__dsub_rn((double)tv[k], x0), kY);
+          y[k] = (float)__dsub_rn(__dadd_rn(Y, cY), cY);
+        }
+        ys4[c * 32 + lane] = make_float4(y[0], y[1], y[2], y[3]);
+      }
+      GF_CHECK(S::diag_off(p.stride) + 16 <= S::bytes(p.stride), "bytes", S::bytes(p.stride));
+      GF_CHECK(row0 * p.ld + (int64_t)LPR * E <= p.rows * p.ld, "xread", row0);
+      if (q == 0) {
+        rf[gw].x0 = x0; rf[gw].x1 = x1; rf[gw].step = step;
+        rf[gw].min_steps = __dmul_rn(__dmul_rn((double)p.b, __dsub_rn(1.0, p.r)), step);   // :173
+      }
+    }
+    __syncwarp();
+    const float Wf0 = (float)p.b;                                                     // :174
+    float Lbest = group_sum<LPR>(eval_one_x2<E>(ysl, 0.f, -Wf0, kw_of(Wf0), hh));
+    int nl = 0, nr = 0, bi = 0, bj = 0;
+    float BLf = 15.f;                      // base of the L candidate, 15 * (nl + 1)
+    int it = 0;
+    {
+      // Phase A: iterations whose loop condition provably holds (it < it_exact_from) and
+      // whose width takes the shift evaluation (W >= 17): straight-line body, no float64
+      // test, no per-iteration vote but the near-boundary one.  kW of the next width and
+      // the square-root term of the band come off the decision's critical path:
+      // c1 sqrt(m) <= c1 (m / sqrt(S0) + sqrt(S0)) / 2 for any S0 > 0 (AM-GM), with S0 the
+      // previous iteration's loss scale -- an upper bound, so the band stays sound.
+      const int itA = max(0, min(p.it_exact_from, p.b - 17));
+      const float c1h = 0.5f * p.c1;
+      float kWn = kw_of((float)(p.b - 1));
+      float sq = sqrt_approx(fmaxf(Lbest, 1e-30f));
+      float rsq = __frcp_rn(sq) * 1.000001f;
+      for (; it < itA; ++it) {
+        const float Wf = (float)(p.b - it - 1);
+        const float kW = kWn;
+        kWn = kw_of(Wf - 1.f);
+        float aL, aR;
+        eval_pair_x2_shift<E>(ysl, BLf, -Wf, kW, hh, aL, aR);
+        float SL, SR;
+        group_sum_pair<LPR>(aL, aR, SL, SR);
+        const bool goL = SL < SR;                                                 // clipping.py:185
+        const float cand = goL ? SL : SR;
+        const float mall = fmaxf(fmaxf(SL, SR), Lbest);
+        const float band = __fmaf_rn(p.tau2, mall, __fmaf_rn(c1h, __fmaf_rn(mall, rsq, sq),
+                                                             __fmaf_rn(p.kmis * Wf, Wf, p.c0)));
+        const float gap = fminf(fabsf(SL - SR), fabsf(cand - Lbest));
+#ifdef G_NODECIDE   // development: timing without the band test
+        bool need = false;
+        const bool chk = false;
+        (void)gap; (void)band;
+#else
+        bool need = active && gap <= band;
+        const bool chk = active && !need && gap <= __fmaf_rn(p.kmisx * Wf, Wf, band);
+#endif
+        if (__any_sync(FULL, chk))
+          need |= near_escalate<LPR, E, true>(p, reinterpret_cast<const float*>(ys4), chk, q, gw, p.d, BLf,
+                                              Wf, bi, bj, wdiag);
+        defer |= need;
+        active = active && !need;
+        const bool mv = active && goL;
+        nl += mv;
+        nr += active && !goL;
+        BLf += mv ? 15.f : 0.f;
+        const bool better = active && cand < Lbest;                               // clipping.py:187,191
+        Lbest = better ? cand : Lbest;
+        bi = better ? nl : bi;
+        bj = better ? nr : bj;
+        sq = sqrt_approx(fmaxf(mall, 1e-30f));
+        rsq = __frcp_rn(sq) * 1.000001f;
+      }
+    }
+    for (;; ++it) {
+      if (active && it >= p.it_exact_from) {   // clipping.py:180 in float64 (earlier: provably true)
+        const RowFast& R = rf[gw];
+        const double lhs = __dadd_rn(__dadd_rn(R.x0, __dmul_rn((double)nl, R.step)), R.min_steps);
+        const double rhs = __dsub_rn(R.x1, __dmul_rn((double)nr, R.step));
+        active = lhs < rhs;
+      }
+      if (!__any_sync(FULL, active)) break;
+      const int W = p.b - it - 1;
+      if (W < 1) {   // widths the fp32 grid cannot take: the exact kernel walks on
+        defer |= active;
+        break;
+      }
+      const float Wf = (float)W;
+      float aL, aR;
+      if (W >= 17)   // codes move by at most one under the 15-shift
+        eval_pair_x2_shift<E>(ysl, BLf, -Wf, kw_of(Wf), hh, aL, aR);
+      else
+        eval_pair_x2<E>(ysl, BLf, -Wf, kw_of(Wf), hh, aL, aR);
+      float SL, SR;
+      group_sum_pair<LPR>(aL, aR, SL, SR);
+      const bool goL = SL < SR;                                                   // clipping.py:185
+      const float cand = goL ? SL : SR;
+      const float mall = fmaxf(fmaxf(SL, SR), Lbest);
+      const float band = p.tau2 * mall + p.c1 * sqrt_approx(mall) + (p.c0 + p.kmis * Wf * Wf);
+      const float gap = fminf(fabsf(SL - SR), fabsf(cand - Lbest));
+      bool need = active && gap <= band;
+      const bool chk = active && !need && gap <= __fmaf_rn(p.kmisx * Wf, Wf, band);
+      if (__any_sync(FULL, chk))
+        need |= near_escalate<LPR, E, true>(p, reinterpret_cast<const float*>(ys4), chk, q, gw, p.d, BLf,
+                                            Wf, bi, bj, wdiag);
+      if (need) {
+        defer = true;
+        active = false;
+      }
+      if (active) {
+        nl += goL;
+        nr += !goL;
+        BLf += goL ? 15.f : 0.f;
+        if (cand < Lbest) {                                                       // clipping.py:187,191
+          Lbest = cand;
+          bi = nl;
+          bj = nr;
+        }
+      }
+    }
+
+    // ---- result, codes, pack ----
+    const size_t gofs = (size_t)row0 * p.stride;
+    uint8_t* out_tile = out_base + (((uintptr_t)p.packed + gofs) & 15);
+    uint8_t* orow = out_tile + gw * p.stride;
+    const bool ok = rvalid && !defer;
+    {
+      const int Wb = p.b - bi - bj;
+      const float B = (float)(15 * bi);
+      const float Wbf = (float)(Wb > 0 ? Wb : 1);
+      const float kW = __fdividef(1.f, Wbf * ALPHA);
+      const float nb = NEAR + p.delta / Wbf;
+      bool near = false;
+      const f2_t nB2 = pk2(-B, -B), al2 = pk2(ALPHA, ALPHA);
+      const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC);
+#pragma unroll 4
+      for (int c = 0; c < E / 4; ++c) {
+        const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ysl + c * 32);
+        uint32_t w = 0;
+#pragma unroll
+        for (int hlf = 0; hlf < 2; ++hlf) {
+          const f2_t z = add2(hlf ? yy.y : yy.x, nB2);
+          float z0, z1;
+          upk2(z, z0, z1);
+          const float s0 = sat_fma(z0, kW, hh), s1 = sat_fma(z1, kW, hh);
+          const f2_t sv = pk2(s0, s1);
+          const f2_t m = fma2_rm(sv, al2, mg2);
+          const f2_t fr = sub2(fma2(sv, al2, pk2(0.f, 0.f)), add2(m, nmg2));   // frac of alpha*s
+          float m0, m1, f0, f1;
+          upk2(m, m0, m1);
+          upk2(fr, f0, f1);
+          // an element within nb of a rounding boundary (strictly inside the clamp
+          // range) may take another code in the reference: the row is deferred
+          near |= (s0 > 0.f && s0 < 1.f && fabsf(f0 - 0.5f) > 0.5f - nb) ||
+                  (s1 > 0.f && s1 < 1.f && fabsf(f1 - 0.5f) > 0.5f - nb);
+          w |= ((__float_as_uint(m0) & 0xFu) | ((__float_as_uint(m1) & 0xFu) << 4)) << (8 * hlf);
+        }
+        if (rvalid) *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = (uint16_t)w;
+      }
+      const bool anynear = group_any<LPR>(near);   // warp-collective: every lane votes
+      defer |= ok && anynear;
+    }
+    if (rvalid && !defer && q == 0) {
+      const RowFast& R = rf[gw];
+      // clipping.py:175,182: x0 + bi*step (x0 itself for the start pair), x1 - bj*step
+      const double lo = (bi == 0 && bj == 0) ? R.x0 : __dadd_rn(R.x0, __dmul_rn((double)bi, R.step));
+      const double hi = bj == 0 ? R.x1 : __dsub_rn(R.x1, __dmul_rn((double)bj, R.step));
+      const double sc = div15(__dsub_rn(hi, lo));                                  // uniform.py:74-80
+      uint8_t* a = orow + p.half;
+      if (p.aux == EQ4_AUX_FP16) {
+        const uint32_t s16 = aux_bits_f16(sc), b16 = aux_bits_f16(lo);
+        *reinterpret_cast<uint16_t*>(a) = (uint16_t)s16;
+        *reinterpret_cast<uint16_t*>(a + 2) = (uint16_t)b16;
+      } else {
+        const uint32_t s32 = aux_bits_f32(sc), b32 = aux_bits_f32(lo);
+        *reinterpret_cast<uint16_t*>(a) = (uint16_t)s32;
+        *reinterpret_cast<uint16_t*>(a + 2) = (uint16_t)(s32 >> 16);
+        *reinterpret_cast<uint16_t*>(a + 4) = (uint16_t)b32;
+        *reinterpret_cast<uint16_t*>(a + 6) = (uint16_t)(b32 >> 16);
+      }
+      if (p.lo_out) { p.lo_out[row] = lo; p.hi_out[row] = hi; }
+      if (p.info0) p.info0[row] = nl + nr;
+      if (p.info1) p.info1[row] = p.b > 65535 ? bi : ((bi << 16) | bj);
+    }
+    // deferred rows: one list slot each (about 2% of the rows)
+    if (rvalid && defer && q == 0) {
+      const unsigned slot = (unsigned)atomicAdd(p.dcount, 1);
+      GF_CHECK(slot < p.rows, "dlist", slot);
+      p.dlist[slot] = (uint32_t)row;
+      ++ndefer;
+    }
+    __syncwarp();
+    GF_CHECK(gofs + (size_t)min((int64_t)RPW, p.rows - row0) * p.stride <= (size_t)p.rows * p.stride, "out", gofs);
+    GF_CHECK(out_tile - out_base < 16, "tile", out_tile - out_base);
+    warp_copy_out(p.packed + gofs, out_tile, (int)min((int64_t)RPW, p.rows - row0) * p.stride);
+    __syncwarp();
+  }
+  if (lane < 4 && wdiag[lane]) atomicAdd(&g_diag[lane], (unsigned long long)wdiag[lane]);
+  if (ndefer) atomicAdd(&g_diag[4], (unsigned long long)ndefer);
 }
 
 // ---------------------------------------------------------------------------
@@ -1909,6 +2227,62 @@ static int launch_persistent(Kern kern, size_t smem, int64_t ntiles, const Param
   return EQ4_OK;
 }
 
+// The device's default memory pool keeps what it has (stream-ordered scratch of
+// the GREEDY deferral list is then recycled, not remapped, call after call).
+static void keep_pool_memory() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
+// GREEDY on vector rows: k_greedy_fast screens every row, then k_greedy (list mode)
+// redoes the deferred ones with the exact tier.  Both on stream s, no host sync;
+// the deferral list (4 bytes per row) is stream-ordered scratch.
+template <int LPR, int E>
+static int greedy_two_pass(Params p, cudaStream_t s, int nw_exact) {
+  keep_pool_memory();
+  using F = FastSlice<LPR, E>;
+  using S = WarpSliceG<LPR, E, true>;
+  const int64_t chunk = (int64_t)1 << 30;   // list entries are 32-bit row offsets
+  uint32_t* buf = nullptr;
+  const int64_t cap = std::min<int64_t>(p.rows, chunk);
+  cudaError_t e = cudaMallocAsync((void**)&buf, (size_t)(cap + 4) * 4, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  int nwf = NWARPS_G;
+  while (nwf > 1 && (size_t)nwf * F::bytes(p.stride) > 220 * 1024) nwf >>= 1;
+  int rc = EQ4_OK;
+  const int64_t rows = p.rows;
+  for (int64_t r0 = 0; r0 < rows && rc == EQ4_OK; r0 += chunk) {
+    Params c = p;
+    c.rows = std::min<int64_t>(chunk, rows - r0);
+    c.x = p.x + r0 * p.ld;
+    c.packed = p.packed + r0 * p.stride;
+    if (p.lo_out) { c.lo_out = p.lo_out + r0; c.hi_out = p.hi_out + r0; }
+    if (p.info0) c.info0 = p.info0 + r0;
+    if (p.info1) c.info1 = p.info1 + r0;
+    c.dcount = reinterpret_cast<int*>(buf);
+    c.dlist = buf + 4;
+    e = cudaMemsetAsync(c.dcount, 0, 4, s);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "cudaMemsetAsync"); break; }
+    c.list = 0;
+    rc = launch_persistent(k_greedy_fast<LPR, E>, nwf * F::bytes(p.stride),
+                           (c.rows + F::RPW * nwf - 1) / (F::RPW * nwf), c, s, "k_greedy_fast", 32 * nwf);
+    if (rc != EQ4_OK) break;
+    if (getenv("EQ4_DEV_SKIP_EXACT")) continue;   // development only
+    c.list = 1;
+    rc = launch_persistent(k_greedy<LPR, E, true>, nw_exact * S::bytes(p.stride),
+                           (c.rows + S::RPW * nw_exact - 1) / (S::RPW * nw_exact), c, s, "k_greedy", 32 * nw_exact);
+  }
+  cudaFreeAsync(buf, s);
+  return rc;
+}
+
 template <int METHOD, int LPR, int E, bool VEC>
 static int launch_rq(const Params& p, cudaStream_t s) {
   if constexpr (METHOD == M_ASYM) {
@@ -1940,6 +2314,9 @@ static int launch_rq(const Params& p, cudaStream_t s) {
     int nw = NWARPS_G;
     while (nw > 1 && (size_t)nw * S::bytes(p.stride) > 220 * 1024) nw >>= 1;
     if (S::bytes(p.stride) > 220 * 1024) return fail(EQ4_EUNSUPPORTED, "GREEDY row does not fit in shared memory");
+    if constexpr (VEC) {
+      if (!getenv("EQ4_DEV_ONE_PASS")) return greedy_two_pass<LPR, E>(p, s, nw);   // (env: development A/B only)
+    }
     return launch_persistent(k_greedy<LPR, E, VEC>, nw * S::bytes(p.stride),
                              (p.rows + S::RPW * nw - 1) / (S::RPW * nw), p, s, "k_greedy", 32 * nw);
   }
@@ -2566,14 +2943,14 @@ int eq4_quant_mse_rows(const void* x, int x_is_f64, int64_t rows, int64_t dim, i
 // Diagnostics: the GREEDY rare-path counters (g_diag) of the current device;
 // reset != 0 zeroes them after the read.  Synchronous.
 int eq4_diag_counters(int64_t* out, int reset) {
-  unsigned long long h[4] = {0, 0, 0, 0};
+  unsigned long long h[5] = {0, 0, 0, 0, 0};
   cudaError_t e = cudaMemcpyFromSymbol(h, g_diag, sizeof h);
   if (e == cudaSuccess && reset) {
-    const unsigned long long z[4] = {0, 0, 0, 0};
+    const unsigned long long z[5] = {0, 0, 0, 0, 0};
     e = cudaMemcpyToSymbol(g_diag, z, sizeof z);
   }
   if (e != cudaSuccess) return cuda_fail(e, "diag counters");
-  for (int i = 0; i < 4; i++) out[i] = (int64_t)h[i];
+  for (int i = 0; i < 5; i++) out[i] = (int64_t)h[i];
   return EQ4_OK;
 }
 

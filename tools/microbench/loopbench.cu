@@ -1,0 +1,150 @@
+// GREEDY element-loop throughput in isolation (development microbenchmark): each warp
+// evaluates candidate pairs over a 64-element row slice per lane in shared memory, the
+// way k_greedy_fast's phase A does, with no decision work between evaluations.
+// Reports element-pair evaluations per second and the FMA-pipe share that implies.
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -I../../include \
+//        -o loopbench loopbench.cu && ./loopbench
+#include "../../paper_1911_02079_b200/csrc/eq4.cu"
+
+namespace lb {
+using namespace eq4;
+constexpr int E = 64;
+constexpr int NIT = 2048;
+
+// variant 1: two accumulator chains per candidate
+__device__ __forceinline__ void pair_split(const float4* ys4, float BL, float nW, float kW, float h,
+                                           float& aL, float& aR) {
+  const f2_t nBL2 = pk2(-BL, -BL), al2 = pk2(ALPHA, ALPHA);
+  const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
+  const float thr = -0.5f * nW - 15.f, cW = 15.f + nW, top = MAGIC + 15.f;
+  f2_t sL[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)}, sR[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
+#pragma unroll 4
+  for (int c = 0; c < E / 4; ++c) {
+    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32);
+#pragma unroll
+    for (int hlf = 0; hlf < 2; ++hlf) {
+      const f2_t zL = add2(hlf ? yy.y : yy.x, nBL2);
+      float a0, a1;
+      upk2(zL, a0, a1);
+      const f2_t mL = fma2_rm(pk2(sat_fma(a0, kW, h), sat_fma(a1, kW, h)), al2, mg2);
+      const f2_t eL = fma2(add2(mL, nmg2), nW2, zL);
+      float e0, e1, m0, m1;
+      upk2(eL, e0, e1);
+      upk2(mL, m0, m1);
+      const f2_t eR = add2(eL, pk2(sel_ge_lt(e0, thr, m0, top, cW, 15.f), sel_ge_lt(e1, thr, m1, top, cW, 15.f)));
+      sL[hlf] = fma2(eL, eL, sL[hlf]);
+      sR[hlf] = fma2(eR, eR, sR[hlf]);
+    }
+  }
+  float l0, l1, r0, r1;
+  upk2(add2(sL[0], sL[1]), l0, l1);
+  upk2(add2(sR[0], sR[1]), r0, r1);
+  aL = l0 + l1;
+  aR = r0 + r1;
+}
+
+// variant 2: interior elements only (no clamp): code = floor(z/W + 1/2) from one round-down
+// FMA, R's code moves up iff eL >= W/2 - 15 (upper bound of what a clamp-free slice costs)
+__device__ __forceinline__ void pair_core(const float4* ys4, float BL, float nW, float kW1,
+                                          float& aL, float& aR) {
+  const f2_t nBL2 = pk2(-BL, -BL), k2 = pk2(kW1, kW1);
+  const f2_t mg2 = pk2(MAGIC + 0.5f, MAGIC + 0.5f), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
+  const float thr = -0.5f * nW - 15.f, cW = 15.f + nW;
+  f2_t sL = pk2(0.f, 0.f), sR = pk2(0.f, 0.f);
+#pragma unroll 4
+  for (int c = 0; c < E / 4; ++c) {
+    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32);
+#pragma unroll
+    for (int hlf = 0; hlf < 2; ++hlf) {
+      const f2_t zL = add2(hlf ? yy.y : yy.x, nBL2);
+      const f2_t mL = fma2_rm(zL, k2, mg2);
+      const f2_t eL = fma2(add2(mL, nmg2), nW2, zL);
+      float e0, e1;
+      upk2(eL, e0, e1);
+      const f2_t eR = add2(eL, pk2(e0 >= thr ? cW : 15.f, e1 >= thr ? cW : 15.f));
+      sL = fma2(eL, eL, sL);
+      sR = fma2(eR, eR, sR);
+    }
+  }
+  float l0, l1, r0, r1;
+  upk2(sL, l0, l1);
+  upk2(sR, r0, r1);
+  aL = l0 + l1;
+  aR = r0 + r1;
+}
+
+template <int VAR, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_loop(float* sink, int nit) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4* ys4 = reinterpret_cast<float4*>(smem + warp * E * 128);
+  unsigned st = 12345u + 7919u * (blockIdx.x * 128 + threadIdx.x);
+  for (int c = 0; c < E / 4; ++c) {
+    float y[4];
+    for (int k = 0; k < 4; ++k) {
+      st = st * 1664525u + 1013904223u;
+      y[k] = (float)(st >> 8) * (3000.f / 16777216.f);
+      y[k] = rintf(y[k] * 4096.f) * (1.f / 4096.f);
+    }
+    ys4[c * 32 + lane] = make_float4(y[0], y[1], y[2], y[3]);
+  }
+  __syncwarp();
+  const float4* ysl = ys4 + lane;
+  float acc = 0.f, BL = 15.f;
+  for (int it = 0; it < nit; ++it) {
+    const float Wf = (float)(190 - (it & 63));
+    float aL, aR;
+    if constexpr (VAR == 0) eval_pair_x2_shift<E>(ysl, BL, -Wf, kw_of(Wf), 0.5f / ALPHA, aL, aR);
+    if constexpr (VAR == 1) pair_split(ysl, BL, -Wf, kw_of(Wf), 0.5f / ALPHA, aL, aR);
+    if constexpr (VAR == 2) pair_core(ysl, BL, -Wf, __frcp_rn(Wf), aL, aR);
+    acc += aL - aR;
+    BL = aL < aR ? BL + 15.f : BL;
+    BL = BL > 400.f ? 15.f : BL;
+  }
+  if (acc == 1.2345f) sink[0] = acc;
+}
+
+template <int VAR, int MINB>
+void run(const char* name, float* sink) {
+  const int smem = 4 * E * 128;
+  cudaFuncSetAttribute(k_loop<VAR, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_loop<VAR, MINB>, 128, smem);
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = nsm * occ;
+  k_loop<VAR, MINB><<<grid, 128, smem>>>(sink, 64);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k_loop<VAR, MINB><<<grid, 128, smem>>>(sink, NIT);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, k_loop<VAR, MINB>);
+  // element pairs evaluated (both candidates) per second; 16 FMA-pipe cycles per pair
+  // and warp at 32 lanes/clk/SMSP is the current formulation's pipe cost
+  const double pairs = (double)grid * 128 * NIT * (E / 2);
+  const double clk = 1.965e9, fma_cap = (double)nsm * 4 * clk;   // warp-pipe-cycles/s
+  printf("{\"variant\": \"%s\", \"regs\": %d, \"warps_per_smsp\": %d, \"ms\": %.3f, "
+         "\"Gpairs_per_s\": %.1f, \"fma_share_at_16cyc\": %.3f}\n",
+         name, fa.numRegs, occ, ms, pairs / ms / 1e6, pairs / 32.0 * 16.0 / (ms * 1e-3) / fma_cap);
+}
+}  // namespace lb
+
+int main() {
+  float* sink;
+  cudaMalloc(&sink, 4);
+  lb::run<0, 4>("shift x4", sink);
+  lb::run<0, 5>("shift x5", sink);
+  lb::run<0, 8>("shift x8", sink);
+  lb::run<1, 4>("split x4", sink);
+  lb::run<1, 5>("split x5", sink);
+  lb::run<2, 4>("core x4", sink);
+  lb::run<2, 5>("core x5", sink);
+  lb::run<2, 8>("core x8", sink);
+  return 0;
+}
