@@ -22,6 +22,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "../../include/eq4.h"
@@ -336,6 +338,161 @@ __global__ void __launch_bounds__(RR_THREADS) k_rowrange(const RRParams p) {
   }
 }
 
+// ACIQ, cooperative (d % 8 == 0, 8 <= d <= 128: one numpy leaf, no remainder): eight lanes
+// per row, four rows per warp.  numpy's leaf sum runs 8 sequential accumulator chains --
+// chain j sums elements j, j+8, j+16, ... -- then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7));
+// lane j of a row owns chain j (its elements are exactly j + 8k, loaded with 4-byte
+// loads whose 8 lanes cover 32 contiguous bytes: every sector is used), and the tree is
+// the xor-butterfly over the 8 lanes (IEEE addition commutes, so each level's pairs are
+// numpy's).  Elements stay in registers for both sums and the codes; the nibble codes of
+// a row are transposed across its 8 lanes (3 butterfly stages on 32-bit words) so lane t
+// stores packed bytes 4t..4t+3 (elements 8t..8t+7) with one 32-bit store.
+// One row of k_aciq8 (the lane's chain j), elements already loaded.
+template <int NCH>
+__device__ __forceinline__ void aciq8_row(const RRParams& p, const float (&x)[NCH], int64_t row, bool rvalid,
+                                          int j, double n, double rn, bool pow2) {
+  constexpr unsigned FULLM = 0xffffffffu;
+  double xd[NCH];
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) xd[k] = (double)x[k];
+  // np.mean (clipping.py:135): chain j, then the leaf tree, then np.add.reduce's 0.0 +
+  double r = xd[0];
+#pragma unroll
+  for (int k = 1; k < NCH; ++k) r = __dadd_rn(r, xd[k]);
+  r = __dadd_rn(r, __shfl_xor_sync(FULLM, r, 1));
+  r = __dadd_rn(r, __shfl_xor_sync(FULLM, r, 2));
+  r = __dadd_rn(r, __shfl_xor_sync(FULLM, r, 4));
+  const double sum = __dadd_rn(0.0, r);
+  const bool bad = !isfinite(sum);   // a non-finite element (the float64 sum of floats cannot overflow)
+  const double mean = pow2 ? __dmul_rn(sum, rn) : __ddiv_rn(sum, n);
+  // np.mean(np.abs(x - mean)) (clipping.py:136)
+  double a = fabs(__dsub_rn(xd[0], mean));
+#pragma unroll
+  for (int k = 1; k < NCH; ++k) a = __dadd_rn(a, fabs(__dsub_rn(xd[k], mean)));
+  a = __dadd_rn(a, __shfl_xor_sync(FULLM, a, 1));
+  a = __dadd_rn(a, __shfl_xor_sync(FULLM, a, 2));
+  a = __dadd_rn(a, __shfl_xor_sync(FULLM, a, 4));
+  const double sa = __dadd_rn(0.0, a);
+  const double alpha = __dmul_rn(p.aciq_const, pow2 ? __dmul_rn(sa, rn) : __ddiv_rn(sa, n));
+  double lo = __dsub_rn(mean, alpha), hi = __dadd_rn(mean, alpha);
+  const bool flat = rvalid && !bad && alpha == 0.0;
+  if (__any_sync(FULLM, flat)) {   // rare: clipping.py:137-138 -> clip_range_asym (numpy's zero choice)
+    float mn = x[0], mx = x[0];
+#pragma unroll
+    for (int k = 1; k < NCH; ++k) { mn = fminf(mn, x[k]); mx = fmaxf(mx, x[k]); }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      mn = fminf(mn, __shfl_xor_sync(FULLM, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(FULLM, mx, o));
+    }
+    unsigned kz = 0u;
+    if (mn == 0.f || mx == 0.f) {
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) kz = max(kz, np_zero_key_t(x[k], j + 8 * k, p.d));
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) kz = max(kz, __shfl_xor_sync(FULLM, kz, o));
+    if (flat) {
+      const double z = (kz & 1u) ? -0.0 : 0.0;
+      lo = mn == 0.f ? z : (double)mn;
+      hi = mx == 0.f ? z : (double)mx;
+    }
+  }
+  if (bad) { lo = 0.0; hi = 0.0; }
+  // codes (uniform.py:60-80): branch-free fp32 estimate, the float64 codec for a lane's
+  // elements when one of them lies within NEAR of a rounding boundary
+  const bool degenerate = bad || hi == lo;
+  const double w64 = __dsub_rn(hi, lo);
+  const float lo_hi = __double2float_rn(lo), lo_lo = __double2float_rn(__dsub_rn(lo, (double)lo_hi));
+  const float wf = __double2float_rn(w64);
+  const float inv1 = degenerate ? 0.f : __fdividef(1.f, wf);
+  // the estimate needs a normal, finite range (fast_codec's test, on the float copies)
+  const bool slow = !degenerate && !(wf > 1e-30f && wf < 1e30f && fabsf(lo_hi) < 1e30f &&
+                                     fabsf(__double2float_rn(hi)) < 1e30f);
+  unsigned w[(NCH + 7) / 8];
+#pragma unroll
+  for (int g = 0; g < (NCH + 7) / 8; ++g) w[g] = 0u;
+  float gmax = 0.f;
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const float sv = __saturatef(__fmul_rn(__fadd_rn(__fadd_rn(x[k], -lo_hi), -lo_lo), inv1));
+    const float m = __fadd_rd(__fmaf_rn(sv, 15.f, 0.5f), 8388608.f);
+    gmax = fmaxf(gmax, fabsf(__fmaf_rn(sv, 15.f, -__fadd_rn(m, -8388608.f))));
+    w[k >> 3] |= (__float_as_uint(m) & 0xFu) << (4 * (k & 7));
+  }
+  const bool exact = rvalid && (degenerate || slow || gmax > 0.5f - NEAR);
+  if (__any_sync(FULLM, exact) && exact) {
+    const CodeParams cp = make_code_params(degenerate ? 0.0 : lo, degenerate ? 0.0 : hi);
+#pragma unroll
+    for (int g = 0; g < (NCH + 7) / 8; ++g) w[g] = 0u;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) w[k >> 3] |= code_exact(x[k], cp) << (4 * (k & 7));
+  }
+  // 8 x 8 nibble transpose across the row's lanes: lane t ends with nibble t of every lane
+#pragma unroll
+  for (int g = 0; g < (NCH + 7) / 8; ++g) {
+#pragma unroll
+    for (int b = 4; b >= 1; b >>= 1) {
+      const unsigned msk = b == 4 ? 0x0000FFFFu : (b == 2 ? 0x00FF00FFu : 0x0F0F0F0Fu);
+      const unsigned pw = __shfl_xor_sync(FULLM, w[g], b);
+      w[g] = (j & b) ? (((pw & ~msk) >> (4 * b)) | (w[g] & ~msk)) : ((w[g] & msk) | ((pw & msk) << (4 * b)));
+    }
+  }
+  if (rvalid) {
+    uint8_t* orow = p.packed + (size_t)row * p.stride;
+#pragma unroll
+    for (int g = 0; g < (NCH + 7) / 8; ++g)
+      if (j + 8 * g < NCH) *reinterpret_cast<uint32_t*>(orow + 4 * (j + 8 * g)) = w[g];
+    if (j == 0) {
+      const double sc = degenerate ? 0.0 : div15(w64);   // uniform.py:74-80
+      uint32_t* a4 = reinterpret_cast<uint32_t*>(orow + p.half);
+      if (p.aux == EQ4_AUX_FP16) {
+        a4[0] = aux_bits_f16(sc) | (aux_bits_f16(lo) << 16);
+      } else {
+        a4[0] = aux_bits_f32(sc);
+        a4[1] = aux_bits_f32(lo);
+      }
+      if (p.lo_out) { p.lo_out[row] = lo; p.hi_out[row] = hi; }
+      if (p.info0) p.info0[row] = 0;
+      if (bad && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
+    }
+  }
+}
+
+// occupancy measured on 4M x 64 / 2M x 128 N(0,1): 3 blocks of 256 (d = 64: 0.42 -> 0.415 ms),
+// 4 at d = 128 (0.42 -> 0.37 ms)
+template <int NCH>
+__global__ void __launch_bounds__(256, NCH >= 16 ? 4 : 3) k_aciq8(const RRParams p) {
+  const int lane = threadIdx.x & 31, j = lane & 7;
+  const int64_t nsets = (p.rows + 3) / 4;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // np.mean divides by n: a power-of-two d makes it an exact scaling (same rounding as the divide)
+  const double n = (double)p.d, rn = 1.0 / n;
+  const bool pow2 = (p.d & (p.d - 1)) == 0;
+  // the next row set's elements are in flight while the current one is computed
+  float xn[NCH];
+  {
+    const int64_t row = wid * 4 + (lane >> 3);
+    const float* xr = p.x + (row < p.rows ? row : 0) * p.ld + j;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) xn[k] = __ldcs(xr + 8 * k);
+  }
+  for (int64_t set = wid; set < nsets; set += nw) {
+    const int64_t row = set * 4 + (lane >> 3);
+    float x[NCH];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) x[k] = xn[k];
+    if (set + nw < nsets) {
+      const int64_t rown = row + 4 * nw;
+      const float* xr = p.x + (rown < p.rows ? rown : 0) * p.ld + j;
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) xn[k] = __ldcs(xr + 8 * k);
+    }
+    aciq8_row<NCH>(p, x, row, row < p.rows, j, n, rn, pow2);
+  }
+}
+
 // The scalar entry points on float64 rows (clip_range_aciq / clip_range_gss of any array,
 // clipping.py:46 promotes it to float64): ranges (and GSS evaluation counts) only, lane
 // per row straight from global memory.
@@ -393,6 +550,7 @@ int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, i
                         int aux, uint8_t* packed, double* xmin, double* xmax, int32_t* info0,
                         int32_t* status, cudaStream_t s, std::string& err) {
   RRParams p;
+  memset(&p, 0, sizeof(p));
   p.aciq_const = method == EQ4_METHOD_ACIQ ? param : 5.03;
   p.gss_tol = method == EQ4_METHOD_GSS ? param : 1e-4;
   p.x = x; p.rows = rows; p.ld = ld; p.d = (int)dim; p.aux = aux; p.method = method;
@@ -400,6 +558,27 @@ int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, i
   p.stride = p.half + 2 * (aux == EQ4_AUX_FP16 ? 2 : 4);
   p.packed = packed; p.lo_out = xmin; p.hi_out = xmax; p.info0 = info0; p.status = status;
   p.invphi = (std::sqrt(5.0) - 1.0) / 2.0;
+  if (method == EQ4_METHOD_ACIQ && (dim == 64 || dim == 128) && ((uintptr_t)packed & 3) == 0 &&
+      !getenv("EQ4_DEV_ACIQ_LANE")) {   // (env: development A/B only)
+    const int nch = (int)(dim / 8);
+    auto kern = nch == 1 ? k_aciq8<1> : nch == 2 ? k_aciq8<2> : nch == 4 ? k_aciq8<4> : nch == 8 ? k_aciq8<8>
+              : nch == 16 ? k_aciq8<16> : nullptr;
+    if (kern) {
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaError_t e = cudaGetDevice(&dev);
+      if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+      if (e != cudaSuccess) { err = std::string("k_aciq8 setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+      const int64_t nsets = (rows + 3) / 4;
+      int64_t grid = (nsets + 7) / 8;
+      const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+      if (grid > cap) grid = cap;
+      kern<<<(unsigned)std::max<int64_t>(1, grid), 256, 0, s>>>(p);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) { err = std::string("k_aciq8: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
+      return EQ4_OK;
+    }
+  }
   p.staged = dim <= RR_MAX_STAGED;
   p.vec4 = (dim % 4 == 0) && (ld % 4 == 0) && (((uintptr_t)x & 15) == 0);
   const size_t xs_bytes = p.staged ? (size_t)dim * RR_COL * 4 : 0;
