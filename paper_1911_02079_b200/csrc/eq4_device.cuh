@@ -448,6 +448,31 @@ static __device__ __noinline__ double apprx_norm_np_warp(const int* cnt, int b, 
     const int c = cnt[j];
     t[j] = c ? apprx_term(c, j, w, s, dst_w, half, cw) : 0.0;
   }
+  {
+    // one leaf (b <= 128) or two (both halves <= 128 elements): lanes 8l..8l+7 run leaf l's
+    // chains, the leaves are added once -- no leaf table, no recursion
+    int n2 = b;
+    if (b > 128) { n2 = b / 2; n2 -= n2 % 8; }
+    if (b <= 128 || b - n2 <= 128) {
+      __syncwarp();
+      const int nleaves = b > 128 ? 2 : 1;
+      const int leaf = (lane >> 3) & 1, k = lane & 7;
+      const int ls = leaf ? n2 : 0, ln = leaf ? b - n2 : n2;
+      const int nfull = ln < 8 ? 0 : ln - (ln % 8);
+      double r = 0.0;
+      if (lane < 8 * nleaves)
+        for (int jj = k; jj < nfull; jj += 8) r = __dadd_rn(r, t[ls + jj]);
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+      double res = ln >= 8 ? r : 0.0;
+      for (int jj = nfull; jj < ln; jj++) res = __dadd_rn(res, t[ls + jj]);
+      const double leaf1 = __shfl_sync(0xffffffffu, res, 8);
+      const double total = nleaves == 2 ? __dadd_rn(res, leaf1) : res;   // lane 0: leaf 0 + leaf 1
+      __syncwarp();
+      return __shfl_sync(0xffffffffu, __dadd_rn(0.0, total), 0);
+    }
+  }
   int nl = 0;
   if (lane == 0) nl = np_leaves(b, leaf_st, leaf_ln, max_leaves);
   nl = __shfl_sync(0xffffffffu, nl, 0);

@@ -43,22 +43,27 @@ struct KMParams {
   int staged;   // rows staged in shared memory as a [d][33] tile
 };
 
+// This lane's row: a staged [d][33] column (STAGED) or the row in global memory (wide
+// rows); the stride is a compile-time constant either way.
+template <bool STAGED>
 struct KMLane {
-  const float* xs;   // this lane's row: element k at xs[k * ks] (staged column or global row)
-  int ks;
+  const float* xs;   // element k at xs[k * KM_COL] (staged) or xs[k]
   uint8_t* a;        // assignments, element k at a[k * 32]
-  __device__ __forceinline__ double v(int k) const { return (double)xs[(size_t)k * ks]; }
+  __device__ __forceinline__ float f(int k) const { return xs[STAGED ? k * KM_COL : k]; }
+  __device__ __forceinline__ double v(int k) const { return (double)f(k); }
 };
 
 // members.mean() of the m members at perm[s0 ..] (perm holds each cluster's members in
 // element order: a stable counting sort): 0.0 + numpy pairwise sum / m (eq4_np.cuh)
-__device__ __forceinline__ double km_sorted_mean(const KMLane& L, const uint16_t* perm, int s0, int m) {
+template <class Lane, typename PermT>
+__device__ __forceinline__ double km_sorted_mean(const Lane& L, const PermT* perm, int s0, int m) {
   const double s = np_pw([&](int i) { return L.v(perm[(s0 + i) * 32]); }, 0, m);
   return __ddiv_rn(__dadd_rn(0.0, s), (double)m);
 }
 
 // np.sum((v - c[a])**2): numpy's pairwise order over the d squared errors (eq4_np.cuh)
-__device__ __forceinline__ double km_sse(const KMLane& L, const double* cl, int d) {
+template <class Lane>
+__device__ __forceinline__ double km_sse(const Lane& L, const double* cl, int d) {
   return np_sum([&](int k) {
     const double e = __dsub_rn(L.v(k), cl[L.a[k * 32]]);
     return __dmul_rn(e, e);
@@ -68,7 +73,8 @@ __device__ __forceinline__ double km_sse(const KMLane& L, const double* cl, int 
 // argmin_j |v - c_j| (first minimum), assignments to L.a, per-cluster counts (counted in
 // the lane's shared-memory column hist[j * 32], then read back: one increment per
 // element instead of a 16-way compare-and-add)
-__device__ __forceinline__ void km_assign(const KMLane& L, const double (&c)[KM_K], int d,
+template <class Lane>
+__device__ __forceinline__ void km_assign(const Lane& L, const double (&c)[KM_K], int d,
                                           int (&cnt)[KM_K], int* hist) {
 #pragma unroll
   for (int j = 0; j < KM_K; j++) hist[j * 32] = 0;
@@ -88,15 +94,18 @@ __device__ __forceinline__ void km_assign(const KMLane& L, const double (&c)[KM_
   for (int j = 0; j < KM_K; j++) cnt[j] = hist[j * 32];
 }
 
+// PermT: the cluster-sorted element indices (bytes while d <= 256: half the shared memory)
+template <bool STAGED, typename PermT>
 __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* ws = smem + (size_t)warp * p.warp_bytes;
   const int d = p.d;
   float* xs = reinterpret_cast<float*>(ws);
-  uint8_t* abuf = ws + (p.staged ? (((size_t)d * KM_COL * 4 + 15) & ~(size_t)15) : 0);
-  uint16_t* pbuf = reinterpret_cast<uint16_t*>(abuf + (((size_t)d * 32 + 15) & ~(size_t)15));   // sorted indices
-  int* obuf = reinterpret_cast<int*>(pbuf + (((size_t)d * 32 + 7) & ~(size_t)7));      // [16][32] offsets
+  uint8_t* abuf = ws + (STAGED ? (((size_t)d * KM_COL * 4 + 15) & ~(size_t)15) : 0);
+  PermT* pbuf = reinterpret_cast<PermT*>(abuf + (((size_t)d * 32 + 15) & ~(size_t)15));   // sorted indices
+  int* obuf = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(pbuf) +
+                                     (((size_t)d * 32 * sizeof(PermT) + 15) & ~(size_t)15));   // [16][32] offsets
   uint8_t* out_base = reinterpret_cast<uint8_t*>(obuf + KM_K * 32);
   const int ab = p.aux == EQ4_AUX_FP16 ? 2 : 4;
   const int64_t nblk = (p.rows + 31) / 32;
@@ -107,20 +116,15 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
     const int nrows = (int)min((int64_t)32, p.rows - row0);
     for (int r = 0; r < nrows; r++) {
       const float* src = p.x + (row0 + r) * p.ld;
-      if (p.staged)
+      if (STAGED)
         for (int k = lane; k < d; k += 32) xs[k * KM_COL + r] = __ldcs(src + k);
     }
     __syncwarp();
-    KMLane L;
-    if (p.staged) {
-      L.xs = xs + lane;
-      L.ks = KM_COL;
-    } else {   // wide rows: read the row from global memory (L1/L2)
-      L.xs = p.x + (rvalid ? row : row0) * p.ld;
-      L.ks = 1;
-    }
+    KMLane<STAGED> L;
+    // wide rows: read the row from global memory (L1/L2)
+    L.xs = STAGED ? xs + lane : p.x + (rvalid ? row : row0) * p.ld;
     L.a = abuf + lane;
-    uint16_t* perm = pbuf + lane;
+    PermT* perm = pbuf + lane;
     int* offs = obuf + lane;
     double c[KM_K];
     int iters = -1;
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
     if (rvalid) {
       double lo = L.v(0), hi = lo;
       for (int k = 0; k < d; k++) {
-        const float f = L.xs[(size_t)k * L.ks];
+        const float f = L.f(k);
         bad |= !isfinite(f);
         const double x = (double)f;
         lo = x < lo ? x : lo;
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(KM_THREADS) k_kmeans_rows(const KMParams p) {
             for (int k = 0; k < d; k++) {
               const int j = L.a[k * 32];
               const int pos = offs[j * 32];
-              perm[pos * 32] = (uint16_t)k;
+              perm[pos * 32] = (PermT)k;
               offs[j * 32] = pos + 1;
             }
           }
@@ -291,9 +295,12 @@ int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int
   // rows whose staged [d][33] tile would take more than half the shared memory are read
   // from global memory instead
   p.staged = (size_t)dim * KM_COL * 4 <= 96 * 1024;
+  const size_t pbytes = dim <= 256 ? 1 : 2;
   size_t wb = (p.staged ? (((size_t)dim * KM_COL * 4 + 15) & ~(size_t)15) : 0) + (((size_t)dim * 32 + 15) & ~(size_t)15) +
-              (((size_t)dim * 32 * 2 + 15) & ~(size_t)15) + (size_t)KM_K * 32 * 4 + (size_t)32 * p.stride + 32;
+              (((size_t)dim * 32 * pbytes + 15) & ~(size_t)15) + (size_t)KM_K * 32 * 4 + (size_t)32 * p.stride + 32;
   p.warp_bytes = (wb + 15) & ~(size_t)15;
+  auto kern = p.staged ? (dim <= 256 ? k_kmeans_rows<true, uint8_t> : k_kmeans_rows<true, uint16_t>)
+                       : (dim <= 256 ? k_kmeans_rows<false, uint8_t> : k_kmeans_rows<false, uint16_t>);
   int dev = 0, sms = 0, per_sm = 0, max_optin = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -307,8 +314,8 @@ int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int
     const size_t sm_w = p.warp_bytes * w;
     if (sm_w > (size_t)max_optin) break;
     int blocks = 0;
-    e = cudaFuncSetAttribute(k_kmeans_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_kmeans_rows, w * 32, sm_w);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, w * 32, sm_w);
     if (e != cudaSuccess) { err = std::string("k_kmeans_rows setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
     if (blocks * w > best_warps) { best_warps = blocks * w; nw = w; per_sm = blocks; }
   }
@@ -317,14 +324,14 @@ int eq4_kmeans_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, int
     return EQ4_EUNSUPPORTED;
   }
   const size_t smem = p.warp_bytes * nw;
-  e = cudaFuncSetAttribute(k_kmeans_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) { err = std::string("k_kmeans_rows setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
   const int64_t nblk = (rows + 31) / 32;
   int64_t grid = (nblk + nw - 1) / nw;
   const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  k_kmeans_rows<<<(unsigned)grid, nw * 32, smem, s>>>(p);
+  kern<<<(unsigned)grid, nw * 32, smem, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) { err = std::string("k_kmeans_rows: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
   return EQ4_OK;
