@@ -715,38 +715,64 @@ __device__ __forceinline__ void eval_pair(const float4* ys4, int nv, float BL, f
 // instruction for z, the round-down code, the code removal, the error and the
 // accumulation; only the saturating FFMA stays scalar (no .sat for f32x2).
 // 3.5 issue slots per element and candidate instead of 6.
+// Accumulator chains per candidate and f32x2 half in the packed evaluations: chunk c adds
+// into chain c % NACC, the chains are summed as a tree at the end.  Shorter chains tighten
+// the fp32 error band (tau2_for: E/(2 NACC) terms per chain + log2 NACC tree levels), which
+// matters for the wide rows (E = 128..512: 64..256-term chains otherwise).
+#ifndef G_NACC64
+#define G_NACC64 1
+#endif
+__host__ __device__ constexpr int nacc_for(int E) { return E >= 128 ? 4 : (E == 64 ? G_NACC64 : 1); }
+
+template <int N>
+__device__ __forceinline__ float acc_tree(const f2_t (&s)[N]) {
+  f2_t t = s[0];
+  if constexpr (N == 2) t = add2(s[0], s[1]);
+  if constexpr (N == 4) t = add2(add2(s[0], s[1]), add2(s[2], s[3]));
+  float a, b;
+  upk2(t, a, b);
+  return __fadd_rn(a, b);
+}
+
+// Packed variant of eval_pair (vector kernels): element pairs share one
+// instruction for z, the round-down code, the code removal, the error and the
+// accumulation; only the saturating FFMA stays scalar (no .sat for f32x2).
+// 3.5 issue slots per element and candidate instead of 6.
 template <int E>
 __device__ __forceinline__ void eval_pair_x2(const float4* ys4, float BL, float nW, float kW,
                                              float h, float& aL, float& aR) {
+  constexpr int NA = nacc_for(E);
   const f2_t nBL2 = pk2(-BL, -BL), c15 = pk2(15.f, 15.f), al2 = pk2(ALPHA, ALPHA);
   const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
-  f2_t sL = pk2(0.f, 0.f), sR = pk2(0.f, 0.f);
-#pragma unroll kGUnroll
-  for (int c = 0; c < E / 4; ++c) {
-    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32);
+  f2_t sL[NA], sR[NA];
 #pragma unroll
-    for (int hlf = 0; hlf < 2; ++hlf) {
-      const f2_t y2 = hlf ? yy.y : yy.x;
-      const f2_t zL = add2(y2, nBL2);
-      const f2_t zR = add2(zL, c15);                                   // exact
-      float a0, a1, b0, b1;
-      upk2(zL, a0, a1);
-      upk2(zR, b0, b1);
-      const f2_t tL = pk2(sat_fma(a0, kW, h), sat_fma(a1, kW, h));
-      const f2_t tR = pk2(sat_fma(b0, kW, h), sat_fma(b1, kW, h));
-      const f2_t cL = add2(fma2_rm(tL, al2, mg2), nmg2);              // floor(alpha * t)
-      const f2_t cR = add2(fma2_rm(tR, al2, mg2), nmg2);
-      const f2_t eL = fma2(cL, nW2, zL);                               // exact
-      const f2_t eR = fma2(cR, nW2, zR);
-      sL = fma2(eL, eL, sL);
-      sR = fma2(eR, eR, sR);
+  for (int a = 0; a < NA; ++a) { sL[a] = pk2(0.f, 0.f); sR[a] = pk2(0.f, 0.f); }
+#pragma unroll (kGUnroll / NA > 0 ? kGUnroll / NA : 1)
+  for (int c0 = 0; c0 < E / 4; c0 += NA) {
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + (c0 + a) * 32);
+#pragma unroll
+      for (int hlf = 0; hlf < 2; ++hlf) {
+        const f2_t y2 = hlf ? yy.y : yy.x;
+        const f2_t zL = add2(y2, nBL2);
+        const f2_t zR = add2(zL, c15);                                   // exact
+        float a0, a1, b0, b1;
+        upk2(zL, a0, a1);
+        upk2(zR, b0, b1);
+        const f2_t tL = pk2(sat_fma(a0, kW, h), sat_fma(a1, kW, h));
+        const f2_t tR = pk2(sat_fma(b0, kW, h), sat_fma(b1, kW, h));
+        const f2_t cL = add2(fma2_rm(tL, al2, mg2), nmg2);              // floor(alpha * t)
+        const f2_t cR = add2(fma2_rm(tR, al2, mg2), nmg2);
+        const f2_t eL = fma2(cL, nW2, zL);                               // exact
+        const f2_t eR = fma2(cR, nW2, zR);
+        sL[a] = fma2(eL, eL, sL[a]);
+        sR[a] = fma2(eR, eR, sR[a]);
+      }
     }
   }
-  float l0, l1, r0, r1;
-  upk2(sL, l0, l1);
-  upk2(sR, r0, r1);
-  aL = __fadd_rn(l0, l1);
-  aR = __fadd_rn(r0, r1);
+  aL = acc_tree<NA>(sL);
+  aR = acc_tree<NA>(sR);
 }
 
 // Packed pair evaluation with R derived from L (valid for W > 15): the R grid
@@ -770,60 +796,67 @@ __device__ __forceinline__ float sel_ge_lt(float e, float thr, float m, float to
 template <int E>
 __device__ __forceinline__ void eval_pair_x2_shift(const float4* ys4, float BL, float nW, float kW,
                                                    float h, float& aL, float& aR) {
+  constexpr int NA = nacc_for(E);
   const f2_t nBL2 = pk2(-BL, -BL), al2 = pk2(ALPHA, ALPHA);
   const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
   // eR = eL + (15 - W k):  k = [eL + 15 >= W/2] and [cL < 15]
   const float thr = -0.5f * nW - 15.f, cW = 15.f + nW, top = MAGIC + 15.f;   // ulp(2^23) = 1
-  f2_t sL = pk2(0.f, 0.f), sR = pk2(0.f, 0.f);
-#pragma unroll kGUnroll
-  for (int c = 0; c < E / 4; ++c) {
-    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32);
+  f2_t sL[NA], sR[NA];
 #pragma unroll
-    for (int hlf = 0; hlf < 2; ++hlf) {
-      const f2_t zL = add2(hlf ? yy.y : yy.x, nBL2);
-      float a0, a1;
-      upk2(zL, a0, a1);
-      const f2_t mL = fma2_rm(pk2(sat_fma(a0, kW, h), sat_fma(a1, kW, h)), al2, mg2);   // 2^23 + cL
-      const f2_t eL = fma2(add2(mL, nmg2), nW2, zL);                                    // exact
-      float e0, e1, m0, m1;
-      upk2(eL, e0, e1);
-      upk2(mL, m0, m1);
-      const float c0 = sel_ge_lt(e0, thr, m0, top, cW, 15.f);
-      const float c1 = sel_ge_lt(e1, thr, m1, top, cW, 15.f);
-      const f2_t eR = add2(eL, pk2(c0, c1));                                            // exact
-      sL = fma2(eL, eL, sL);
-      sR = fma2(eR, eR, sR);
+  for (int a = 0; a < NA; ++a) { sL[a] = pk2(0.f, 0.f); sR[a] = pk2(0.f, 0.f); }
+#pragma unroll (kGUnroll / NA > 0 ? kGUnroll / NA : 1)
+  for (int c0 = 0; c0 < E / 4; c0 += NA) {
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + (c0 + a) * 32);
+#pragma unroll
+      for (int hlf = 0; hlf < 2; ++hlf) {
+        const f2_t zL = add2(hlf ? yy.y : yy.x, nBL2);
+        float a0, a1;
+        upk2(zL, a0, a1);
+        const f2_t mL = fma2_rm(pk2(sat_fma(a0, kW, h), sat_fma(a1, kW, h)), al2, mg2);   // 2^23 + cL
+        const f2_t eL = fma2(add2(mL, nmg2), nW2, zL);                                    // exact
+        float e0, e1, m0, m1;
+        upk2(eL, e0, e1);
+        upk2(mL, m0, m1);
+        const float c0v = sel_ge_lt(e0, thr, m0, top, cW, 15.f);
+        const float c1v = sel_ge_lt(e1, thr, m1, top, cW, 15.f);
+        const f2_t eR = add2(eL, pk2(c0v, c1v));                                          // exact
+        sL[a] = fma2(eL, eL, sL[a]);
+        sR[a] = fma2(eR, eR, sR[a]);
+      }
     }
   }
-  float l0, l1, r0, r1;
-  upk2(sL, l0, l1);
-  upk2(sR, r0, r1);
-  aL = __fadd_rn(l0, l1);
-  aR = __fadd_rn(r0, r1);
+  aL = acc_tree<NA>(sL);
+  aR = acc_tree<NA>(sR);
 }
 
 // Packed single-candidate loss (the full range, clipping.py:174).
 template <int E>
 __device__ __forceinline__ float eval_one_x2(const float4* ys4, float B, float nW, float kW, float h) {
+  constexpr int NA = nacc_for(E);
   const f2_t nB2 = pk2(-B, -B), al2 = pk2(ALPHA, ALPHA);
   const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
-  f2_t acc = pk2(0.f, 0.f);
-#pragma unroll kGUnroll
-  for (int c = 0; c < E / 4; ++c) {
-    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32);
+  f2_t acc[NA];
 #pragma unroll
-    for (int hlf = 0; hlf < 2; ++hlf) {
-      const f2_t z = add2(hlf ? yy.y : yy.x, nB2);
-      float a0, a1;
-      upk2(z, a0, a1);
-      const f2_t t = pk2(sat_fma(a0, kW, h), sat_fma(a1, kW, h));
-      const f2_t e = fma2(add2(fma2_rm(t, al2, mg2), nmg2), nW2, z);
-      acc = fma2(e, e, acc);
+  for (int a = 0; a < NA; ++a) acc[a] = pk2(0.f, 0.f);
+#pragma unroll (kGUnroll / NA > 0 ? kGUnroll / NA : 1)
+  for (int c0 = 0; c0 < E / 4; c0 += NA) {
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + (c0 + a) * 32);
+#pragma unroll
+      for (int hlf = 0; hlf < 2; ++hlf) {
+        const f2_t z = add2(hlf ? yy.y : yy.x, nB2);
+        float a0, a1;
+        upk2(z, a0, a1);
+        const f2_t t = pk2(sat_fma(a0, kW, h), sat_fma(a1, kW, h));
+        const f2_t e = fma2(add2(fma2_rm(t, al2, mg2), nmg2), nW2, z);
+        acc[a] = fma2(e, e, acc[a]);
+      }
     }
   }
-  float l0, l1;
-  upk2(acc, l0, l1);
-  return __fadd_rn(l0, l1);
+  return acc_tree<NA>(acc);
 }
 
 // Y coordinates on the exact fp32 grid of quantum qY (see file header).
@@ -1683,15 +1716,39 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fa
           upk2(m, m0, m1);
           upk2(fr, f0, f1);
           // an element within nb of a rounding boundary (strictly inside the clamp
-          // range) may take another code in the reference: the row is deferred
+          // range) may take another code in the reference: the float64 codec below
           near |= (s0 > 0.f && s0 < 1.f && fabsf(f0 - 0.5f) > 0.5f - nb) ||
                   (s1 > 0.f && s1 < 1.f && fabsf(f1 - 0.5f) > 0.5f - nb);
           w |= ((__float_as_uint(m0) & 0xFu) | ((__float_as_uint(m1) & 0xFu) << 4)) << (8 * hlf);
         }
         if (rvalid) *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = (uint16_t)w;
       }
-      const bool anynear = group_any<LPR>(near);   // warp-collective: every lane votes
-      defer |= ok && anynear;
+      // rare (a few % of the rows at d >= 2048): the lane's flagged elements take numpy's
+      // float64 codec (uniform.py:77-79), patched into the staged nibbles
+      if (__any_sync(FULL, near && ok) && near && ok) {
+        const RowFast& R = rf[gw];
+        const double lo = (bi == 0 && bj == 0) ? R.x0 : __dadd_rn(R.x0, __dmul_rn((double)bi, R.step));
+        const double hi = bj == 0 ? R.x1 : __dsub_rn(R.x1, __dmul_rn((double)bj, R.step));
+        const CodeParams cp = make_code_params(lo, hi);
+        const float* src = xr + 4 * q;
+        for (int c = 0; c < E / 4; ++c) {
+          const float4 yv = ysl[c * 32];
+          const float yk[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float sv = sat_fma(__fadd_rn(yk[k], -B), kW, hh);
+            const float mm = __fadd_rn(__fmaf_rd(sv, ALPHA, MAGIC), -MAGIC);
+            const float fr = __fmaf_rn(sv, ALPHA, -mm);
+            if (sv > 0.f && sv < 1.f && fabsf(fr - 0.5f) > 0.5f - nb) {
+              const unsigned cc = code_exact(src[4 * LPR * c + k], cp);
+              uint8_t* by = orow + 2 * (q + LPR * c) + (k >> 1);
+              const int sh = (k & 1) * 4;
+              *by = (uint8_t)((*by & ~(0xF << sh)) | (cc << sh));
+            }
+          }
+        }
+        atomicAdd(&wdiag[1], 1u);   // per lane with flagged elements
+      }
     }
     if (rvalid && !defer && q == 0) {
       const RowFast& R = rf[gw];
@@ -2409,7 +2466,10 @@ static float tau2_for(int d, bool vec) {
                               d == 1024 || d == 2048 || d == 4096 || d == 8192 || d == 16384);
   int lg = 0;
   while ((1 << lg) < lpr) lg++;
-  const int h = (packed ? e / 2 + 1 : e) + lg + 1;
+  // packed: chains of e / (2 nacc) terms, log2(nacc) tree levels, the two halves added
+  const int na = nacc_for(e);
+  const int lna = na == 4 ? 2 : (na == 2 ? 1 : 0);
+  const int h = (packed ? e / 2 / na + lna + 1 : e) + lg + 1;
   return (float)(2.0 * 1.05 * h * 5.9604645e-8);
 }
 
