@@ -73,6 +73,60 @@ __device__ __forceinline__ void pair_core(const float4* ys4, float BL, float nW,
   aR = r0 + r1;
 }
 
+
+// variant 3: the shift loop with scalar square-accumulates (4 chains of scalar FFMA)
+__device__ __forceinline__ void pair_sq_scalar(const float4* ys4, float BL, float nW, float kW, float h,
+                                               float& aL, float& aR) {
+  const f2_t nBL2 = pk2(-BL, -BL), al2 = pk2(ALPHA, ALPHA);
+  const f2_t mg2 = pk2(MAGIC, MAGIC), nmg2 = pk2(-MAGIC, -MAGIC), nW2 = pk2(nW, nW);
+  const float thr = -0.5f * nW - 15.f, cW = 15.f + nW, top = MAGIC + 15.f;
+  float sL0 = 0.f, sL1 = 0.f, sR0 = 0.f, sR1 = 0.f;
+#pragma unroll 4
+  for (int c = 0; c < E / 4; ++c) {
+    const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(ys4 + c * 32);
+#pragma unroll
+    for (int hlf = 0; hlf < 2; ++hlf) {
+      const f2_t zL = add2(hlf ? yy.y : yy.x, nBL2);
+      float a0, a1;
+      upk2(zL, a0, a1);
+      const f2_t mL = fma2_rm(pk2(sat_fma(a0, kW, h), sat_fma(a1, kW, h)), al2, mg2);
+      const f2_t eL = fma2(add2(mL, nmg2), nW2, zL);
+      float e0, e1, m0, m1;
+      upk2(eL, e0, e1);
+      upk2(mL, m0, m1);
+      const float r0 = __fadd_rn(e0, sel_ge_lt(e0, thr, m0, top, cW, 15.f));
+      const float r1 = __fadd_rn(e1, sel_ge_lt(e1, thr, m1, top, cW, 15.f));
+      sL0 = __fmaf_rn(e0, e0, sL0); sL1 = __fmaf_rn(e1, e1, sL1);
+      sR0 = __fmaf_rn(r0, r0, sR0); sR1 = __fmaf_rn(r1, r1, sR1);
+    }
+  }
+  aL = sL0 + sL1;
+  aR = sR0 + sR1;
+}
+
+// variant 4: fully scalar shift loop
+__device__ __forceinline__ void pair_scalar(const float4* ys4, float BL, float nW, float kW, float h,
+                                            float& aL, float& aR) {
+  const float thr = -0.5f * nW - 15.f, cW = 15.f + nW, top = MAGIC + 15.f;
+  float sL0 = 0.f, sL1 = 0.f, sR0 = 0.f, sR1 = 0.f;
+#pragma unroll 4
+  for (int c = 0; c < E / 4; ++c) {
+    const float4 y4 = ys4[c * 32];
+    const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float z = __fadd_rn(yv[k], -BL);
+      const float m = __fmaf_rd(sat_fma(z, kW, h), ALPHA, MAGIC);
+      const float e = __fmaf_rn(__fadd_rn(m, -MAGIC), nW, z);
+      const float r = __fadd_rn(e, sel_ge_lt(e, thr, m, top, cW, 15.f));
+      if (k & 1) { sL1 = __fmaf_rn(e, e, sL1); sR1 = __fmaf_rn(r, r, sR1); }
+      else { sL0 = __fmaf_rn(e, e, sL0); sR0 = __fmaf_rn(r, r, sR0); }
+    }
+  }
+  aL = sL0 + sL1;
+  aR = sR0 + sR1;
+}
+
 template <int VAR, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_loop(float* sink, int nit) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -97,6 +151,8 @@ __global__ void __launch_bounds__(128, MINB) k_loop(float* sink, int nit) {
     if constexpr (VAR == 0) eval_pair_x2_shift<E>(ysl, BL, -Wf, kw_of(Wf), 0.5f / ALPHA, aL, aR);
     if constexpr (VAR == 1) pair_split(ysl, BL, -Wf, kw_of(Wf), 0.5f / ALPHA, aL, aR);
     if constexpr (VAR == 2) pair_core(ysl, BL, -Wf, __frcp_rn(Wf), aL, aR);
+    if constexpr (VAR == 3) pair_sq_scalar(ysl, BL, -Wf, kw_of(Wf), 0.5f / ALPHA, aL, aR);
+    if constexpr (VAR == 4) pair_scalar(ysl, BL, -Wf, kw_of(Wf), 0.5f / ALPHA, aL, aR);
     acc += aL - aR;
     BL = aL < aR ? BL + 15.f : BL;
     BL = BL > 400.f ? 15.f : BL;
@@ -138,13 +194,10 @@ void run(const char* name, float* sink) {
 int main() {
   float* sink;
   cudaMalloc(&sink, 4);
-  lb::run<0, 4>("shift x4", sink);
-  lb::run<0, 5>("shift x5", sink);
-  lb::run<0, 8>("shift x8", sink);
-  lb::run<1, 4>("split x4", sink);
-  lb::run<1, 5>("split x5", sink);
-  lb::run<2, 4>("core x4", sink);
-  lb::run<2, 5>("core x5", sink);
-  lb::run<2, 8>("core x8", sink);
+  lb::run<0, 4>("shift", sink);
+  lb::run<1, 4>("split", sink);
+  lb::run<2, 4>("core", sink);
+  lb::run<3, 4>("shift scalar squares", sink);
+  lb::run<4, 4>("shift all scalar", sink);
   return 0;
 }
