@@ -1598,7 +1598,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fa
       const float c1h = 0.5f * p.c1;
       float kWn = kw_of((float)(p.b - 1));
       float sq = sqrt_approx(fmaxf(Lbest, 1e-30f));
-      float rsq = __frcp_rn(sq) * 1.000001f;
+      float rsq = rcp_approx(sq) * 1.000001f;   // any sq > 0 gives an upper bound; rcp.approx is within 1 ulp
       for (; it < itA; ++it) {
         const float Wf = (float)(p.b - it - 1);
         const float kW = kWn;
@@ -1635,7 +1635,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fa
         bi = better ? nl : bi;
         bj = better ? nr : bj;
         sq = sqrt_approx(fmaxf(mall, 1e-30f));
-        rsq = __frcp_rn(sq) * 1.000001f;
+        rsq = rcp_approx(sq) * 1.000001f;
       }
     }
     for (;; ++it) {
