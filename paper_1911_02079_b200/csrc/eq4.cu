@@ -2333,6 +2333,14 @@ static int greedy_two_pass(Params p, cudaStream_t s, int nw_exact) {
     if (rc != EQ4_OK) break;
     if (getenv("EQ4_DEV_SKIP_EXACT")) continue;   // development only
     c.list = 1;
+    // wide rows: as few warps per block as packs the most resident warps per SM (the
+    // per-warp slices of k_greedy are 20-43 KB at E >= 128)
+    int nwe = nw_exact, best = 0;
+    for (int w = nw_exact; w >= 1; w >>= 1) {
+      const int per_sm = (int)((227 * 1024) / ((size_t)w * S::bytes(p.stride))) * w;
+      if (per_sm > best) { best = per_sm; nwe = w; }
+    }
+    nw_exact = nwe;
     rc = launch_persistent(k_greedy<LPR, E, true>, nw_exact * S::bytes(p.stride),
                            (c.rows + S::RPW * nw_exact - 1) / (S::RPW * nw_exact), c, s, "k_greedy", 32 * nw_exact);
   }

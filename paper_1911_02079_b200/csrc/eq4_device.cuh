@@ -220,11 +220,51 @@ static __device__ __noinline__ double warp_np_loss(const float* xs, int d, doubl
     return __dadd_rn(0.0, res);
   }
   const FastCodec fc = fast_codec(lo, hi);
+  const int g = lane >> 3, m = lane & 7;
+  if (d >= 256 && d <= 16384 && (d & (d - 1)) == 0) {
+    // power-of-two rows: numpy's halving is exact down to 128-element leaves, so the leaves are
+    // [128 l, 128 l + 128) and they combine as a balanced binary tree -- a shuffle tree over the
+    // leaf sums (a + b == b + a bitwise), no leaf table and no recursion
+    const int nl = d >> 7;
+    for (int base = 0; base < nl; base += 4) {
+      const int r0 = base << 7, n4 = (min(base + 4, nl) - base) << 7;
+      bool near = fc.slow;
+      for (int k = lane; k < n4; k += 32) {
+        const float xf = xs[r0 + k];
+        e2[k] = np_err2_code((double)xf, fast_code(xf, fc, near), cd);
+      }
+      if (__any_sync(FULL, near))   // an element near a rounding boundary: the float64 codec
+        for (int k = lane; k < n4; k += 32) e2[k] = np_err2_fast((double)xs[r0 + k], cd);
+      __syncwarp();
+      const int li = base + g;
+      double r = 0.0;
+      if (li < nl) {
+        r = e2[(g << 7) + m];
+        for (int i = 8 + m; i < 128; i += 8) r = __dadd_rn(r, e2[(g << 7) + i]);
+      }
+      r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 1));
+      r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 2));
+      r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 4));
+      if (li < nl && m == 0) leaf_sum[li] = r;
+      __syncwarp();
+    }
+    // balanced tree over the nl = 2..128 leaf sums: up to 4 per lane, then the lane butterfly
+    const int per = nl > 32 ? nl / 32 : 1;
+    double v = 0.0;
+    if (lane * per < nl) {
+      v = leaf_sum[lane * per];
+      if (per >= 2) v = __dadd_rn(v, leaf_sum[lane * per + 1]);
+      if (per == 4) v = __dadd_rn(v, __dadd_rn(leaf_sum[lane * per + 2], leaf_sum[lane * per + 3]));
+    }
+    const int lanes = nl / per;
+    for (int o = 1; o < lanes; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
+    __syncwarp();
+    return __dadd_rn(0.0, __shfl_sync(FULL, v, 0));
+  }
   int nl = 0;
   if (lane == 0) nl = np_leaves(d, leaf_start, leaf_len, max_leaves);
   nl = __shfl_sync(FULL, nl, 0);
   __syncwarp();
-  const int g = lane >> 3, m = lane & 7;
   for (int base = 0; base < nl; base += 4) {
     const int last = min(base + 4, nl) - 1;
     const int r0 = leaf_start[base], r1 = leaf_start[last] + leaf_len[last];
