@@ -1582,6 +1582,16 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fa
       }
     }
     __syncwarp();
+    // the next row block's rows towards L2 while this one is walked (its setup then waits on
+    // L2, not HBM: -0.7% at 20M x 64, -2.3% at d = 16)
+    {
+      const int64_t nrow = row + wstride * RPW;
+      if (nrow < p.rows) {
+        const char* np = reinterpret_cast<const char*>(p.x + nrow * p.ld) + q * 16;
+        for (int o = 0; o < E * 4 * LPR; o += 128 * LPR)
+          asm volatile("prefetch.global.L2 [%0];" :: "l"(np + o));
+      }
+    }
     const float Wf0 = (float)p.b;                                                     // :174
     float Lbest = group_sum<LPR>(eval_one_x2<E>(ysl, 0.f, -Wf0, kw_of(Wf0), hh));
     int nl = 0, nr = 0, bi = 0, bj = 0;
