@@ -1587,7 +1587,7 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fa
     {
       const int64_t nrow = row + wstride * RPW;
       if (nrow < p.rows) {
-        const char* np = reinterpret_cast<const char*>(p.x + nrow * p.ld) + q * 16;
+        const char* np = reinterpret_cast<const char*>(p.x + nrow * p.ld) + q * 128;
         for (int o = 0; o < E * 4 * LPR; o += 128 * LPR)
           asm volatile("prefetch.global.L2 [%0];" :: "l"(np + o));
       }
