@@ -120,8 +120,15 @@ struct Params {
   // k_greedy with list != 0 then runs exactly those rows
   uint32_t* dlist;
   int* dcount;
-  int list;
+  int list;          // k_greedy: 0 all rows, 1 the deferred rows (restart list + resume records)
+  // resume records (b <= 65535): a row deferred during the walk is stored with its state at
+  // the last checkpoint (iteration 8k, k = 1..RG_GROUPS-1) in group k -- {row, nl | bi << 16,
+  // bj, Lbest bits} -- and k_greedy (list mode) continues it from iteration 8k
+  uint4* drec;
+  int* drec_count;   // [RG_GROUPS]; [0] unused
+  int drec_cap;      // records per group
 };
+constexpr int RG_GROUPS = 8;   // checkpoints at iterations 8, 16, ..., 56
 
 // Copy nbytes from shared src to global dst; src and dst agree modulo 16.
 __device__ __forceinline__ void copy_out(uint8_t* dst, const uint8_t* src, int nbytes) {
@@ -1154,16 +1161,35 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
   const float hh = 0.5f / ALPHA;
   // list mode: the rows the screening kernel deferred (dlist[0 .. *dcount)), each
   // written on its own; otherwise blocks of RPW consecutive rows
-  const int64_t nlist = p.list ? (int64_t)*reinterpret_cast<volatile const int*>(p.dcount) : 0;
-  const int64_t nunits = p.list ? nlist : p.rows;
-  const int64_t nblocks = (nunits + RPW - 1) / RPW;
+  // list mode: the restart list (group 0) then the resume groups 1.. in one index space of
+  // RPW-row units, so every warp's rows start at one iteration (8g) and the longest rows
+  // (restarts) are handed out first
+  int64_t gcnt[RG_GROUPS], gcum[RG_GROUPS + 1];
+  gcum[0] = 0;
+#pragma unroll
+  for (int g = 0; g < RG_GROUPS; g++) {
+    int64_t n = 0;
+    if (p.list) {
+      if (g == 0) n = *reinterpret_cast<volatile const int*>(p.dcount);
+      else if (p.drec) n = min((int64_t)*reinterpret_cast<volatile const int*>(p.drec_count + g), (int64_t)p.drec_cap);
+    }
+    gcnt[g] = n;
+    gcum[g + 1] = gcum[g] + (n + RPW - 1) / RPW;
+  }
+  const int64_t nblocks = p.list ? gcum[RG_GROUPS] : (p.rows + RPW - 1) / RPW;
   const int nwb = (int)(blockDim.x >> 5);   // warps per block (fewer for wide rows)
   const int64_t wstride = (int64_t)gridDim.x * nwb;
 
   for (int64_t blk = (int64_t)blockIdx.x * nwb + warp; blk < nblocks; blk += wstride) {
-    const int64_t row0 = blk * RPW;
+    int grp = 0;
+#pragma unroll
+    for (int g = 1; g < RG_GROUPS; g++) grp = (p.list && blk >= gcum[g]) ? g : grp;
+    const int64_t row0 = p.list ? (blk - gcum[grp]) * RPW : blk * RPW;
+    const int64_t nunits = p.list ? gcnt[grp] : p.rows;
     const bool rvalid = row0 + gw < nunits;
-    const int64_t row = p.list ? (rvalid ? (int64_t)p.dlist[row0 + gw] : 0) : row0 + gw;
+    uint4 rec = make_uint4(0u, 0u, 0u, 0u);
+    if (grp > 0 && rvalid) rec = p.drec[(size_t)grp * p.drec_cap + row0 + gw];
+    const int64_t row = grp > 0 ? (int64_t)rec.x : p.list ? (rvalid ? (int64_t)p.dlist[row0 + gw] : 0) : row0 + gw;
     RowShared& R = rs[gw];
     // the raw rows stay in global memory (L1/L2-resident while the block is
     // searched): only the rare exact decisions and code fix-ups read them
@@ -1307,7 +1333,21 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
       if (!(M <= 1e6f * Dwf)) flags |= F_EXACT_ONLY;   // reference grid rounds coarsely
     }
     float Lbest;
-    {
+    int nl = 0, nr = 0, bi = 0, bj = 0, iters = 0;
+    float BLf = 15.f;                       // base of the L candidate, 15 * (nl + 1)
+    int it = 0;
+    if (grp > 0) {
+      // resume where the screening kernel's checkpoint left the row: its fp32 walk up to
+      // iteration 8 grp is this kernel's own (same evaluations, all outside the band)
+      Lbest = __uint_as_float(rec.w);
+      nl = (int)(rec.y & 0xFFFFu);
+      bi = (int)(rec.y >> 16);
+      bj = (int)rec.z;
+      it = 8 * grp;
+      nr = it - nl;
+      iters = it;
+      BLf = 15.f * (float)(nl + 1);
+    } else {
       const float Wf = (float)p.b;                                                   // :174
       float a0;
       if constexpr (VEC)
@@ -1316,9 +1356,6 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GREEDY_MINB : (E <= 32 ?
         a0 = eval_one<E, true>(ys4, nv, 0.f, -Wf, kw_of(Wf), hh);
       Lbest = group_sum<LPR>(a0);
     }
-    int nl = 0, nr = 0, bi = 0, bj = 0, iters = 0;
-    float BLf = 15.f;                       // base of the L candidate, 15 * (nl + 1)
-    int it = 0;
     // Phase A: for it < it_exact_from every active row provably stays in the
     // loop (its float64 condition holds by >= 2 steps) and W >= 1, so the body
     // is straight-line: evaluate, reduce, decide.  An iteration that needs an
@@ -1597,6 +1634,15 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fa
     int nl = 0, nr = 0, bi = 0, bj = 0;
     float BLf = 15.f;                      // base of the L candidate, 15 * (nl + 1)
     int it = 0;
+    // the walk's state at the last checkpoint (iteration 8k) before a deferral: the exact kernel
+    // resumes the row from there (resume records, Params::drec)
+    int cp_it = 0, cp_nl = 0, cp_bi = 0, cp_bj = 0;
+    float cp_L = 0.f;
+    auto checkpoint = [&](int at) {
+      if ((at & 7) == 0 && at > 0 && at < 8 * RG_GROUPS && !defer) {
+        cp_it = at; cp_nl = nl; cp_bi = bi; cp_bj = bj; cp_L = Lbest;
+      }
+    };
     {
       // Phase A: iterations whose loop condition provably holds (it < it_exact_from) and
       // whose width takes the shift evaluation (W >= 17): straight-line body, no float64
@@ -1609,7 +1655,10 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fa
       float kWn = kw_of((float)(p.b - 1));
       float sq = sqrt_approx(fmaxf(Lbest, 1e-30f));
       float rsq = rcp_approx(sq) * 1.000001f;   // any sq > 0 gives an upper bound; rcp.approx is within 1 ulp
-      for (; it < itA; ++it) {
+      for (; it < itA;) {
+      checkpoint(it);   // once per 8 iterations
+      const int itE = min(itA, (it & ~7) + 8);
+      for (; it < itE; ++it) {
         const float Wf = (float)(p.b - it - 1);
         const float kW = kWn;
         kWn = kw_of(Wf - 1.f);
@@ -1647,8 +1696,10 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fa
         sq = sqrt_approx(fmaxf(mall, 1e-30f));
         rsq = rcp_approx(sq) * 1.000001f;
       }
+      }
     }
     for (;; ++it) {
+      checkpoint(it);
       if (active && it >= p.it_exact_from) {   // clipping.py:180 in float64 (earlier: provably true)
         const RowFast& R = rf[gw];
         const double lhs = __dadd_rn(__dadd_rn(R.x0, __dmul_rn((double)nl, R.step)), R.min_steps);
@@ -1782,11 +1833,25 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fa
       if (p.info0) p.info0[row] = nl + nr;
       if (p.info1) p.info1[row] = p.b > 65535 ? bi : ((bi << 16) | bj);
     }
-    // deferred rows: one list slot each (about 2% of the rows)
+    // deferred rows (about 2% of the rows): a resume record when the walk passed a checkpoint,
+    // else (or when the group is full) a slot of the restart list
     if (rvalid && defer && q == 0) {
-      const unsigned slot = (unsigned)atomicAdd(p.dcount, 1);
-      GF_CHECK(slot < p.rows, "dlist", slot);
-      p.dlist[slot] = (uint32_t)row;
+      bool stored = false;
+      if (p.drec && cp_it > 0) {
+        const int k = cp_it >> 3;
+        const int slot = atomicAdd(&p.drec_count[k], 1);
+        if (slot < p.drec_cap) {
+          p.drec[(size_t)k * p.drec_cap + slot] =
+              make_uint4((unsigned)row, (unsigned)cp_nl | ((unsigned)cp_bi << 16), (unsigned)cp_bj,
+                         __float_as_uint(cp_L));
+          stored = true;
+        }
+      }
+      if (!stored) {
+        const unsigned slot = (unsigned)atomicAdd(p.dcount, 1);
+        GF_CHECK(slot < p.rows, "dlist", slot);
+        p.dlist[slot] = (uint32_t)row;
+      }
       ++ndefer;
     }
     __syncwarp();
@@ -2319,8 +2384,16 @@ static int greedy_two_pass(Params p, cudaStream_t s, int nw_exact) {
   const int64_t chunk = (int64_t)1 << 30;   // list entries are 32-bit row offsets
   uint32_t* buf = nullptr;
   const int64_t cap = std::min<int64_t>(p.rows, chunk);
-  cudaError_t e = cudaMallocAsync((void**)&buf, (size_t)(cap + 4) * 4, s);
+  // restart list (4 B per row) + resume records (16 B, groups 1..RG_GROUPS-1, b <= 65535)
+  const bool resume = p.b <= 65535 && !getenv("EQ4_DEV_NO_RESUME");   // (env: development A/B only)
+  int64_t rcap = resume ? std::min<int64_t>(cap, (int64_t)1 << 18) : 0;
+  if (const char* ev = getenv("EQ4_DEV_RCAP")) rcap = resume ? std::min<int64_t>(rcap, atoll(ev)) : 0;   // tests: overflow
+  const size_t list_bytes = ((size_t)(cap + 4) * 4 + 255) & ~(size_t)255;
+  const size_t rec_bytes = (size_t)rcap * RG_GROUPS * 16;
+  cudaError_t e = cudaMallocAsync((void**)&buf, list_bytes + rec_bytes + 64, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  int* rcount = reinterpret_cast<int*>(reinterpret_cast<char*>(buf) + list_bytes + rec_bytes);
+  uint4* recs = resume ? reinterpret_cast<uint4*>(reinterpret_cast<char*>(buf) + list_bytes) : nullptr;
   int nwf = NWARPS_G;
   while (nwf > 1 && (size_t)nwf * F::bytes(p.stride) > 220 * 1024) nwf >>= 1;
   int rc = EQ4_OK;
@@ -2335,7 +2408,11 @@ static int greedy_two_pass(Params p, cudaStream_t s, int nw_exact) {
     if (p.info1) c.info1 = p.info1 + r0;
     c.dcount = reinterpret_cast<int*>(buf);
     c.dlist = buf + 4;
+    c.drec = recs;
+    c.drec_count = rcount;
+    c.drec_cap = (int)rcap;
     e = cudaMemsetAsync(c.dcount, 0, 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(rcount, 0, RG_GROUPS * sizeof(int), s);
     if (e != cudaSuccess) { rc = cuda_fail(e, "cudaMemsetAsync"); break; }
     c.list = 0;
     rc = launch_persistent(k_greedy_fast<LPR, E>, nwf * F::bytes(p.stride),

@@ -17,9 +17,11 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-def _run(eq, x, one_pass):
+def _run(eq, x, one_pass, env=None):
     if one_pass:
         os.environ["EQ4_DEV_ONE_PASS"] = "1"
+    for k, v in (env or {}).items():
+        os.environ[k] = v
     try:
         rows, d = x.shape
         out = torch.zeros(rows * eq.packed_row_stride(d, "fp16"), dtype=torch.uint8, device="cuda")
@@ -35,6 +37,8 @@ def _run(eq, x, one_pass):
         return out.cpu().numpy(), rr, diag
     finally:
         os.environ.pop("EQ4_DEV_ONE_PASS", None)
+        for k in (env or {}):
+            os.environ.pop(k, None)
 
 
 @pytest.mark.parametrize("d,rows", [(16, 40_000), (64, 30_000), (128, 12_000), (1024, 1_500)])
@@ -72,3 +76,20 @@ def test_two_pass_all_rows_deferred():
     assert diag["deferred_rows"] == 3000
     want = oracle.quantize_pack_table(xh, "greedy", 200, 0.16, "fp16")
     assert np.array_equal(got, want.packed)
+
+
+@pytest.mark.parametrize("env", [{"EQ4_DEV_RCAP": "40"}, {"EQ4_DEV_NO_RESUME": "1"}])
+def test_two_pass_resume_overflow_and_restart(env):
+    """Deferred rows resume from the screen's last checkpoint (iteration 8k) when their group has
+    room and restart otherwise: a 40-record cap (most resumable rows overflow to the restart list)
+    and resuming switched off give the same bytes as the one-kernel path."""
+    import paper_1911_02079_b200 as eq
+
+    xh = rng.mixed_table(20_000, 64, 31)
+    x = torch.from_numpy(xh).cuda()
+    got, rr, diag = _run(eq, x, one_pass=False, env=env)
+    ref, rr1, _ = _run(eq, x, one_pass=True)
+    assert diag["deferred_rows"] > 100, diag
+    assert np.array_equal(got, ref)
+    for f in ("xmin", "xmax", "info0", "info1"):
+        assert torch.equal(getattr(rr, f), getattr(rr1, f)), f
