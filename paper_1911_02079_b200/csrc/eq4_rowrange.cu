@@ -493,6 +493,170 @@ __global__ void __launch_bounds__(256, NCH >= 16 ? 4 : 3) k_aciq8(const RRParams
   }
 }
 
+// ACIQ at d = 64, four lanes per row (eight rows per warp): lane q owns numpy's chains 2q and
+// 2q+1 (elements 2q + 8k and 2q + 1 + 8k: one 8-byte load per k, the row's four lanes cover
+// 32 contiguous bytes), so the leaf tree's first level (r_2q + r_2q+1) is lane-local and the
+// other two are xor-shuffles over the four lanes; the per-row work (trees, range, codec
+// constants) is shared by 4 lanes instead of 8.  Every lane's element pairs are whole packed
+// bytes (byte q + 4k), transposed 4 x 4 across the row's lanes for 32-bit stores.
+template <int NPL>   // elements per lane (16 at d = 64)
+__device__ __forceinline__ void aciq4_row(const RRParams& p, const float (&x)[NPL], int64_t row, bool rvalid,
+                                          int q, double n, double rn) {
+  constexpr unsigned FULLM = 0xffffffffu;
+  constexpr int NK = NPL / 2;   // elements per chain
+  // np.mean (clipping.py:135): chains 2q (even slots) and 2q+1 (odd slots), the tree, 0.0 +
+  double ra = (double)x[0], rb = (double)x[1];
+#pragma unroll
+  for (int k = 1; k < NK; ++k) {
+    ra = __dadd_rn(ra, (double)x[2 * k]);
+    rb = __dadd_rn(rb, (double)x[2 * k + 1]);
+  }
+  double r = __dadd_rn(ra, rb);
+  r = __dadd_rn(r, __shfl_xor_sync(FULLM, r, 1));
+  r = __dadd_rn(r, __shfl_xor_sync(FULLM, r, 2));
+  const double sum = __dadd_rn(0.0, r);
+  const bool bad = !isfinite(sum);
+  const double mean = __dmul_rn(sum, rn);   // d = 64: exact scaling
+  double aa = fabs(__dsub_rn((double)x[0], mean)), ab = fabs(__dsub_rn((double)x[1], mean));
+#pragma unroll
+  for (int k = 1; k < NK; ++k) {
+    aa = __dadd_rn(aa, fabs(__dsub_rn((double)x[2 * k], mean)));
+    ab = __dadd_rn(ab, fabs(__dsub_rn((double)x[2 * k + 1], mean)));
+  }
+  double a = __dadd_rn(aa, ab);
+  a = __dadd_rn(a, __shfl_xor_sync(FULLM, a, 1));
+  a = __dadd_rn(a, __shfl_xor_sync(FULLM, a, 2));
+  const double alpha = __dmul_rn(p.aciq_const, __dmul_rn(__dadd_rn(0.0, a), rn));
+  double lo = __dsub_rn(mean, alpha), hi = __dadd_rn(mean, alpha);
+  (void)n;
+  const bool flat = rvalid && !bad && alpha == 0.0;
+  if (__any_sync(FULLM, flat)) {   // rare: clipping.py:137-138 -> clip_range_asym (numpy's zero choice)
+    float mn = x[0], mx = x[0];
+#pragma unroll
+    for (int k = 1; k < NPL; ++k) { mn = fminf(mn, x[k]); mx = fmaxf(mx, x[k]); }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      mn = fminf(mn, __shfl_xor_sync(FULLM, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(FULLM, mx, o));
+    }
+    unsigned kz = 0u;
+    if (mn == 0.f || mx == 0.f) {
+#pragma unroll
+      for (int k = 0; k < NPL; ++k) kz = max(kz, np_zero_key_t(x[k], 2 * q + (k & 1) + 8 * (k >> 1), p.d));
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) kz = max(kz, __shfl_xor_sync(FULLM, kz, o));
+    if (flat) {
+      const double z = (kz & 1u) ? -0.0 : 0.0;
+      lo = mn == 0.f ? z : (double)mn;
+      hi = mx == 0.f ? z : (double)mx;
+    }
+  }
+  if (bad) { lo = 0.0; hi = 0.0; }
+  const bool degenerate = bad || hi == lo;
+  const double w64 = __dsub_rn(hi, lo);
+  const float lo_hi = __double2float_rn(lo), lo_lo = __double2float_rn(__dsub_rn(lo, (double)lo_hi));
+  const float wf = __double2float_rn(w64);
+  const float inv1 = degenerate ? 0.f : __fdividef(1.f, wf);
+  const bool slow = !degenerate && !(wf > 1e-30f && wf < 1e30f && fabsf(lo_hi) < 1e30f &&
+                                     fabsf(__double2float_rn(hi)) < 1e30f);
+  // codes: element pairs (2q + 8k, 2q + 1 + 8k) are packed byte q + 4k; bytes k = 0..3 / 4..7
+  uint32_t wb[NK / 4];
+#pragma unroll
+  for (int g = 0; g < NK / 4; ++g) wb[g] = 0u;
+  float gmax = 0.f;
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    unsigned cc[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float sv = __saturatef(__fmul_rn(__fadd_rn(__fadd_rn(x[2 * k + h], -lo_hi), -lo_lo), inv1));
+      const float m = __fadd_rd(__fmaf_rn(sv, 15.f, 0.5f), 8388608.f);
+      gmax = fmaxf(gmax, fabsf(__fmaf_rn(sv, 15.f, -__fadd_rn(m, -8388608.f))));
+      cc[h] = __float_as_uint(m) & 0xFu;
+    }
+    wb[k >> 2] |= (cc[0] | (cc[1] << 4)) << (8 * (k & 3));
+  }
+  const bool exact = rvalid && (degenerate || slow || gmax > 0.5f - NEAR);
+  if (__any_sync(FULLM, exact) && exact) {
+    const CodeParams cp = make_code_params(degenerate ? 0.0 : lo, degenerate ? 0.0 : hi);
+#pragma unroll
+    for (int g = 0; g < NK / 4; ++g) wb[g] = 0u;
+#pragma unroll
+    for (int k = 0; k < NK; ++k)
+      wb[k >> 2] |= (code_exact(x[2 * k], cp) | (code_exact(x[2 * k + 1], cp) << 4)) << (8 * (k & 3));
+  }
+  // 4 x 4 byte transpose across the row's lanes: lane t ends with bytes 4t..4t+3 of each group
+#pragma unroll
+  for (int g = 0; g < NK / 4; ++g) {
+#pragma unroll
+    for (int b = 2; b >= 1; b >>= 1) {
+      const unsigned msk = b == 2 ? 0x0000FFFFu : 0x00FF00FFu;
+      const int sh = 8 * b;
+      const unsigned pw = __shfl_xor_sync(FULLM, wb[g], b);
+      wb[g] = (q & b) ? (((pw & ~msk) >> sh) | (wb[g] & ~msk)) : ((wb[g] & msk) | ((pw & msk) << sh));
+    }
+  }
+  if (rvalid) {
+    uint8_t* orow = p.packed + (size_t)row * p.stride;
+#pragma unroll
+    for (int g = 0; g < NK / 4; ++g) *reinterpret_cast<uint32_t*>(orow + 16 * g + 4 * q) = wb[g];
+    if (q == 0) {
+      const double sc = degenerate ? 0.0 : div15(w64);   // uniform.py:74-80
+      uint32_t* a4 = reinterpret_cast<uint32_t*>(orow + p.half);
+      if (p.aux == EQ4_AUX_FP16) {
+        a4[0] = aux_bits_f16(sc) | (aux_bits_f16(lo) << 16);
+      } else {
+        a4[0] = aux_bits_f32(sc);
+        a4[1] = aux_bits_f32(lo);
+      }
+      if (p.lo_out) { p.lo_out[row] = lo; p.hi_out[row] = hi; }
+      if (p.info0) p.info0[row] = 0;
+      if (bad && p.status) atomicOr(p.status, EQ4_STATUS_NONFINITE);
+    }
+  }
+}
+
+#ifndef ACIQ4_MINB
+#define ACIQ4_MINB 2   // 124 registers: the next row set's 16 floats stay in registers (3: spills, 0.38 ms)
+#endif
+__global__ void __launch_bounds__(256, ACIQ4_MINB) k_aciq4(const RRParams p) {
+  constexpr int NPL = 16;   // d = 64: 2 chains x 8 elements per lane
+  const int lane = threadIdx.x & 31, q = lane & 3;
+  const int64_t nsets = (p.rows + 7) / 8;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const double n = (double)p.d, rn = 1.0 / n;
+  float xn[NPL];
+  {
+    const int64_t row = wid * 8 + (lane >> 2);
+    const float2* xr = reinterpret_cast<const float2*>(p.x + (row < p.rows ? row : 0) * p.ld) + q;
+#pragma unroll
+    for (int k = 0; k < NPL / 2; ++k) {
+      const float2 t = __ldcs(xr + 4 * k);
+      xn[2 * k] = t.x;
+      xn[2 * k + 1] = t.y;
+    }
+  }
+  for (int64_t set = wid; set < nsets; set += nw) {
+    const int64_t row = set * 8 + (lane >> 2);
+    float x[NPL];
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) x[k] = xn[k];
+    if (set + nw < nsets) {
+      const int64_t rown = row + 8 * nw;
+      const float2* xr = reinterpret_cast<const float2*>(p.x + (rown < p.rows ? rown : 0) * p.ld) + q;
+#pragma unroll
+      for (int k = 0; k < NPL / 2; ++k) {
+        const float2 t = __ldcs(xr + 4 * k);
+        xn[2 * k] = t.x;
+        xn[2 * k + 1] = t.y;
+      }
+    }
+    aciq4_row<NPL>(p, x, row, row < p.rows, q, n, rn);
+  }
+}
+
 // The scalar entry points on float64 rows (clip_range_aciq / clip_range_gss of any array,
 // clipping.py:46 promotes it to float64): ranges (and GSS evaluation counts) only, lane
 // per row straight from global memory.
@@ -561,15 +725,17 @@ int eq4_rowrange_launch(const float* x, int64_t rows, int64_t dim, int64_t ld, i
   if (method == EQ4_METHOD_ACIQ && (dim == 64 || dim == 128) && ((uintptr_t)packed & 3) == 0 &&
       !getenv("EQ4_DEV_ACIQ_LANE")) {   // (env: development A/B only)
     const int nch = (int)(dim / 8);
-    auto kern = nch == 1 ? k_aciq8<1> : nch == 2 ? k_aciq8<2> : nch == 4 ? k_aciq8<4> : nch == 8 ? k_aciq8<8>
-              : nch == 16 ? k_aciq8<16> : nullptr;
+    // d = 64 with 8-byte aligned rows: four lanes per row (k_aciq4), else eight (k_aciq8)
+    const bool four = dim == 64 && (ld % 2) == 0 && (((uintptr_t)x & 7) == 0) && !getenv("EQ4_DEV_ACIQ8");
+    auto kern = four ? k_aciq4 : nch == 1 ? k_aciq8<1> : nch == 2 ? k_aciq8<2> : nch == 4 ? k_aciq8<4>
+              : nch == 8 ? k_aciq8<8> : nch == 16 ? k_aciq8<16> : nullptr;
     if (kern) {
       int dev = 0, sms = 0, per_sm = 0;
       cudaError_t e = cudaGetDevice(&dev);
       if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
       if (e != cudaSuccess) { err = std::string("k_aciq8 setup: ") + cudaGetErrorString(e); return EQ4_ECUDA; }
-      const int64_t nsets = (rows + 3) / 4;
+      const int64_t nsets = (rows + (four ? 7 : 3)) / (four ? 8 : 4);
       int64_t grid = (nsets + 7) / 8;
       const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
       if (grid > cap) grid = cap;
