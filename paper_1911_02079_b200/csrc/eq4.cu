@@ -2394,8 +2394,15 @@ static int greedy_two_pass(Params p, cudaStream_t s, int nw_exact) {
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
   int* rcount = reinterpret_cast<int*>(reinterpret_cast<char*>(buf) + list_bytes + rec_bytes);
   uint4* recs = resume ? reinterpret_cast<uint4*>(reinterpret_cast<char*>(buf) + list_bytes) : nullptr;
+  // warps per block: as many as pack the most resident warps per SM (wide rows: 17-33 KB slices)
   int nwf = NWARPS_G;
-  while (nwf > 1 && (size_t)nwf * F::bytes(p.stride) > 220 * 1024) nwf >>= 1;
+  {
+    int best = 0;
+    for (int w = NWARPS_G; w >= 1; w >>= 1) {
+      const int per_sm = (int)((227 * 1024) / ((size_t)w * F::bytes(p.stride))) * w;
+      if (per_sm > best) { best = per_sm; nwf = w; }
+    }
+  }
   int rc = EQ4_OK;
   const int64_t rows = p.rows;
   for (int64_t r0 = 0; r0 < rows && rc == EQ4_OK; r0 += chunk) {
