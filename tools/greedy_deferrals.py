@@ -1,3 +1,5 @@
+"""GREEDY rare-path counters (deferred rows, exact re-decisions, near-boundary counts) with and
+without the exact pass:  python tools/greedy_deferrals.py rows:d:dist ..."""
 import os, sys; sys.path.insert(0, '.')
 import torch, paper_1911_02079_b200 as eq
 from paper_1911_02079_b200 import workloads, _lib

@@ -1,3 +1,5 @@
+"""GREEDY device time of the two-pass path and of the screening kernel alone (EQ4_DEV_SKIP_EXACT),
+for A/B of library variants (EQ4_LIB=variants/libeq4_NAME.so):  python tools/time_greedy.py rows:d:dist ..."""
 import os, sys; sys.path.insert(0, '.')
 import torch, paper_1911_02079_b200 as eq
 from paper_1911_02079_b200 import workloads

@@ -1,3 +1,4 @@
+"""KMEANS rows and HIST-APPRX device time (A/B of library variants via EQ4_LIB)."""
 import os, sys; sys.path.insert(0, '.')
 import torch, paper_1911_02079_b200 as eq
 from paper_1911_02079_b200 import workloads
