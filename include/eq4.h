@@ -11,7 +11,13 @@
  * Conventions
  *   - Device entry points (eq4_quantize_pack, eq4_pack, eq4_unpack,
  *     eq4_quant_mse) take DEVICE pointers and a cudaStream_t passed as void*;
- *     they are stream-ordered and never synchronize the host.
+ *     they are stream-ordered and never synchronize the host.  GREEDY on
+ *     vector rows (d % 4 == 0, 16-byte aligned) runs two kernels on the
+ *     stream -- an fp32 screening kernel, then the exact kernel over the rows
+ *     it deferred -- with stream-ordered scratch from the device's default
+ *     memory pool (cudaMallocAsync: 4 bytes per row + 28 MB of resume
+ *     records); the first such call raises that pool's release threshold so
+ *     the scratch is recycled, not remapped, by later calls.
  *   - Return 0 on success, an EQ4_E* code otherwise (argument errors are
  *     detected synchronously, before any launch); eq4_last_error() returns a
  *     thread-local message for the last failure on the calling thread.
