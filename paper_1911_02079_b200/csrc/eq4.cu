@@ -61,10 +61,11 @@ constexpr int NWARPS_G = NTHREADS_G / 32;
 constexpr int MAX_LEAVES = 64;          // numpy pairwise leaves for d <= 4096
 constexpr float ALPHA = 15.75f;         // saturation scale for the code FFMA
 // |alpha * s - (z/W + 1/2)| <= ETA_CODE for s = RN(z * kw_of(W) + h), |z/W| <= 15.5:
-// 15.5 * 2^-23 (kW within 1 ulp) + 15.75 * 2^-25 (s rounded once) = 2.32e-6.
-constexpr double ETA_CODE = 2.6e-6;
+// 15.5 * (2^-24 + 2^-46) (kW rounded once after one Newton step) + 15.75 * 2^-25 (s rounded
+// once) + 15.75 * 2^-24 * h (h = 1/(2 alpha) rounded) = 1.43e-6.
+constexpr double ETA_CODE = 1.6e-6;
 // elements counted as able to take the other code: within ETA_CODE (+ margin) + delta/W
-constexpr float NEAR_CNT = 3.5e-6f;
+constexpr float NEAR_CNT = 2.2e-6f;
 constexpr float MAGIC = 8388608.f;      // 2^23
 enum { M_ASYM = 0, M_GREEDY = 1 };
 #ifndef GREEDY_MINB
@@ -208,10 +209,14 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   return r;
 }
 
-// 1 / (W alpha) by rcp.approx (max error 1 ulp; W alpha is exact in fp32 for
+// 1 / (W alpha): rcp.approx (1 ulp) refined by one Newton step (W alpha is exact in fp32 for
 // W < 2^18): the search's code argument alpha * sat(z * kW + h) is then within
 // ETA_CODE of (z / W + 1/2).
-__device__ __forceinline__ float kw_of(float Wf) { return rcp_approx(Wf * ALPHA); }
+__device__ __forceinline__ float kw_of(float Wf) {
+  const float x = Wf * ALPHA;            // exact (W < 2^18)
+  const float r = rcp_approx(x);         // within 1 ulp
+  return __fmaf_rn(r, __fmaf_rn(-x, r, 1.f), r);   // one Newton step: 1/x within 2^-24 + 2^-46
+}
 
 __device__ __forceinline__ float sat_fma(float a, float b, float c) {
   float r;
