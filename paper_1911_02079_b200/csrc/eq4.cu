@@ -128,6 +128,9 @@ struct Params {
   uint4* drec;
   int* drec_count;   // [RG_GROUPS]; [0] unused
   int drec_cap;      // records per group
+  // table walk (k_greedy_table, eq4_gtable.cuh): band = tb_eps mr L + (tb_c1a + tb_c1b mr) sqrt(L) + tb_c0
+  // with mr = max(1, max|x| / (max - min)) of the row
+  double tb_eps, tb_c1a, tb_c1b, tb_c0;
 };
 constexpr int RG_GROUPS = 8;   // checkpoints at iterations 8, 16, ..., 56
 
@@ -1869,6 +1872,8 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fa
   if (ndefer) atomicAdd(&g_diag[4], (unsigned long long)ndefer);
 }
 
+#include "eq4_gtable.cuh"
+
 // ---------------------------------------------------------------------------
 // ASYM vector kernel: warp-autonomous (per-warp staging, no block barriers),
 // the next row block's loads in flight while the current one is coded, and
@@ -2381,6 +2386,15 @@ static void keep_pool_memory() {
 // GREEDY on vector rows: k_greedy_fast screens every row, then k_greedy (list mode)
 // redoes the deferred ones with the exact tier.  Both on stream s, no host sync;
 // the deferral list (4 bytes per row) is stream-ordered scratch.
+// Rows the table walk takes (eq4_gtable.cuh): wide vector rows whose table fits a warp's
+// share of shared memory and whose integer sums fit 64 bits (d * 15 b < 2^27).
+static bool table_walk_applies(const Params& p) {
+  int min_d = 1024;
+  if (const char* ev = getenv("EQ4_DEV_TABLE_MIN_D")) min_d = atoi(ev);   // development A/B only
+  return p.d >= min_d && p.d <= 16384 && p.b <= 400 && (int64_t)p.d * 15 * p.b < ((int64_t)1 << 27) &&
+         p.rows < ((int64_t)1 << 32);
+}
+
 template <int LPR, int E>
 static int greedy_two_pass(Params p, cudaStream_t s, int nw_exact) {
   keep_pool_memory();
@@ -2427,8 +2441,18 @@ static int greedy_two_pass(Params p, cudaStream_t s, int nw_exact) {
     if (e == cudaSuccess) e = cudaMemsetAsync(rcount, 0, RG_GROUPS * sizeof(int), s);
     if (e != cudaSuccess) { rc = cuda_fail(e, "cudaMemsetAsync"); break; }
     c.list = 0;
-    rc = launch_persistent(k_greedy_fast<LPR, E>, nwf * F::bytes(p.stride),
-                           (c.rows + F::RPW * nwf - 1) / (F::RPW * nwf), c, s, "k_greedy_fast", 32 * nwf);
+    if (table_walk_applies(p)) {
+      const size_t tb = TableSlice::bytes(p.b);
+      int nwt = 4, bestt = 0;
+      for (int w = 4; w >= 1; w >>= 1) {
+        const int per_sm = (int)((227 * 1024) / ((size_t)w * tb + 1024)) * w;
+        if (per_sm > bestt) { bestt = per_sm; nwt = w; }
+      }
+      rc = launch_persistent(k_greedy_table, nwt * tb, (c.rows + nwt - 1) / nwt, c, s, "k_greedy_table", 32 * nwt);
+    } else {
+      rc = launch_persistent(k_greedy_fast<LPR, E>, nwf * F::bytes(p.stride),
+                             (c.rows + F::RPW * nwf - 1) / (F::RPW * nwf), c, s, "k_greedy_fast", 32 * nwf);
+    }
     if (rc != EQ4_OK) break;
     if (getenv("EQ4_DEV_SKIP_EXACT")) continue;   // development only
     c.list = 1;
@@ -2866,6 +2890,19 @@ static int quantize_pack_impl(const float* x, int64_t rows, int64_t dim, int64_t
     p.tau2 += (float)(2.0 * 3e-14 * 1e6);
     p.c1 = (float)(4.2 * p.delta * std::sqrt((double)dim));
     p.c0 = (float)(2.1 * (double)dim * p.delta * p.delta);
+    {
+      // table walk (eq4_gtable.cuh): y on the 2^-33 grid (plus the float64 rounding of Y itself);
+      // the reference's reconstruction rounds at 2^-53 max|x| per element -- in Y units
+      // 2^-52 * 15 b * mr over both roundings -- and its sums and squares at a few 2^-53 relative
+      // (3e-14 mr with the candidate grid, as above); the polynomial's float64 evaluation and the
+      // conversions of P1 and the chi sum move a candidate by <= 17 * 2^-53 * d (15 b)^2.
+      const double Yb = 15.0 * b, u = std::ldexp(1.0, -53);
+      const double dl = std::ldexp(1.0, -34) + 8.0 * u * Yb;
+      p.tb_eps = 2.1 * 3e-14;
+      p.tb_c1a = 4.2 * dl * std::sqrt((double)dim);
+      p.tb_c1b = 4.2 * 2.0 * u * Yb * std::sqrt((double)dim);
+      p.tb_c0 = 2.1 * (double)dim * dl * dl + 40.0 * u * (double)dim * Yb * Yb + 1e-9 * (double)dim;
+    }
     return dispatch_rq<M_GREEDY>(p, vec, s);
   }
   if (method == EQ4_METHOD_HIST_BRUTE) {
