@@ -2389,7 +2389,8 @@ static void keep_pool_memory() {
 // Rows the table walk takes (eq4_gtable.cuh): wide vector rows whose table fits a warp's
 // share of shared memory and whose integer sums fit 64 bits (d * 15 b < 2^27).
 static bool table_walk_applies(const Params& p) {
-  int min_d = 1024;
+  // measured crossover against the per-element screen on 1 GiB N(0,1) tables (K2)
+  int min_d = 4096;
   if (const char* ev = getenv("EQ4_DEV_TABLE_MIN_D")) min_d = atoi(ev);   // development A/B only
   return p.d >= min_d && p.d <= 16384 && p.b <= 400 && (int64_t)p.d * 15 * p.b < ((int64_t)1 << 27) &&
          p.rows < ((int64_t)1 << 32);
