@@ -131,6 +131,7 @@ struct Params {
   // table walk (k_greedy_table, eq4_gtable.cuh): band = tb_eps mr L + (tb_c1a + tb_c1b mr) sqrt(L) + tb_c0
   // with mr = max(1, max|x| / (max - min)) of the row
   double tb_eps, tb_c1a, tb_c1b, tb_c0;
+  int tb_wave;   // blocks per grid wave (the SM count): picks each block's walking warp
 };
 constexpr int RG_GROUPS = 8;   // checkpoints at iterations 8, 16, ..., 56
 
@@ -2390,7 +2391,7 @@ static void keep_pool_memory() {
 // share of shared memory and whose integer sums fit 64 bits (d * 15 b < 2^27).
 static bool table_walk_applies(const Params& p) {
   // measured crossover against the per-element screen on 1 GiB N(0,1) tables (K2)
-  int min_d = 4096;
+  int min_d = 2048;
   if (const char* ev = getenv("EQ4_DEV_TABLE_MIN_D")) min_d = atoi(ev);   // development A/B only
   return p.d >= min_d && p.d <= 16384 && p.b <= 400 && (int64_t)p.d * 15 * p.b < ((int64_t)1 << 27) &&
          p.rows < ((int64_t)1 << 32);
@@ -2443,13 +2444,14 @@ static int greedy_two_pass(Params p, cudaStream_t s, int nw_exact) {
     if (e != cudaSuccess) { rc = cuda_fail(e, "cudaMemsetAsync"); break; }
     c.list = 0;
     if (table_walk_applies(p)) {
-      const size_t tb = TableSlice::bytes(p.b);
-      int nwt = 4, bestt = 0;
-      for (int w = 4; w >= 1; w >>= 1) {
-        const int per_sm = (int)((227 * 1024) / ((size_t)w * tb + 1024)) * w;
-        if (per_sm > bestt) { bestt = per_sm; nwt = w; }
-      }
-      rc = launch_persistent(k_greedy_table, nwt * tb, (c.rows + nwt - 1) / nwt, c, s, "k_greedy_table", 32 * nwt);
+      // one block per row, the table in its shared memory (4 blocks per SM at b = 200)
+      int nt = 128;   // (256 threads per row measured slower at every d: 3 blocks per SM)
+      if (const char* ev = getenv("EQ4_DEV_TABLE_NT")) nt = atoi(ev) == 256 ? 256 : 128;   // development A/B only
+      c.tb_wave = sm_count();
+      if (nt == 256)
+        rc = launch_persistent(k_greedy_table<256>, TableSlice::bytes(p.b, 256), c.rows, c, s, "k_greedy_table", 256);
+      else
+        rc = launch_persistent(k_greedy_table<128>, TableSlice::bytes(p.b, 128), c.rows, c, s, "k_greedy_table", 128);
     } else {
       rc = launch_persistent(k_greedy_fast<LPR, E>, nwf * F::bytes(p.stride),
                              (c.rows + F::RPW * nwf - 1) / (F::RPW * nwf), c, s, "k_greedy_fast", 32 * nwf);
