@@ -2445,13 +2445,9 @@ static int greedy_two_pass(Params p, cudaStream_t s, int nw_exact) {
     c.list = 0;
     if (table_walk_applies(p)) {
       // one block per row, the table in its shared memory (4 blocks per SM at b = 200)
-      int nt = 128;   // (256 threads per row measured slower at every d: 3 blocks per SM)
-      if (const char* ev = getenv("EQ4_DEV_TABLE_NT")) nt = atoi(ev) == 256 ? 256 : 128;   // development A/B only
+      // 128 threads per row (256 measured slower at every d: 3 blocks per SM)
       c.tb_wave = sm_count();
-      if (nt == 256)
-        rc = launch_persistent(k_greedy_table<256>, TableSlice::bytes(p.b, 256), c.rows, c, s, "k_greedy_table", 256);
-      else
-        rc = launch_persistent(k_greedy_table<128>, TableSlice::bytes(p.b, 128), c.rows, c, s, "k_greedy_table", 128);
+      rc = launch_persistent(k_greedy_table<128>, TableSlice::bytes(p.b, 128), c.rows, c, s, "k_greedy_table", 128);
     } else {
       rc = launch_persistent(k_greedy_fast<LPR, E>, nwf * F::bytes(p.stride),
                              (c.rows + F::RPW * nwf - 1) / (F::RPW * nwf), c, s, "k_greedy_fast", 32 * nwf);

@@ -54,6 +54,7 @@ struct TableScratch {
   unsigned long long tw[8];
   int res[8];   // nl, nr, bi, bj, defer, checkpoint it / nl / (bi | bj << 16)
   float cpL;
+  int q;        // next item of the codes / range queue
 };
 
 struct TableSlice {
@@ -121,33 +122,86 @@ __global__ void __launch_bounds__(NT) k_greedy_table(const Params p) {
 #else
 #define TBP(i) do {} while (0)
 #endif
-  for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
-    const float4* src = reinterpret_cast<const float4*>(p.x + row * p.ld);
-    // ---- clear the table; range and finiteness (clipping.py:163-165) ----
-    for (int i = tid; i < L * NT; i += NT) tab[i] = 0ull;
-    float mn = INFINITY, mx = -INFINITY, sm = 0.f;
-#pragma unroll 4
-    for (int i = tid; i < d4; i += NT) {
-      const float4 t = __ldg(src + i);
-      mn = fminf(mn, fminf(fminf(t.x, t.y), fminf(t.z, t.w)));
-      mx = fmaxf(mx, fmaxf(fmaxf(t.x, t.y), fmaxf(t.z, t.w)));
-      sm = __fadd_rn(sm, __fadd_rn(__fadd_rn(t.x, t.y), __fadd_rn(t.z, t.w)));
+  // Rows are pipelined through the block: while one warp walks row r (the only phase that is a
+  // chain of dependent steps), the others write the codes of row r - 1 and take the range of row
+  // r + 1 -- neither touches the table -- from a queue of 128-float4 items; the walking warp
+  // joins the queue when its walk is done.
+  const int nit = (d4 + 127) >> 7;   // queue items per row pass
+  auto range_item = [&](const float4* src, int item, float& mn, float& mx, float& sm) {
+    float4 t[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = (item * 4 + k) * 32 + lane;
+      t[k] = i < d4 ? __ldg(src + i) : make_float4(INFINITY, -INFINITY, 0.f, 0.f);
     }
-    mn = group_min<32>(mn);
-    mx = group_max<32>(mx);
-    sm = group_sum<32>(sm);
-    if (lane == 0) { sc->mn[warp] = mn; sc->mx[warp] = mx; sc->sm[warp] = sm; }
-    TBP(0);
-    __syncthreads();
-    TBP(1);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = (item * 4 + k) * 32 + lane;
+      if (i < d4) {
+        mn = fminf(mn, fminf(fminf(t[k].x, t[k].y), fminf(t[k].z, t[k].w)));
+        mx = fmaxf(mx, fmaxf(fmaxf(t[k].x, t[k].y), fmaxf(t[k].z, t[k].w)));
+        sm = __fadd_rn(sm, __fadd_rn(__fadd_rn(t[k].x, t[k].y), __fadd_rn(t[k].z, t[k].w)));
+      }
+    }
+  };
+  auto emit_item = [&](const float4* src, uint8_t* orow, const CodeParams& cp, int item, bool& any_exact) {
+    float4 t[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = (item * 4 + k) * 32 + lane;
+      t[k] = i < d4 ? __ldg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = (item * 4 + k) * 32 + lane;
+      bool n0, n1, n2, n3;
+      unsigned c0 = code_of(t[k].x, cp, n0), c1 = code_of(t[k].y, cp, n1);
+      unsigned c2 = code_of(t[k].z, cp, n2), c3 = code_of(t[k].w, cp, n3);
+      if ((n0 | n1 | n2 | n3) && i < d4) {   // rare: numpy's float64 codec for an element next to a boundary
+        if (n0) c0 = code_exact(t[k].x, cp);
+        if (n1) c1 = code_exact(t[k].y, cp);
+        if (n2) c2 = code_exact(t[k].z, cp);
+        if (n3) c3 = code_exact(t[k].w, cp);
+        any_exact = true;
+      }
+      if (i < d4) *reinterpret_cast<uint16_t*>(orow + 2 * i) = (uint16_t)(c0 | (c1 << 4) | (c2 << 8) | (c3 << 12));
+    }
+  };
+  // block-wide range from the warps' partial values in the scratch (after a barrier)
+  auto block_range = [&](float& mn, float& mx, float& sm) {
+    mn = INFINITY; mx = -INFINITY; sm = 0.f;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
       mn = fminf(mn, sc->mn[w]);
       mx = fmaxf(mx, sc->mx[w]);
+      sm = __fadd_rn(sm, sc->sm[w]);
     }
-    sm = 0.f;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) sm = __fadd_rn(sm, sc->sm[w]);
+  };
+
+  float mn, mx, sm;
+  {   // prologue: the first row's range (clipping.py:163-165)
+    float wmn = INFINITY, wmx = -INFINITY, wsm = 0.f;
+    if ((int64_t)blockIdx.x < p.rows) {
+      const float4* src = reinterpret_cast<const float4*>(p.x + (int64_t)blockIdx.x * p.ld);
+      for (int item = warp; item < nit; item += NW) range_item(src, item, wmn, wmx, wsm);
+    }
+    wmn = group_min<32>(wmn); wmx = group_max<32>(wmx); wsm = group_sum<32>(wsm);
+    if (lane == 0) { sc->mn[warp] = wmn; sc->mx[warp] = wmx; sc->sm[warp] = wsm; }
+    __syncthreads();
+    block_range(mn, mx, sm);
+  }
+  // the previous row, whose codes are still to be written
+  bool pv = false;
+  int64_t pv_row = 0;
+  double pv_lo = 0.0, pv_hi = 0.0;
+
+  for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+    const float4* src = reinterpret_cast<const float4*>(p.x + row * p.ld);
+    const int64_t nrow = row + gridDim.x;
+    const bool has_next = nrow < p.rows;
+    // ---- clear the table ----
+    for (int i = tid; i < L * NT; i += NT) tab[i] = 0ull;
+    if (tid == 0) sc->q = 0;
     const float M = fmaxf(fabsf(mn), fabsf(mx));
     // rows the table walk does not take (the band's premises; numpy's signed-zero choice)
     const bool skip = !isfinite(sm) || mn == 0.f || mx == 0.f || !(mn < mx) || !(M <= 1e6f * (mx - mn));
@@ -155,6 +209,9 @@ __global__ void __launch_bounds__(NT) k_greedy_table(const Params p) {
     const double step = __ddiv_rn(__dsub_rn(x1, x0), (double)p.b);                    // clipping.py:172
     bool defer = skip;
     int nl = 0, nr = 0, bi = 0, bj = 0;
+    TBP(0);
+    __syncthreads();   // the table is clear; the scratch of the last row has been read
+    TBP(1);
     if (!skip) {
       // ---- histogram: bin = floor(2 y), offset sums with carries, exact P1 ----
       const double kY = __ddiv_rn(15.0, step);
@@ -369,47 +426,45 @@ __global__ void __launch_bounds__(NT) k_greedy_table(const Params p) {
           sc->res[5] = cp_it; sc->res[6] = cp_nl; sc->res[7] = cp_bi | (cp_bj << 16);
           sc->cpL = cp_L;
         }
-      } else {
-        // the next row towards L2 while this one is walked
-        const int64_t nrow = row + gridDim.x;
-        if (nrow < p.rows) {
-          const char* np = reinterpret_cast<const char*>(p.x + nrow * p.ld);
-          const int w = warp - (warp > walker);
-          for (int o = (w * 32 + lane) * 128; o < p.d * 4; o += (NT - 32) * 128)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(np + o));
-        }
+        TBP(4);
       }
-      TBP(4);
-      __syncthreads();
-      TBP(1);
+    }
+    // ---- the queue: codes of the previous row, then the range of the next one ----
+    bool any_exact = false;
+    {
+      float wmn = INFINITY, wmx = -INFINITY, wsm = 0.f;
+      const int n_emit = pv ? nit : 0, n_items = n_emit + (has_next ? nit : 0);
+      const float4* psrc = reinterpret_cast<const float4*>(p.x + pv_row * p.ld);
+      const float4* nsrc = reinterpret_cast<const float4*>(p.x + (has_next ? nrow : row) * p.ld);
+      uint8_t* porow = p.packed + (size_t)pv_row * p.stride;
+      CodeParams cp;
+      if (pv) cp = make_code_params(pv_lo, pv_hi);
+      for (;;) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(&sc->q, 1);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= n_items) break;
+        if (item < n_emit) emit_item(psrc, porow, cp, item, any_exact);
+        else range_item(nsrc, item - n_emit, wmn, wmx, wsm);
+      }
+      wmn = group_min<32>(wmn); wmx = group_max<32>(wmx); wsm = group_sum<32>(wsm);
+      if (lane == 0) { sc->mn[warp] = wmn; sc->mx[warp] = wmx; sc->sm[warp] = wsm; }
+    }
+    TBP(5);
+    nexact += __syncthreads_or(any_exact) ? 1u : 0u;
+    TBP(1);
+    block_range(mn, mx, sm);   // the next row's
+    if (!skip) {
       nl = sc->res[0]; nr = sc->res[1]; bi = sc->res[2]; bj = sc->res[3]; defer = sc->res[4] != 0;
     }
+    pv = !defer;
     if (!defer) {
-      // ---- result, codes (uniform.py:77-79), pack ----
+      // ---- result (the codes follow from the queue of the next round) ----
       const double lo = (bi == 0 && bj == 0) ? x0 : __dadd_rn(x0, __dmul_rn((double)bi, step));   // :175,182
       const double hi = bj == 0 ? x1 : __dsub_rn(x1, __dmul_rn((double)bj, step));
-      const CodeParams cp = make_code_params(lo, hi);
-      uint8_t* orow = p.packed + (size_t)row * p.stride;
-      bool any_exact = false;
-#pragma unroll 4
-      for (int i = tid; i < d4; i += NT) {
-        const float4 t = __ldg(src + i);
-        bool n0, n1, n2, n3;
-        unsigned c0 = code_of(t.x, cp, n0), c1 = code_of(t.y, cp, n1);
-        unsigned c2 = code_of(t.z, cp, n2), c3 = code_of(t.w, cp, n3);
-        if (n0 | n1 | n2 | n3) {   // rare: numpy's float64 codec for an element next to a boundary
-          if (n0) c0 = code_exact(t.x, cp);
-          if (n1) c1 = code_exact(t.y, cp);
-          if (n2) c2 = code_exact(t.z, cp);
-          if (n3) c3 = code_exact(t.w, cp);
-          any_exact = true;
-        }
-        *reinterpret_cast<uint16_t*>(orow + 2 * i) = (uint16_t)(c0 | (c1 << 4) | (c2 << 8) | (c3 << 12));
-      }
-      TBP(5);
-      nexact += __syncthreads_or(any_exact) ? 1u : 0u;
-      TBP(1);
+      pv_row = row; pv_lo = lo; pv_hi = hi;
       if (tid == 0) {
+        uint8_t* orow = p.packed + (size_t)row * p.stride;
         const double scl = div15(__dsub_rn(hi, lo));                                  // uniform.py:74-80
         uint8_t* a = orow + p.half;
         if (p.aux == EQ4_AUX_FP16) {
@@ -427,31 +482,39 @@ __global__ void __launch_bounds__(NT) k_greedy_table(const Params p) {
         if (p.info0) p.info0[row] = nl + nr;
         if (p.info1) p.info1[row] = p.b > 65535 ? bi : ((bi << 16) | bj);
       }
-    } else {
-      if (tid == 0) {
-        // deferred: a resume record when the walk passed a checkpoint, else the restart list
-        bool stored = false;
-        const int cp_it = skip ? 0 : sc->res[5];
-        if (p.drec && cp_it > 0) {
-          const int k = cp_it >> 3;
-          const int slot = atomicAdd(&p.drec_count[k], 1);
-          if (slot < p.drec_cap) {
-            const unsigned bb = (unsigned)sc->res[7];
-            p.drec[(size_t)k * p.drec_cap + slot] =
-                make_uint4((unsigned)row, (unsigned)sc->res[6] | ((bb & 0xFFFFu) << 16), bb >> 16,
-                           __float_as_uint(sc->cpL));
-            stored = true;
-          }
+    } else if (tid == 0) {
+      // deferred: a resume record when the walk passed a checkpoint, else the restart list
+      bool stored = false;
+      const int cp_it = skip ? 0 : sc->res[5];
+      if (p.drec && cp_it > 0) {
+        const int k = cp_it >> 3;
+        const int slot = atomicAdd(&p.drec_count[k], 1);
+        if (slot < p.drec_cap) {
+          const unsigned bb = (unsigned)sc->res[7];
+          p.drec[(size_t)k * p.drec_cap + slot] =
+              make_uint4((unsigned)row, (unsigned)sc->res[6] | ((bb & 0xFFFFu) << 16), bb >> 16,
+                         __float_as_uint(sc->cpL));
+          stored = true;
         }
-        if (!stored) p.dlist[(unsigned)atomicAdd(p.dcount, 1)] = (uint32_t)row;
-        ++ndefer;
       }
-      __syncthreads();   // the scratch is read above; the next row rewrites it
+      if (!stored) p.dlist[(unsigned)atomicAdd(p.dcount, 1)] = (uint32_t)row;
+      ++ndefer;
     }
+  }
+  // epilogue: the last row's codes
+  {
+    bool any_exact = false;
+    if (pv) {
+      const CodeParams cp = make_code_params(pv_lo, pv_hi);
+      const float4* psrc = reinterpret_cast<const float4*>(p.x + pv_row * p.ld);
+      uint8_t* porow = p.packed + (size_t)pv_row * p.stride;
+      for (int item = warp; item < nit; item += NW) emit_item(psrc, porow, cp, item, any_exact);
+    }
+    nexact += __syncthreads_or(any_exact) ? 1u : 0u;
   }
 #ifdef TB_PROF
   if (blockIdx.x == 0 && tid == walker * 32)
-    printf("TB_PROF cycles: range %lld barrier-waits %lld hist %lld scan %lld walk %lld emit %lld\n", tp[0], tp[1], tp[2],
+    printf("TB_PROF cycles: clear %lld barrier-waits %lld hist %lld scan %lld walk %lld queue %lld\n", tp[0], tp[1], tp[2],
            tp[3], tp[4], tp[5]);
 #endif
   if (tid == 0) {
