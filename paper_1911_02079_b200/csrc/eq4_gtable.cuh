@@ -257,27 +257,38 @@ __global__ void __launch_bounds__(NT) k_greedy_table(const Params p) {
           xl += ((unsigned long long)(cl + (e.y & 0x1FFFFu)) << 32) + e.x;
           cl += e.y >> 17;
         }
-        unsigned cin = cl;   // counts in this warp's lanes from this one up
+        // suffix sums over the threads above, within the warp first and with ONE block barrier:
+        // counts (cin) and chi (xin).  A thread's chunk adds tl = xl + cin_total * L half-units
+        // to everything below it; cin_total = (counts above in the warp) + (counts of the warps
+        // above, Ca, known only after the barrier), so the warp-level sums are taken with Ca = 0
+        // and the Ca terms -- (lanes above in the warp) * Ca * L -- are added afterwards.
+        unsigned cin = cl;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const unsigned v = __shfl_down_sync(FULL, cin, o);
           if (lane + o < 32) cin += v;
         }
-        if (lane == 0) sc->cw[warp] = cin;
-        __syncthreads();
-        cin -= cl;
-        for (int w = warp + 1; w < NW; ++w) cin += sc->cw[w];   // counts in the threads above
-        const unsigned long long tl = xl + ((unsigned long long)(cin * (unsigned)L) << 32);
-        unsigned long long xin = tl;   // chi entering this thread's chunk from above
+        const unsigned cw = __shfl_sync(FULL, cin, 0);   // this warp's count
+        cin -= cl;                                       // counts above, inside the warp
+        const unsigned long long tl0 = xl + ((unsigned long long)(cin * (unsigned)L) << 32);
+        unsigned long long xin = tl0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const unsigned long long v = shfl_down_u64(xin, o);
           if (lane + o < 32) xin += v;
         }
-        if (lane == 0) sc->tw[warp] = xin;
+        if (lane == 0) { sc->cw[warp] = cw; sc->tw[warp] = xin; }
         __syncthreads();
-        xin -= tl;
-        for (int w = warp + 1; w < NW; ++w) xin += sc->tw[w];
+        xin -= tl0;                                      // chi from the lanes above, Ca = 0
+        unsigned Ca = 0u;                                // counts of the warps above
+        unsigned long long Xa = 0ull;                    // chi entering this warp from above
+        for (int w = NW - 1; w > warp; --w) {
+          // warp w as a whole: its Ca = 0 total plus 32 chunks of L bins under the counts above it
+          Xa += sc->tw[w] + ((unsigned long long)(Ca * (unsigned)(32 * L)) << 32);
+          Ca += sc->cw[w];
+        }
+        xin += Xa + ((unsigned long long)(Ca * (unsigned)((31 - lane) * L)) << 32);
+        cin += Ca;
 #pragma unroll 8
         for (int t = L - 1; t >= 0; --t) {
           const uint2 e = *reinterpret_cast<const uint2*>(mine + t);
