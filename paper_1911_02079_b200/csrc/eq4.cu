@@ -132,6 +132,7 @@ struct Params {
   // with mr = max(1, max|x| / (max - min)) of the row
   double tb_eps, tb_c1a, tb_c1b, tb_c0;
   int tb_wave;   // blocks per grid wave (the SM count): picks each block's walking warp
+  int tb_defer_at;   // tests: the table walk defers every row at this iteration (-1: off)
 };
 constexpr int RG_GROUPS = 8;   // checkpoints at iterations 8, 16, ..., 56
 
@@ -2447,6 +2448,8 @@ static int greedy_two_pass(Params p, cudaStream_t s, int nw_exact) {
       // one block per row, the table in its shared memory (4 blocks per SM at b = 200)
       // 128 threads per row (256 measured slower at every d: 3 blocks per SM)
       c.tb_wave = sm_count();
+      c.tb_defer_at = -1;
+      if (const char* ev = getenv("EQ4_DEV_TABLE_DEFER_AT")) c.tb_defer_at = atoi(ev);   // tests: resume records
       rc = launch_persistent(k_greedy_table<128>, TableSlice::bytes(p.b, 128), c.rows, c, s, "k_greedy_table", 128);
     } else {
       rc = launch_persistent(k_greedy_fast<LPR, E>, nwf * F::bytes(p.stride),

@@ -387,7 +387,9 @@ __global__ void __launch_bounds__(NT) k_greedy_table(const Params p) {
             exitl = !(lhs < rhs);
           }
           // widths below 1 (the exact kernel walks on) and comparisons inside the band
-          const bool deferl = (p.b - itl - 1 < 1) || ((NLR >> mypos) & 1u) || fabs(candl - before) <= bandl;
+          // (tb_defer_at: development / tests -- hand every row over at that iteration)
+          const bool deferl = (p.b - itl - 1 < 1) || ((NLR >> mypos) & 1u) || fabs(candl - before) <= bandl ||
+                              itl == p.tb_defer_at;
           const unsigned E = __ballot_sync(FULL, lvl && exitl) & KM;
           const unsigned D = __ballot_sync(FULL, lvl && deferl) & KM;
           const unsigned I = __ballot_sync(FULL, improved) & KM;

@@ -128,3 +128,18 @@ def test_table_walk_nonfinite_row_reported():
     x[17, 500] = np.nan
     with pytest.raises(ValueError):
         eq.quantize_pack_table4(torch.from_numpy(x).cuda(), "greedy", "fp16", 200, 0.16)
+
+
+@pytest.mark.parametrize("at", [0, 1, 5, 7, 8, 9, 12, 15, 16, 17, 23, 24, 29, 31])
+def test_table_walk_hand_over_at_every_iteration(at):
+    """The walk settles six iterations per round and records its checkpoint (iteration 8k) from
+    inside a round: hand every row over to the exact kernel at iteration `at` (development
+    switch) -- restart list below iteration 8, resume records above -- and compare with the
+    oracle.  Exercises the checkpoint taken at every position of a round."""
+    x = rng.mixed_table(512, 1024, 1000 + at)
+    os.environ["EQ4_DEV_TABLE_DEFER_AT"] = str(at)
+    try:
+        _, _, diag = _check(x, "fp16", min_d=16)
+    finally:
+        os.environ.pop("EQ4_DEV_TABLE_DEFER_AT", None)
+    assert diag["deferred_rows"] == 512, diag
