@@ -36,9 +36,13 @@
 // chain of dependent decisions and runs on one warp, SPECULATIVELY: lane q evaluates one
 // of the 27 candidates the next six iterations can reach (level l = 1..6 has the l + 1
 // candidates with l moves, a of them to the left) with 15 table reads of its own, and the
-// six decisions are then settled one after the other on those values -- 6 iterations per
-// table round trip instead of one.  The row itself is read three times (range; histogram;
-// codes), twice from L2.
+// six decisions are then settled at once: each lane compares its candidate with its neighbour's
+// (two ballots: decision bits, in-band bits), the path through the masks is integer work, and
+// lane = level evaluates the loop test, the band against the running best loss and the
+// checkpoint -- 6 iterations per table round trip instead of one.  Rows are pipelined through
+// the block: while one warp walks row r, the others write the codes of row r - 1 and take the
+// range of row r + 1 (neither touches the table) from a shared-memory work queue.  The row
+// itself is read three times (range; histogram; codes), twice from L2.
 #pragma once
 
 constexpr int TB_K = 6;                          // iterations settled per table round trip
