@@ -1899,6 +1899,17 @@ __device__ __forceinline__ void asym_load(const float* rowp, bool ok, int q, flo
 
 // Code + pack one row slice (E elements of lane q) straight to the packed row
 // in global memory (2-byte stores; L2 merges a row's partial sectors).
+// The winning zero key (np_zero_key) over a whole row, by one lane (rare path of asym_row).
+__device__ __noinline__ unsigned asym_zero_key_row(const float* rowp, int d) {
+  unsigned kz = 0u;
+  for (int i = 0; i < d; i += 4) {
+    const float4 t = *reinterpret_cast<const float4*>(rowp + i);
+    kz = max(max(max(kz, np_zero_key(t.x, i, d)), np_zero_key(t.y, i + 1, d)),
+             max(np_zero_key(t.z, i + 2, d), np_zero_key(t.w, i + 3, d)));
+  }
+  return kz;
+}
+
 template <int LPR, int E, int RM>
 __device__ __forceinline__ void asym_row(const Params& p, const float4 (&cur)[E / 4], int64_t row,
                                          int q) {
@@ -1914,16 +1925,6 @@ __device__ __forceinline__ void asym_row(const Params& p, const float4 (&cur)[E 
   mn = group_min<LPR>(mn);
   mx = group_max<LPR>(mx);
   sm = group_sum<LPR>(sm);
-  if (__any_sync(FULL, rvalid && (mn == 0.f || mx == 0.f))) {   // rare: numpy's signed-zero choice
-    unsigned kz = 0u;
-#pragma unroll
-    for (int c = 0; c < E / 4; ++c) {
-      const int p0 = 4 * (q + LPR * c);
-      kz = max(max(max(kz, np_zero_key(cur[c].x, p0, p.d)), np_zero_key(cur[c].y, p0 + 1, p.d)),
-               max(np_zero_key(cur[c].z, p0 + 2, p.d), np_zero_key(cur[c].w, p0 + 3, p.d)));
-    }
-    np_zero_apply(group_umax<LPR>(kz), mn, mx);
-  }
   bool bad = false;
   if (__any_sync(FULL, !isfinite(sm) && rvalid)) {
     bool lb = false;
@@ -1983,6 +1984,13 @@ __device__ __forceinline__ void asym_row(const Params& p, const float4 (&cur)[E 
     for (int c = 0; c < E / 4; ++c)
       *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = (uint16_t)(bad ? 0u : w16[c]);
     if (q == 0) {
+      // rare: numpy's signed-zero choice for a zero min / max (np_zero_key).  Only the stored
+      // bias and the reported range carry the sign -- codes and scale do not -- so the row's
+      // first lane settles it here, out of line and from global memory (inline in the main
+      // path, with a warp vote, it cost 4% of the launch).  SYM / TABLE ranges do not use it.
+      if constexpr (RM == 0) {
+        if (mn == 0.f || mx == 0.f) np_zero_apply(asym_zero_key_row(p.x + row * p.ld, p.d), mn, mx);
+      }
       const double sc = (!bad && !degenerate) ? div15(__dsub_rn((double)mx, (double)mn)) : 0.0;
       uint8_t* a = orow + p.half;
       if (p.aux == EQ4_AUX_FP16) {
