@@ -1081,8 +1081,12 @@ __device__ __forceinline__ bool near_over(const Params& p, const float* ysf, int
 // elements in reach of a boundary right away; more than 2 on a side sends the
 // row to the exact re-decision.  Rows one at a time; returns the lane's row's
 // escalation.
+// (out of line: inlined into the screen's iteration it cost 1.9% of the 20M x 64 launch)
+#ifndef NEAR_ESC_INLINE
+#define NEAR_ESC_INLINE __noinline__
+#endif
 template <int LPR, int E, bool VEC>
-__device__ __forceinline__ bool near_escalate(const Params& p, const float* ysf, bool chk, int q, int gw,
+__device__ NEAR_ESC_INLINE bool near_escalate(const Params& p, const float* ysf, bool chk, int q, int gw,
                                               int d, float BL, float W, int bi, int bj, unsigned* wdiag) {
   unsigned bal = __ballot_sync(FULL, chk && q == 0);
   bool esc = false;
@@ -1560,6 +1564,33 @@ struct FastSlice {
 #define GF_MINB 5
 #endif
 
+// k_greedy_fast's emit, rare path: the elements of one lane's slice that lie within nb of a
+// rounding boundary of the winning pair take numpy's float64 codec; their nibbles are patched
+// into the staged packed row (orow_q: the lane's first byte).
+template <int LPR, int E>
+__device__ __noinline__ void fast_emit_patch(const RowFast& R, int bi, int bj, const float* src, const float4* ysl,
+                                             uint8_t* orow_q, float B, float kW, float hh, float nb) {
+  const double lo = (bi == 0 && bj == 0) ? R.x0 : __dadd_rn(R.x0, __dmul_rn((double)bi, R.step));
+  const double hi = bj == 0 ? R.x1 : __dsub_rn(R.x1, __dmul_rn((double)bj, R.step));
+  const CodeParams cp = make_code_params(lo, hi);
+  for (int c = 0; c < E / 4; ++c) {
+    const float4 yv = ysl[c * 32];
+    const float yk[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float sv = sat_fma(__fadd_rn(yk[k], -B), kW, hh);
+      const float mm = __fadd_rn(__fmaf_rd(sv, ALPHA, MAGIC), -MAGIC);
+      const float fr = __fmaf_rn(sv, ALPHA, -mm);
+      if (sv > 0.f && sv < 1.f && fabsf(fr - 0.5f) > 0.5f - nb) {
+        const unsigned cc = code_exact(src[4 * LPR * c + k], cp);
+        uint8_t* by = orow_q + 2 * LPR * c + (k >> 1);
+        const int sh = (k & 1) * 4;
+        *by = (uint8_t)((*by & ~(0xF << sh)) | (cc << sh));
+      }
+    }
+  }
+}
+
 template <int LPR, int E>
 __global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fast(const Params p) {
   using S = FastSlice<LPR, E>;
@@ -1796,29 +1827,9 @@ __global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fa
         if (rvalid) *reinterpret_cast<uint16_t*>(orow + 2 * (q + LPR * c)) = (uint16_t)w;
       }
       // rare (a few % of the rows at d >= 2048): the lane's flagged elements take numpy's
-      // float64 codec (uniform.py:77-79), patched into the staged nibbles
+      // float64 codec (uniform.py:77-79), patched into the staged nibbles (out of line)
       if (__any_sync(FULL, near && ok) && near && ok) {
-        const RowFast& R = rf[gw];
-        const double lo = (bi == 0 && bj == 0) ? R.x0 : __dadd_rn(R.x0, __dmul_rn((double)bi, R.step));
-        const double hi = bj == 0 ? R.x1 : __dsub_rn(R.x1, __dmul_rn((double)bj, R.step));
-        const CodeParams cp = make_code_params(lo, hi);
-        const float* src = xr + 4 * q;
-        for (int c = 0; c < E / 4; ++c) {
-          const float4 yv = ysl[c * 32];
-          const float yk[4] = {yv.x, yv.y, yv.z, yv.w};
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float sv = sat_fma(__fadd_rn(yk[k], -B), kW, hh);
-            const float mm = __fadd_rn(__fmaf_rd(sv, ALPHA, MAGIC), -MAGIC);
-            const float fr = __fmaf_rn(sv, ALPHA, -mm);
-            if (sv > 0.f && sv < 1.f && fabsf(fr - 0.5f) > 0.5f - nb) {
-              const unsigned cc = code_exact(src[4 * LPR * c + k], cp);
-              uint8_t* by = orow + 2 * (q + LPR * c) + (k >> 1);
-              const int sh = (k & 1) * 4;
-              *by = (uint8_t)((*by & ~(0xF << sh)) | (cc << sh));
-            }
-          }
-        }
+        fast_emit_patch<LPR, E>(rf[gw], bi, bj, xr + 4 * q, ysl, orow + 2 * q, B, kW, hh, nb);
         atomicAdd(&wdiag[1], 1u);   // per lane with flagged elements
       }
     }
