@@ -1563,6 +1563,9 @@ struct FastSlice {
 #ifndef GF_MINB
 #define GF_MINB 5
 #endif
+#ifndef GF_MINB_SMALL   // E <= 16 (d <= 16): 72 registers, 7 blocks of 4 warps per SM (d = 16: 4.58 ms at 5, 4.46 at 6, 4.42 at 7)
+#define GF_MINB_SMALL 7
+#endif
 
 // k_greedy_fast's emit, rare path: the elements of one lane's slice that lie within nb of a
 // rounding boundary of the winning pair take numpy's float64 codec; their nibbles are patched
@@ -1592,7 +1595,7 @@ __device__ __noinline__ void fast_emit_patch(const RowFast& R, int bi, int bj, c
 }
 
 template <int LPR, int E>
-__global__ void __launch_bounds__(NTHREADS_G, E <= 32 ? 5 : GF_MINB) k_greedy_fast(const Params p) {
+__global__ void __launch_bounds__(NTHREADS_G, E <= 16 ? GF_MINB_SMALL : (E <= 32 ? 5 : GF_MINB)) k_greedy_fast(const Params p) {
   using S = FastSlice<LPR, E>;
   constexpr int RPW = S::RPW;
   extern __shared__ __align__(16) unsigned char smem[];
