@@ -1081,13 +1081,9 @@ __device__ __forceinline__ bool near_over(const Params& p, const float* ysf, int
 // elements in reach of a boundary right away; more than 2 on a side sends the
 // row to the exact re-decision.  Rows one at a time; returns the lane's row's
 // escalation.
-// (out of line: inlined into the screen's iteration it cost 1.9% of the 20M x 64 launch)
-#ifndef NEAR_ESC_INLINE
-#define NEAR_ESC_INLINE __noinline__
-#endif
 template <int LPR, int E, bool VEC>
-__device__ NEAR_ESC_INLINE bool near_escalate(const Params& p, const float* ysf, bool chk, int q, int gw,
-                                              int d, float BL, float W, int bi, int bj, unsigned* wdiag) {
+__device__ __forceinline__ bool near_escalate_body(const Params& p, const float* ysf, bool chk, int q, int gw,
+                                                   int d, float BL, float W, int bi, int bj, unsigned* wdiag) {
   unsigned bal = __ballot_sync(FULL, chk && q == 0);
   bool esc = false;
   while (bal) {
@@ -1099,6 +1095,19 @@ __device__ NEAR_ESC_INLINE bool near_escalate(const Params& p, const float* ysf,
     if (lg == gw) esc = e;
   }
   return esc;
+}
+// Out of line for rows of one or two lanes (inlined into the screen's unrolled iteration it cost
+// 1.9% of the 20M x 64 launch); inline for wider rows, where the call measured 1% slower.
+template <int LPR, int E, bool VEC>
+__device__ __noinline__ bool near_escalate_call(const Params& p, const float* ysf, bool chk, int q, int gw,
+                                                int d, float BL, float W, int bi, int bj, unsigned* wdiag) {
+  return near_escalate_body<LPR, E, VEC>(p, ysf, chk, q, gw, d, BL, W, bi, bj, wdiag);
+}
+template <int LPR, int E, bool VEC>
+__device__ __forceinline__ bool near_escalate(const Params& p, const float* ysf, bool chk, int q, int gw,
+                                              int d, float BL, float W, int bi, int bj, unsigned* wdiag) {
+  if constexpr (LPR <= 2) return near_escalate_call<LPR, E, VEC>(p, ysf, chk, q, gw, d, BL, W, bi, bj, wdiag);
+  else return near_escalate_body<LPR, E, VEC>(p, ysf, chk, q, gw, d, BL, W, bi, bj, wdiag);
 }
 
 enum : unsigned { F_ACTIVE = 1, F_EXACT_ONLY = 2, F_BEST_EX = 4, F_ERR = 8 };
